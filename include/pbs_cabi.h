@@ -1,0 +1,210 @@
+/*
+ * pbs_cabi.h — C ABI of the B200-native PBS-Attn prefill path.
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (the headers under /root/reference/proj/include/pbs/, header-only C++20 templates in
+ * namespace pbs).  Every entry point below replaces one reference operator;
+ * the citation on each names the function it stands in for.  The signatures
+ * use only plain pointers, sizes and PODs (no torch, no C++ types) so that
+ * ctypes / cgo / JNI / N-API bindings can call them directly.
+ *
+ * Conventions
+ *  - Tensors are head-major [H, N, d] row-major device buffers (the layout of
+ *    a PBST 3-D stack, tensor_io.hpp:23-29, 120-124).  dtype is bf16 or f32.
+ *  - Permutations are int32 with the reference meaning map[new_pos] = old_pos
+ *    (permutation.hpp:19-22), one length-N map per query head.
+ *  - Block masks are uint8 row-major T x T grids (block_selection.hpp:26-81),
+ *    one per query head; T = ceil(N / B).
+ *  - GQA: query head h reads kv head h / (Hq / Hkv).  The reference has no
+ *    GQA (pbs_main.cpp:86-89); with Hq == Hkv every call is the reference's.
+ *  - All device entry points are stream-ordered on `stream` (a cudaStream_t,
+ *    NULL = legacy default stream) and never allocate: callers provide the
+ *    workspace sized by pbs_workspace_size().
+ *  - Status codes mirror pbs::ErrorCode (errors.hpp:11-16) plus PBS_ERR_CUDA.
+ *    pbs_last_error() returns the single-line "E_*: message" text of the
+ *    calling thread's last failure (the CLI's stderr format, README.md:105-111).
+ */
+#ifndef PBS_CABI_H_
+#define PBS_CABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:11-16) ---------------------------------- */
+#define PBS_OK 0
+#define PBS_ERR_CUDA 1       /* CUDA runtime / launch failure (no ref equivalent) */
+#define PBS_ERR_CONFIG 2     /* ConfigError / ShapeError  (errors.hpp:32-40) */
+#define PBS_ERR_IO 3         /* IoError / FormatError     (errors.hpp:42-59) */
+#define PBS_ERR_RESOURCE 4   /* ResourceError             (errors.hpp:61-73) */
+#define PBS_ERR_DEGENERATE 5 /* DegenerateRowError        (errors.hpp:75-89) */
+
+/* ---- enums ------------------------------------------------------------ */
+/* PermutationStrategy, pipeline.hpp:19 */
+enum pbs_strategy {
+  PBS_STRATEGY_NONE = 0,
+  PBS_STRATEGY_KEY_PERMUTE = 1,
+  PBS_STRATEGY_QUERY_PERMUTE = 2,
+  PBS_STRATEGY_BOTH = 3
+};
+
+/* element type of Q/K/V/O buffers */
+enum pbs_dtype { PBS_DTYPE_F32 = 0, PBS_DTYPE_BF16 = 1 };
+
+/* ---- PODs ------------------------------------------------------------- */
+/* PipelineConfig (pipeline.hpp:30-49) + ForcedPolicy (block_selection.hpp:163-166) */
+typedef struct pbs_pipeline_config {
+  int64_t block_size;   /* B >= 1 */
+  int64_t segment_size; /* S == 0 or (S >= B and S % B == 0) */
+  double tau;           /* [0, 1] */
+  int32_t strategy;     /* enum pbs_strategy */
+  int32_t forced_first_block;
+  int32_t forced_diagonal_band;
+  int32_t reserved;
+  double scale; /* 0 => 1/sqrt(d) (attention.hpp:32-34) */
+} pbs_pipeline_config;
+
+/* problem shape (the reference is one head per call; this adds Hq/Hkv) */
+typedef struct pbs_shape {
+  int32_t dtype;        /* enum pbs_dtype */
+  int32_t num_q_heads;  /* Hq */
+  int32_t num_kv_heads; /* Hkv, Hq % Hkv == 0 */
+  int32_t head_dim;     /* d; the tensor-core path needs d == 128 */
+  int64_t seq_len;      /* N (self-attention, N == M, pipeline.hpp:112-113) */
+} pbs_shape;
+
+/* PipelineReport (pipeline.hpp:63-74), aggregated over heads.
+ * density fields are per-head averages; counts are sums over heads. */
+typedef struct pbs_report {
+  double block_density;
+  double causal_density_baseline;
+  double pooled_score_coverage;
+  int64_t selected_blocks;
+  int64_t total_admissible_blocks;
+  /* StageTimings (pipeline.hpp:51-61) in microseconds, from CUDA events */
+  double estimate_us;
+  double permute_us;
+  double select_us;
+  double attention_us;
+  double unpermute_us;
+} pbs_report;
+
+/* ---- library ---------------------------------------------------------- */
+const char* pbs_last_error(void);
+const char* pbs_version(void);
+
+/* Device scratch needed by pbs_attention / the estimate and select stages. */
+size_t pbs_workspace_size(const pbs_shape* shape, const pbs_pipeline_config* cfg);
+
+/* ---- stage 1: importance + permutations -------------------------------- */
+
+/* estimate_key_importance (permutation.hpp:143-178): scores[h][j] = mean over
+ * the last min(B, N) query rows of softmax(scale * q_i K^T)_j, no causal mask.
+ * Bit-exact restatement of the reference's fp32 arithmetic on the
+ * (bf16-upcast) inputs.  scores: f32 [Hq, N]. */
+int pbs_estimate_key_importance(const void* q, const void* k, const pbs_shape* shape,
+                                int64_t block_size, double scale, float* scores,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
+/* build_key_permutation + SegmentedPermutation::flatten + Permutation::inverse
+ * (permutation.hpp:182-201, 118-126, 51-55): per segment a stable descending
+ * argsort of the scores (ties by ascending index); the trailing N mod S keys
+ * map to themselves.  perm, inv: int32 [H, N]; inv may be NULL. */
+int pbs_build_key_permutation(const float* scores, int32_t num_heads, int64_t seq_len,
+                              int64_t segment_size, int32_t* perm, int32_t* inv,
+                              void* stream);
+
+/* build_query_permutation (permutation.hpp:206-275): key-block centroids,
+ * cosine argmax group per query, stable sort by group within each segment.
+ * k may be the already key-permuted K' (strategy both, pipeline.hpp:144-153);
+ * k_heads gives its head count (Hkv for raw K, Hq for a per-q-head K'). */
+int pbs_build_query_permutation(const void* q, const void* k, int32_t k_heads,
+                                const pbs_shape* shape, int64_t block_size,
+                                int64_t segment_size, int32_t* perm, int32_t* inv,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- stage 2: gathers --------------------------------------------------- */
+
+/* apply_rows (permutation.hpp:79-89), batched with a GQA broadcast:
+ * dst[h][i][:] = src[h / (dst_heads / src_heads)][perm[h][i]][:].
+ * perm may be NULL (identity).  Also serves the stage-5 un-permute
+ * (pipeline.hpp:178-180) when called with sigma^{-1}. */
+int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int32_t dst_heads,
+                   int64_t rows, int32_t cols, int32_t dtype, void* dst, void* stream);
+
+/* ---- stage 3: block scores + selection ---------------------------------- */
+
+/* meanpool_block_scores (block_selection.hpp:120-161) under the
+ * segment-band causal mask (build_block_causal_mask, block_selection.hpp:86-97):
+ * scores f32 [Hq, T, T]; entries above the band are 0 (softmax of -inf). */
+int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_shape* shape,
+                              int64_t block_size, int64_t segment_size, double scale,
+                              float* scores, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* select_blocks (block_selection.hpp:171-206): cumulative-tau prefix of the
+ * descending scores (double accumulation), plus forced block 0 and the
+ * diagonal segment band.  mask: uint8 [H, T, T].  kv_idx/kv_cnt (optional):
+ * per (head, query block) the selected key blocks in ascending order,
+ * kv_idx [H, T, T] (row-padded CSR), kv_cnt [H, T]. */
+int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks,
+                      int64_t block_size, int64_t segment_size, double tau,
+                      int32_t forced_first_block, int32_t forced_diagonal_band,
+                      uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, void* stream);
+
+/* ---- stage 4: attention ------------------------------------------------- */
+
+/* attention_block_sparse (attention.hpp:259-310) with the original-position
+ * ElementMask (attention.hpp:41-73): permuted query row i may see permuted key
+ * j iff k_orig[j] <= q_orig[i].  q_orig = sigma, k_orig = pi (NULL = identity).
+ * kv_idx/kv_cnt from pbs_select_blocks (block-level skip, attention.hpp:284-286).
+ * kp/vp hold kv_heads heads (kv_heads == Hq for per-q-head permuted K'/V',
+ * == Hkv for unpermuted shared K/V).  out_rows (optional) scatters output row
+ * i of head h to row out_rows[h][i] -- the fused stage-5 un-permute (pass
+ * sigma).  status (optional, device int32[2]): {degenerate flag, first
+ * degenerate (head * T + query block)}.  out has the dtype of q. */
+int pbs_block_sparse_attention_fwd(const void* qp, const void* kp, const void* vp,
+                                   int32_t kv_heads, const pbs_shape* shape,
+                                   int64_t block_size, double scale, const int32_t* kv_idx,
+                                   const int32_t* kv_cnt, const int32_t* q_orig,
+                                   const int32_t* k_orig, const int32_t* out_rows, void* out,
+                                   int32_t* status, void* stream);
+
+/* The project's dense causal FlashAttention (the comparator; attention_tiled
+ * with causal = true, attention.hpp:314-321).  GQA via kv head h/G. */
+int pbs_dense_causal_attention_fwd(const void* q, const void* k, const void* v,
+                                   const pbs_shape* shape, double scale, void* out,
+                                   void* stream);
+
+/* Read back a status buffer written by the attention kernels; returns
+ * PBS_ERR_DEGENERATE (with "E_DEGENERATE: query block ..." text) if set. */
+int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream);
+
+/* ---- fused pipeline (pbs_attention, pipeline.hpp:107-193) ---------------- */
+
+/* Algorithm 1 end to end for all heads on device buffers.  sigma, pi
+ * (int32 [Hq, N]) and mask (uint8 [Hq, T, T]) are optional outputs.  When
+ * report != NULL the call synchronises `stream` and fills it. */
+int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* shape,
+                  const pbs_pipeline_config* cfg, void* out, int32_t* sigma, int32_t* pi,
+                  uint8_t* mask, void* workspace, size_t workspace_bytes, pbs_report* report,
+                  void* stream);
+
+/* Same, on HOST buffers (the reference-facing call: Matrix<T> in, Matrix<T>
+ * out).  Copies in, runs, copies out, synchronises.  Uses a library-owned
+ * device arena on the current device. */
+int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_shape* shape,
+                       const pbs_pipeline_config* cfg, void* out, int32_t* sigma,
+                       int32_t* pi, uint8_t* mask, pbs_report* report);
+
+/* ---- test hooks ---------------------------------------------------------- */
+/* y[i] = the device port of glibc expf (the reference's std::exp(float)). */
+int pbs_debug_expf(const float* x, float* y, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBS_CABI_H_ */
