@@ -30,6 +30,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define PBS_API __attribute__((visibility("default")))
+#else
+#define PBS_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -93,11 +99,11 @@ typedef struct pbs_report {
 } pbs_report;
 
 /* ---- library ---------------------------------------------------------- */
-const char* pbs_last_error(void);
-const char* pbs_version(void);
+PBS_API const char* pbs_last_error(void);
+PBS_API const char* pbs_version(void);
 
 /* Device scratch needed by pbs_attention / the estimate and select stages. */
-size_t pbs_workspace_size(const pbs_shape* shape, const pbs_pipeline_config* cfg);
+PBS_API size_t pbs_workspace_size(const pbs_shape* shape, const pbs_pipeline_config* cfg);
 
 /* ---- stage 1: importance + permutations -------------------------------- */
 
@@ -105,7 +111,7 @@ size_t pbs_workspace_size(const pbs_shape* shape, const pbs_pipeline_config* cfg
  * the last min(B, N) query rows of softmax(scale * q_i K^T)_j, no causal mask.
  * Bit-exact restatement of the reference's fp32 arithmetic on the
  * (bf16-upcast) inputs.  scores: f32 [Hq, N]. */
-int pbs_estimate_key_importance(const void* q, const void* k, const pbs_shape* shape,
+PBS_API int pbs_estimate_key_importance(const void* q, const void* k, const pbs_shape* shape,
                                 int64_t block_size, double scale, float* scores,
                                 void* workspace, size_t workspace_bytes, void* stream);
 
@@ -113,7 +119,7 @@ int pbs_estimate_key_importance(const void* q, const void* k, const pbs_shape* s
  * (permutation.hpp:182-201, 118-126, 51-55): per segment a stable descending
  * argsort of the scores (ties by ascending index); the trailing N mod S keys
  * map to themselves.  perm, inv: int32 [H, N]; inv may be NULL. */
-int pbs_build_key_permutation(const float* scores, int32_t num_heads, int64_t seq_len,
+PBS_API int pbs_build_key_permutation(const float* scores, int32_t num_heads, int64_t seq_len,
                               int64_t segment_size, int32_t* perm, int32_t* inv,
                               void* stream);
 
@@ -121,7 +127,7 @@ int pbs_build_key_permutation(const float* scores, int32_t num_heads, int64_t se
  * cosine argmax group per query, stable sort by group within each segment.
  * k may be the already key-permuted K' (strategy both, pipeline.hpp:144-153);
  * k_heads gives its head count (Hkv for raw K, Hq for a per-q-head K'). */
-int pbs_build_query_permutation(const void* q, const void* k, int32_t k_heads,
+PBS_API int pbs_build_query_permutation(const void* q, const void* k, int32_t k_heads,
                                 const pbs_shape* shape, int64_t block_size,
                                 int64_t segment_size, int32_t* perm, int32_t* inv,
                                 void* workspace, size_t workspace_bytes, void* stream);
@@ -132,7 +138,7 @@ int pbs_build_query_permutation(const void* q, const void* k, int32_t k_heads,
  * dst[h][i][:] = src[h / (dst_heads / src_heads)][perm[h][i]][:].
  * perm may be NULL (identity).  Also serves the stage-5 un-permute
  * (pipeline.hpp:178-180) when called with sigma^{-1}. */
-int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int32_t dst_heads,
+PBS_API int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int32_t dst_heads,
                    int64_t rows, int32_t cols, int32_t dtype, void* dst, void* stream);
 
 /* ---- stage 3: block scores + selection ---------------------------------- */
@@ -140,7 +146,7 @@ int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int3
 /* meanpool_block_scores (block_selection.hpp:120-161) under the
  * segment-band causal mask (build_block_causal_mask, block_selection.hpp:86-97):
  * scores f32 [Hq, T, T]; entries above the band are 0 (softmax of -inf). */
-int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_shape* shape,
+PBS_API int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_shape* shape,
                               int64_t block_size, int64_t segment_size, double scale,
                               float* scores, void* workspace, size_t workspace_bytes,
                               void* stream);
@@ -150,7 +156,7 @@ int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_shape* s
  * diagonal segment band.  mask: uint8 [H, T, T].  kv_idx/kv_cnt (optional):
  * per (head, query block) the selected key blocks in ascending order,
  * kv_idx [H, T, T] (row-padded CSR), kv_cnt [H, T]. */
-int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks,
+PBS_API int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks,
                       int64_t block_size, int64_t segment_size, double tau,
                       int32_t forced_first_block, int32_t forced_diagonal_band,
                       uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, void* stream);
@@ -166,7 +172,7 @@ int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks
  * i of head h to row out_rows[h][i] -- the fused stage-5 un-permute (pass
  * sigma).  status (optional, device int32[2]): {degenerate flag, first
  * degenerate (head * T + query block)}.  out has the dtype of q. */
-int pbs_block_sparse_attention_fwd(const void* qp, const void* kp, const void* vp,
+PBS_API int pbs_block_sparse_attention_fwd(const void* qp, const void* kp, const void* vp,
                                    int32_t kv_heads, const pbs_shape* shape,
                                    int64_t block_size, double scale, const int32_t* kv_idx,
                                    const int32_t* kv_cnt, const int32_t* q_orig,
@@ -175,20 +181,20 @@ int pbs_block_sparse_attention_fwd(const void* qp, const void* kp, const void* v
 
 /* The project's dense causal FlashAttention (the comparator; attention_tiled
  * with causal = true, attention.hpp:314-321).  GQA via kv head h/G. */
-int pbs_dense_causal_attention_fwd(const void* q, const void* k, const void* v,
+PBS_API int pbs_dense_causal_attention_fwd(const void* q, const void* k, const void* v,
                                    const pbs_shape* shape, double scale, void* out,
                                    void* stream);
 
 /* Read back a status buffer written by the attention kernels; returns
  * PBS_ERR_DEGENERATE (with "E_DEGENERATE: query block ..." text) if set. */
-int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream);
+PBS_API int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream);
 
 /* ---- fused pipeline (pbs_attention, pipeline.hpp:107-193) ---------------- */
 
 /* Algorithm 1 end to end for all heads on device buffers.  sigma, pi
  * (int32 [Hq, N]) and mask (uint8 [Hq, T, T]) are optional outputs.  When
  * report != NULL the call synchronises `stream` and fills it. */
-int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* shape,
+PBS_API int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* shape,
                   const pbs_pipeline_config* cfg, void* out, int32_t* sigma, int32_t* pi,
                   uint8_t* mask, void* workspace, size_t workspace_bytes, pbs_report* report,
                   void* stream);
@@ -196,13 +202,13 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
 /* Same, on HOST buffers (the reference-facing call: Matrix<T> in, Matrix<T>
  * out).  Copies in, runs, copies out, synchronises.  Uses a library-owned
  * device arena on the current device. */
-int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_shape* shape,
+PBS_API int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_shape* shape,
                        const pbs_pipeline_config* cfg, void* out, int32_t* sigma,
                        int32_t* pi, uint8_t* mask, pbs_report* report);
 
 /* ---- test hooks ---------------------------------------------------------- */
 /* y[i] = the device port of glibc expf (the reference's std::exp(float)). */
-int pbs_debug_expf(const float* x, float* y, int64_t n, void* stream);
+PBS_API int pbs_debug_expf(const float* x, float* y, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

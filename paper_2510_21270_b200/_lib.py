@@ -1,0 +1,142 @@
+"""ctypes binding of libpbs_b200.so (the C ABI in include/pbs_cabi.h).
+
+The library is loaded from this package directory (built in-tree by
+paper_2510_21270_b200/build.py).  There is no fallback: if the .so is missing
+or fails to load, importing the op layer raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libpbs_b200.so")
+
+PBS_OK = 0
+PBS_ERR_CUDA = 1
+PBS_ERR_CONFIG = 2
+PBS_ERR_IO = 3
+PBS_ERR_RESOURCE = 4
+PBS_ERR_DEGENERATE = 5
+
+DTYPE_F32 = 0
+DTYPE_BF16 = 1
+
+STRATEGIES = {"none": 0, "key_permute": 1, "query_permute": 2, "both": 3}
+
+# every symbol include/pbs_cabi.h declares
+EXPORTS = [
+    "pbs_last_error", "pbs_version", "pbs_workspace_size", "pbs_estimate_key_importance",
+    "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_apply_rows",
+    "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_block_sparse_attention_fwd",
+    "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
+    "pbs_debug_expf",
+]
+
+
+class Shape(C.Structure):
+    """pbs_shape."""
+
+    _fields_ = [("dtype", C.c_int32), ("num_q_heads", C.c_int32), ("num_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("seq_len", C.c_int64)]
+
+
+class PipelineConfig(C.Structure):
+    """pbs_pipeline_config == PipelineConfig (pipeline.hpp:30-49) + ForcedPolicy."""
+
+    _fields_ = [("block_size", C.c_int64), ("segment_size", C.c_int64), ("tau", C.c_double),
+                ("strategy", C.c_int32), ("forced_first_block", C.c_int32),
+                ("forced_diagonal_band", C.c_int32), ("reserved", C.c_int32), ("scale", C.c_double)]
+
+
+class Report(C.Structure):
+    """pbs_report == PipelineReport (pipeline.hpp:63-74) + StageTimings (51-61)."""
+
+    _fields_ = [("block_density", C.c_double), ("causal_density_baseline", C.c_double),
+                ("pooled_score_coverage", C.c_double), ("selected_blocks", C.c_int64),
+                ("total_admissible_blocks", C.c_int64), ("estimate_us", C.c_double),
+                ("permute_us", C.c_double), ("select_us", C.c_double), ("attention_us", C.c_double),
+                ("unpermute_us", C.c_double)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class PbsError(RuntimeError):
+    """Raised for any non-zero status; `code` mirrors pbs::ErrorCode (errors.hpp:11-16)."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class ConfigError(PbsError):
+    pass
+
+
+class ResourceError(PbsError):
+    pass
+
+
+class DegenerateRowError(PbsError):
+    pass
+
+
+class CudaError(PbsError):
+    pass
+
+
+_ERRORS = {PBS_ERR_CONFIG: ConfigError, PBS_ERR_RESOURCE: ResourceError,
+           PBS_ERR_DEGENERATE: DegenerateRowError, PBS_ERR_CUDA: CudaError}
+
+_lib = None
+
+VP = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+SZ = C.c_size_t
+DBL = C.c_double
+
+_SIGS = {
+    "pbs_last_error": (C.c_char_p, []),
+    "pbs_version": (C.c_char_p, []),
+    "pbs_workspace_size": (SZ, [C.POINTER(Shape), C.POINTER(PipelineConfig)]),
+    "pbs_estimate_key_importance": (C.c_int, [VP, VP, C.POINTER(Shape), I64, DBL, VP, VP, SZ, VP]),
+    "pbs_build_key_permutation": (C.c_int, [VP, I32, I64, I64, VP, VP, VP]),
+    "pbs_build_query_permutation": (C.c_int, [VP, VP, I32, C.POINTER(Shape), I64, I64, VP, VP, VP, SZ, VP]),
+    "pbs_apply_rows": (C.c_int, [VP, VP, I32, I32, I64, I32, I32, VP, VP]),
+    "pbs_meanpool_block_scores": (C.c_int, [VP, VP, C.POINTER(Shape), I64, I64, DBL, VP, VP, SZ, VP]),
+    "pbs_select_blocks": (C.c_int, [VP, I32, I64, I64, I64, DBL, I32, I32, VP, VP, VP, VP]),
+    "pbs_block_sparse_attention_fwd": (C.c_int, [VP, VP, VP, I32, C.POINTER(Shape), I64, DBL, VP, VP, VP, VP,
+                                                 VP, VP, VP, VP]),
+    "pbs_dense_causal_attention_fwd": (C.c_int, [VP, VP, VP, C.POINTER(Shape), DBL, VP, VP]),
+    "pbs_check_status": (C.c_int, [VP, I64, VP]),
+    "pbs_attention": (C.c_int, [VP, VP, VP, C.POINTER(Shape), C.POINTER(PipelineConfig), VP, VP, VP, VP, VP, SZ,
+                                C.POINTER(Report), VP]),
+    "pbs_attention_host": (C.c_int, [VP, VP, VP, C.POINTER(Shape), C.POINTER(PipelineConfig), VP, VP, VP, VP,
+                                     C.POINTER(Report)]),
+    "pbs_debug_expf": (C.c_int, [VP, VP, I64, VP]),
+}
+
+
+def load(path: str = LIB_PATH):
+    """Load libpbs_b200.so (raises if it is missing: there is no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing; build it with `python -m paper_2510_21270_b200.build` "
+                          "(the PBS-Attn path has no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int):
+    if rc != PBS_OK:
+        msg = _lib.pbs_last_error().decode()
+        raise _ERRORS.get(rc, PbsError)(rc, msg)

@@ -1,0 +1,668 @@
+// attn_sm100.cu -- K6/K8: tcgen05/TMEM FlashAttention forward for sm_100a.
+//
+// One kernel serves both the permuted block-sparse attention
+// (attention_block_sparse, attention.hpp:259-310, with the ElementMask of
+// attention.hpp:41-73) and the project's dense causal comparator
+// (attention_tiled with causal = true, attention.hpp:314-321): they differ only
+// in the list of key blocks a query block visits.
+//
+// Tile: B = 128 query rows x 128 keys, d = 128, bf16 in, fp32 accumulate.
+// Persistent CTAs (one per SM) walk (head, query-block) work items, heaviest
+// query blocks first.  Warp roles (192 threads):
+//   warp 0      TMA producer: Q tile once per item, K/V tiles of each selected
+//               key block into a 2-stage ring (cp.async.bulk.tensor, SW128)
+//   warp 1      TMEM owner + MMA issuer: S = Q K^T into one of two TMEM
+//               S buffers (double-buffered so QK^T of block e+1 overlaps the
+//               softmax of block e), then O += P V into the TMEM O buffer
+//   warps 2..5  softmax / correction / epilogue, one thread per query row
+//               (TMEM lane = row): tcgen05.ld of S, block-class masking by
+//               original positions, online softmax in the exp2 domain with
+//               lazy rescaling (only when the running max grows by > 8),
+//               P -> bf16 -> SW128 smem for the PV MMA, and the final
+//               O / l written to row out_rows[i] (the fused un-permute).
+// Block classes follow AdmissibilityIndex::classify (attention.hpp:167-174):
+// per-block [min, max] of original positions; `none` blocks are skipped by
+// every role (an exact no-op, attention.hpp:286), `full` blocks skip the
+// per-element test, `partial` ones compare k_orig[j] <= q_orig[i].
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pbs_b200 {
+namespace {
+
+constexpr int kBM = 128;      // query rows per tile (= block size B)
+constexpr int kBN = 128;      // keys per tile (= block size B)
+constexpr int kD = 128;       // head dim
+constexpr int kStages = 2;    // K/V ring depth
+constexpr int kThreads = 192;
+constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
+constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
+constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | spare
+constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
+
+struct __align__(8) Barriers {
+  uint64_t q_full, q_empty;
+  uint64_t kv_full[kStages], kv_empty[kStages];
+  uint64_t s_full[2], s_free[2];
+  uint64_t p_full, pv_done, o_free;
+  uint32_t tmem_base;
+};
+
+struct SmemLayout {
+  // 1024-byte aligned tiles (SW128 atoms)
+  static constexpr int q = 0;
+  static constexpr int k = q + kTileBytes;
+  static constexpr int v = k + kStages * kTileBytes;
+  static constexpr int p = v + kStages * kTileBytes;
+  static constexpr int korig = p + kTileBytes;                 // int[2][128]
+  static constexpr int bars = korig + 2 * 128 * 4;
+  static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
+};
+
+// ---- PTX wrappers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem]
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                                     \
+  asm volatile(                                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "    \
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"       \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),         \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),   \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),              \
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),              \
+        "=r"(r[30]), "=r"(r[31])                                                                                \
+      : "r"(taddr))
+
+#define TMEM_ST32(taddr, r)                                                                                     \
+  asm volatile(                                                                                                 \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "  \
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"        \
+      ::"r"(taddr),                                                                                             \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),        \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),            \
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),           \
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                        \
+      : "memory")
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// SW128 shared-memory matrix descriptor (sm100: version 1 at bit 46, layout 2 = SWIZZLE_128B)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: f32 accumulate, bf16 A/B, M=128, N=128
+__host__ __device__ constexpr uint32_t make_idesc(uint32_t a_mn_major, uint32_t b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn_major << 15) | (b_mn_major << 16) | ((uint32_t)(kBN >> 3) << 17) |
+         ((uint32_t)(kBM >> 4) << 24);
+}
+
+struct KernelArgs {
+  int hq, kv_heads, group;
+  int64_t n, t;
+  float scale_log2;
+  const int32_t* kv_idx;
+  const int32_t* kv_cnt;
+  const int32_t* q_orig;
+  const int32_t* k_orig;
+  const int32_t* out_rows;
+  const int2* q_mm;  // [hq][t] min/max of q_orig per block (nullptr: identity)
+  const int2* k_mm;  // [hq][t] min/max of k_orig per block
+  int32_t* status;
+  __nv_bfloat16* out;
+  int causal;   // identity element mask when q_orig/k_orig are null
+  int dense;    // dense causal list (kb = 0..qb)
+  int64_t items;
+};
+
+struct Item {
+  int h;
+  int64_t qb;
+};
+
+__device__ __forceinline__ Item item_of(const KernelArgs& a, int64_t idx) {
+  // heaviest query blocks first: qb descending, heads interleaved
+  Item it;
+  it.qb = a.t - 1 - idx / a.hq;
+  it.h = (int)(idx % a.hq);
+  return it;
+}
+
+__device__ __forceinline__ int list_len(const KernelArgs& a, const Item& it) {
+  if (a.dense) return (int)(it.qb + 1);
+  return a.kv_cnt[(int64_t)it.h * a.t + it.qb];
+}
+
+__device__ __forceinline__ int64_t list_at(const KernelArgs& a, const Item& it, int e) {
+  if (a.dense) return e;
+  return a.kv_idx[((int64_t)it.h * a.t + it.qb) * a.t + e];
+}
+
+__device__ __forceinline__ int2 q_range(const KernelArgs& a, const Item& it) {
+  if (a.q_mm) return a.q_mm[(int64_t)it.h * a.t + it.qb];
+  const int64_t lo = it.qb * kBM;
+  return make_int2((int)lo, (int)(min64(a.n, lo + kBM) - 1));
+}
+__device__ __forceinline__ int2 k_range(const KernelArgs& a, const Item& it, int64_t kb) {
+  if (a.k_mm) return a.k_mm[(int64_t)it.h * a.t + kb];
+  const int64_t lo = kb * kBN;
+  return make_int2((int)lo, (int)(min64(a.n, lo + kBN) - 1));
+}
+
+// 0 none, 1 partial, 2 full (AdmissibilityIndex::classify); a ragged key block is
+// treated as partial so that keys past N are masked.
+__device__ __forceinline__ int block_class(const KernelArgs& a, const Item& it, int64_t kb) {
+  const bool masked = a.causal || a.q_orig || a.k_orig;
+  const bool ragged = (kb + 1) * kBN > a.n;
+  if (!masked) return ragged ? 1 : 2;
+  const int2 qr = q_range(a, it), kr = k_range(a, it, kb);
+  if (kr.y <= qr.x) return ragged ? 1 : 2;
+  if (kr.x > qr.y) return 0;
+  return 1;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, const KernelArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  Barriers* bar = reinterpret_cast<Barriers*>(smem + SmemLayout::bars);
+  int* korig_s = reinterpret_cast<int*>(smem + SmemLayout::korig);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar->q_full, 1);
+    mbar_init(&bar->q_empty, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bar->kv_full[s], 1);
+      mbar_init(&bar->kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar->s_full[s], 1);
+      mbar_init(&bar->s_free[s], 128);
+    }
+    mbar_init(&bar->p_full, 128);
+    mbar_init(&bar->pv_done, 1);
+    mbar_init(&bar->o_free, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bar->tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bar->tmem_base;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t q_it = 0, kv_it = 0;
+      for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
+        const Item it = item_of(a, idx);
+        const int kvh = it.h / a.group;
+        mbar_wait(&bar->q_empty, (q_it & 1) ^ 1);
+        mbar_expect_tx(&bar->q_full, kTileBytes);
+        for (int p = 0; p < 2; ++p)
+          tma_load_3d(smem + SmemLayout::q + p * kPanelBytes, &tm_q, &bar->q_full, p * 64, (int)(it.qb * kBM), it.h);
+        ++q_it;
+        const int len = list_len(a, it);
+        for (int e = 0; e < len; ++e) {
+          const int64_t kb = list_at(a, it, e);
+          if (block_class(a, it, kb) == 0) continue;
+          const int s = kv_it % kStages;
+          mbar_wait(&bar->kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
+          mbar_expect_tx(&bar->kv_full[s], 2 * kTileBytes);
+          unsigned char* kd = smem + SmemLayout::k + s * kTileBytes;
+          unsigned char* vd = smem + SmemLayout::v + s * kTileBytes;
+          for (int p = 0; p < 2; ++p) {
+            tma_load_3d(kd + p * kPanelBytes, &tm_k, &bar->kv_full[s], p * 64, (int)(kb * kBN), kvh);
+            tma_load_3d(vd + p * kPanelBytes, &tm_v, &bar->kv_full[s], p * 64, (int)(kb * kBN), kvh);
+          }
+          ++kv_it;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
+    const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major, V MN-major
+    const uint32_t q_base = smem_u32(smem + SmemLayout::q);
+    const uint32_t p_base = smem_u32(smem + SmemLayout::p);
+    uint32_t q_it = 0, kv_it = 0, s_it = 0, pv_it = 0, item_no = 0;
+    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x, ++item_no) {
+      const Item it = item_of(a, idx);
+      const int len = list_len(a, it);
+      mbar_wait(&bar->q_full, q_it & 1);
+      ++q_it;
+      int processed = 0;
+      uint32_t prev_stage = 0;
+      bool have_prev = false;
+      auto issue_pv = [&](uint32_t stage, bool first) {
+        mbar_wait(&bar->p_full, pv_it & 1);
+        if (first) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
+#pragma unroll
+          for (int k = 0; k < kBN / 16; ++k) {
+            // A = P [128 q x 128 kv] K-major SW128: panel k/4, +32 B per 16 keys
+            const uint64_t ad = sdesc(p_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
+            // B = V [128 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
+            const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
+            tc_mma(tmem + kColO, ad, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+          }
+          tc_commit(&bar->pv_done);
+          tc_commit(&bar->kv_empty[stage]);
+        }
+        __syncwarp();
+        ++pv_it;
+      };
+      for (int e = 0; e < len; ++e) {
+        const int64_t kb = list_at(a, it, e);
+        if (block_class(a, it, kb) == 0) continue;
+        const uint32_t stage = kv_it % kStages;
+        mbar_wait(&bar->kv_full[stage], (kv_it / kStages) & 1);
+        const uint32_t sb = s_it & 1;
+        mbar_wait(&bar->s_free[sb], ((s_it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
+            const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
+            tc_mma(tmem + (sb ? kColS1 : kColS0), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
+          }
+          tc_commit(&bar->s_full[sb]);
+        }
+        __syncwarp();
+        ++s_it;
+        ++kv_it;
+        if (have_prev) issue_pv(prev_stage, processed == 1);
+        prev_stage = stage;
+        have_prev = true;
+        ++processed;
+      }
+      // Q is free once every S of this item has been issued and completed
+      if (lane == 0) tc_commit(&bar->q_empty);
+      __syncwarp();
+      if (have_prev) issue_pv(prev_stage, processed == 1);
+    }
+  } else {
+    // ===================== softmax / correction / epilogue =====================
+    const int quad = warp & 3;           // TMEM lane quadrant of this warp
+    const int row = quad * 32 + lane;    // query row within the tile
+    const int sm_tid = threadIdx.x - 64;  // 0..127
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    unsigned char* p_smem = smem + SmemLayout::p;
+    uint32_t s_it = 0, pv_it = 0, part_it = 0;
+    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
+      const Item it = item_of(a, idx);
+      const int len = list_len(a, it);
+      const int64_t i = it.qb * kBM + row;
+      const bool valid = i < a.n;
+      const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
+      float m = -INFINITY;  // running max in the log2 domain
+      float l = 0.0f;
+      int processed = 0;
+      for (int e = 0; e < len; ++e) {
+        const int64_t kb = list_at(a, it, e);
+        const int cls = block_class(a, it, kb);
+        if (cls == 0) continue;
+        // key original positions of a partial block; the buffer alternates per
+        // partial block so that the barrier of the next partial block orders reuse
+        int* ko = korig_s + (part_it & 1) * 128;
+        if (cls == 1) {
+          ++part_it;
+          const int64_t j = kb * kBN + sm_tid;
+          int v = 0x7fffffff;
+          if (j < a.n) v = a.k_orig ? a.k_orig[(int64_t)it.h * a.n + j] : (int)j;
+          if (!(a.causal || a.q_orig || a.k_orig) && j < a.n) v = -1;  // unmasked: only the ragged tail
+          ko[sm_tid] = v;
+          named_bar_sync(1, 128);
+        }
+        const uint32_t sb = s_it & 1;
+        mbar_wait(&bar->s_full[sb], (s_it >> 1) & 1);
+        tc_fence_after();
+        float x[128];
+        {
+          uint32_t r[32];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            TMEM_LD32(tmem + lane_off + (sb ? kColS1 : kColS0) + c * 32, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x[c * 32 + j] = __uint_as_float(r[j]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&bar->s_free[sb]);
+        ++s_it;
+        float bmax = -INFINITY;
+        if (cls == 1) {
+#pragma unroll
+          for (int j = 0; j < 128; ++j) {
+            const bool adm = ko[j] <= qo;
+            x[j] = adm ? x[j] * a.scale_log2 : -INFINITY;
+            bmax = fmaxf(bmax, x[j]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 128; ++j) {
+            x[j] *= a.scale_log2;
+            bmax = fmaxf(bmax, x[j]);
+          }
+        }
+        // online softmax with lazy rescale
+        const float m_new = fmaxf(m, bmax);
+        bool need_rescale = false;
+        float factor = 1.0f;
+        if (m_new != -INFINITY) {
+          if (m == -INFINITY) {
+            m = m_new;  // O rows are still exactly 0 here
+          } else if (m_new > m + 8.0f) {
+            factor = ex2(m - m_new);
+            need_rescale = true;
+            m = m_new;
+          }
+        }
+        // the previous PV must be complete before P is overwritten or O touched
+        if (processed > 0) {
+          mbar_wait(&bar->pv_done, pv_it & 1);
+          ++pv_it;
+        }
+        if (__any_sync(0xffffffffu, need_rescale)) {
+          tc_fence_after();
+          uint32_t r[32];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            TMEM_LD32(tmem + lane_off + kColO + c * 32, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * factor);
+            TMEM_ST32(tmem + lane_off + kColO + c * 32, r);
+          }
+          tmem_wait_st();
+          l *= factor;
+        }
+        float rowsum = 0.0f;
+        const float mm = (m == -INFINITY) ? 0.0f : m;
+#pragma unroll
+        for (int c8 = 0; c8 < 16; ++c8) {
+          uint32_t packed[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float p0 = ex2(x[c8 * 8 + 2 * u] - mm);
+            const float p1 = ex2(x[c8 * 8 + 2 * u + 1] - mm);
+            rowsum += p0 + p1;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            packed[u] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          const int panel = c8 >> 3, chunk = c8 & 7;
+          unsigned char* dst = p_smem + panel * kPanelBytes + row * 128 + ((chunk ^ (row & 7)) << 4);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        }
+        l += rowsum;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&bar->p_full);
+        ++processed;
+      }
+      // ---- epilogue: O / l -> out[out_rows[i]]
+      if (processed > 0) {
+        mbar_wait(&bar->pv_done, pv_it & 1);
+        ++pv_it;
+      }
+      tc_fence_after();
+      const bool degenerate = valid && (processed == 0 || l == 0.0f);
+      if (degenerate && a.status) {
+        a.status[0] = 1;
+        atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
+      }
+      const float inv = (l > 0.0f) ? 1.0f / l : 0.0f;
+      const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
+      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        TMEM_LD32(tmem + lane_off + kColO + c * 32, r);
+        tmem_wait_ld();
+        if (valid && processed > 0) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[u * 8 + 2 * w]) * inv,
+                                                        __uint_as_float(r[u * 8 + 2 * w + 1]) * inv);
+              pk[w] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar->o_free);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// per-block [min, max] of an original-position map (AdmissibilityIndex::build)
+__global__ void block_minmax_kernel(const int32_t* __restrict__ orig, int heads, int64_t n, int64_t t,
+                                    int2* __restrict__ mm) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= (int64_t)heads * t) return;
+  const int64_t h = g / t, b = g % t;
+  const int64_t lo = b * kBM, hi = min64(n, lo + kBM);
+  int mn = 0x7fffffff, mx = -1;
+  for (int64_t p = lo + lane; p < hi; p += 32) {
+    const int v = orig[h * n + p];
+    mn = min(mn, v);
+    mx = max(mx, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) mm[g] = make_int2(mn, mx);
+}
+
+// ---- host side -----------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_map(CUtensorMap* map, const void* base, int heads, int64_t n) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(PBS_ERR_CUDA, "E_CUDA", "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)kD, (cuuint64_t)n, (cuuint64_t)heads};
+  const cuuint64_t strides[2] = {(cuuint64_t)kD * 2, (cuuint64_t)n * kD * 2};
+  const cuuint32_t box[3] = {64, (cuuint32_t)kBM, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PBS_ERR_CUDA, "E_CUDA", "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return PBS_OK;
+}
+
+int g_num_sms = 0;
+
+}  // namespace
+
+bool attention_sm100_supported(const AttnParams& p) {
+  if (p.dtype != PBS_DTYPE_BF16 || p.d != kD || p.block != kBM) return false;
+  if ((uintptr_t)p.q % 16 || (uintptr_t)p.k % 16 || (uintptr_t)p.v % 16 || (uintptr_t)p.out % 16) return false;
+  int dev = 0, major = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return false;
+  if (major != 10) return false;
+  if (getenv("PBS_FORCE_SIMT")) return false;
+  return true;
+}
+
+size_t attention_sm100_workspace_bytes(int hq, int64_t n, int64_t block) {
+  const int64_t t = ceil_div(n, block);
+  return (size_t)2 * hq * t * sizeof(int2) + 256;
+}
+
+int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st) {
+  const int64_t t = ceil_div(p.n, p.block);
+  if (t == 0) return PBS_OK;
+  CUtensorMap mq, mk, mv;
+  if (int rc = make_map(&mq, p.q, p.hq, p.n)) return rc;
+  if (int rc = make_map(&mk, p.k, p.kv_heads, p.n)) return rc;
+  if (int rc = make_map(&mv, p.v, p.kv_heads, p.n)) return rc;
+  KernelArgs a{};
+  a.hq = p.hq;
+  a.kv_heads = p.kv_heads;
+  a.group = p.hq / p.kv_heads;
+  a.n = p.n;
+  a.t = t;
+  a.scale_log2 = p.scale * 1.4426950408889634f;
+  a.kv_idx = p.kv_idx;
+  a.kv_cnt = p.kv_cnt;
+  a.q_orig = p.q_orig;
+  a.k_orig = p.k_orig;
+  a.out_rows = p.out_rows;
+  a.status = p.status;
+  a.out = static_cast<__nv_bfloat16*>(p.out);
+  a.causal = p.causal;
+  a.dense = p.kv_idx == nullptr;
+  if (a.dense && !p.causal) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention without a block list must be causal");
+  a.items = (int64_t)p.hq * t;
+  // block min/max of the original positions (only when a map is given)
+  void* own = nullptr;
+  if (p.q_orig || p.k_orig) {
+    int2* mm = static_cast<int2*>(sched_ws);
+    if (!mm) {
+      PBS_CUDA_CHECK(cudaMallocAsync(&own, attention_sm100_workspace_bytes(p.hq, p.n, p.block), st));
+      mm = static_cast<int2*>(own);
+    }
+    const int64_t rows = (int64_t)p.hq * t;
+    if (p.q_orig) {
+      block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.q_orig, p.hq, p.n, t, mm);
+      a.q_mm = mm;
+    }
+    if (p.k_orig) {
+      block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.k_orig, p.hq, p.n, t, mm + rows);
+      a.k_mm = mm + rows;
+    }
+    PBS_LAUNCH_CHECK("block_minmax_kernel");
+  }
+  static bool attr = false;
+  if (!attr) {
+    PBS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SmemLayout::total));
+    int dev = 0;
+    PBS_CUDA_CHECK(cudaGetDevice(&dev));
+    PBS_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    attr = true;
+  }
+  const int grid = (int)min64(a.items, g_num_sms);
+  attn_sm100_kernel<<<grid, kThreads, SmemLayout::total, st>>>(mq, mk, mv, a);
+  PBS_LAUNCH_CHECK("attn_sm100_kernel");
+  if (own) PBS_CUDA_CHECK(cudaFreeAsync(own, st));
+  return PBS_OK;
+}
+
+}  // namespace pbs_b200

@@ -1,0 +1,528 @@
+// cabi.cu -- the extern "C" boundary (include/pbs_cabi.h) and the fused
+// Algorithm-1 orchestration (pbs_attention, pipeline.hpp:107-193).
+//
+// Host code here only validates, carves the caller's workspace and launches
+// the device stages on the caller's stream; there is no CPU compute path.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pbs_b200 {
+
+namespace {
+thread_local std::string g_err;
+}
+
+void set_error(const char* prefix, const std::string& msg) { g_err = std::string(prefix) + ": " + msg; }
+
+int fail(int code, const char* prefix, const std::string& msg) {
+  set_error(prefix, msg);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  set_error("E_CUDA", std::string(where) + ": " + cudaGetErrorString(e));
+  return PBS_ERR_CUDA;
+}
+
+namespace {
+
+int esize_of(int dtype) { return dtype == PBS_DTYPE_BF16 ? 2 : 4; }
+
+float effective_scale(double scale, int d) {
+  // AttentionConfig::effective_scale (attention.hpp:32-34), cast to float at use
+  return (float)(scale > 0.0 ? scale : 1.0 / sqrt((double)d));
+}
+
+int check_shape(const pbs_shape* s) {
+  if (!s) return fail(PBS_ERR_CONFIG, "E_SHAPE", "null shape");
+  if (s->dtype != PBS_DTYPE_BF16 && s->dtype != PBS_DTYPE_F32)
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "dtype must be bf16 or f32");
+  if (s->num_q_heads <= 0 || s->num_kv_heads <= 0 || s->num_q_heads % s->num_kv_heads != 0)
+    return fail(PBS_ERR_CONFIG, "E_SHAPE", "num_q_heads must be a positive multiple of num_kv_heads");
+  if (s->head_dim <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "head dim must be >= 1");
+  if (s->seq_len <= 0) return fail(PBS_ERR_CONFIG, "E_SHAPE", "pipeline inputs are empty");
+  if (s->seq_len > (int64_t)1 << 30) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "sequence longer than 2^30");
+  return PBS_OK;
+}
+
+// PipelineConfig::validate (pipeline.hpp:39-48)
+int check_cfg(const pbs_pipeline_config* c) {
+  if (!c) return fail(PBS_ERR_CONFIG, "E_CONFIG", "null config");
+  if (c->block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "block size must be >= 1");
+  if (c->segment_size < 0 ||
+      (c->segment_size != 0 && (c->segment_size < c->block_size || c->segment_size % c->block_size != 0)))
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size must be 0 or a multiple of the block size");
+  if (!(c->tau >= 0.0 && c->tau <= 1.0)) return fail(PBS_ERR_CONFIG, "E_CONFIG", "tau must lie in [0, 1]");
+  if (c->strategy < PBS_STRATEGY_NONE || c->strategy > PBS_STRATEGY_BOTH)
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "unknown permutation strategy");
+  if (c->segment_size == 0 && c->strategy != PBS_STRATEGY_NONE)
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size 0 requires strategy none");
+  if (c->scale < 0.0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "scale must be > 0");
+  return PBS_OK;
+}
+
+bool uses_pi(int s) { return s == PBS_STRATEGY_KEY_PERMUTE || s == PBS_STRATEGY_BOTH; }
+bool uses_sigma(int s) { return s == PBS_STRATEGY_QUERY_PERMUTE || s == PBS_STRATEGY_BOTH; }
+
+// workspace carve-up for pbs_attention
+struct Layout {
+  size_t status, imp, scores, pi, pi_inv, sigma, sigma_inv, groups, qperm, kp, vp, qp, qbar, kbar, mask,
+      kv_idx, kv_cnt, row_cov, sched, total;
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout plan(const pbs_shape* s, const pbs_pipeline_config* c) {
+  Layout L{};
+  const int64_t n = s->seq_len, hq = s->num_q_heads, d = s->head_dim, b = c->block_size;
+  const int64_t t = ceil_div(n, b);
+  const size_t es = esize_of(s->dtype);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += al(bytes);
+    return o;
+  };
+  L.status = take(16);
+  L.imp = take(uses_pi(c->strategy) ? importance_workspace_bytes((int)hq, n, b) : 0);
+  L.scores = take(uses_pi(c->strategy) ? (size_t)hq * n * 4 : 0);
+  L.pi = take((size_t)hq * n * 4);
+  L.pi_inv = take(uses_pi(c->strategy) ? (size_t)hq * n * 4 : 0);
+  L.sigma = take((size_t)hq * n * 4);
+  L.sigma_inv = take(uses_sigma(c->strategy) ? (size_t)hq * n * 4 : 0);
+  L.groups = take(uses_sigma(c->strategy) ? (size_t)hq * n * 4 : 0);
+  L.qperm = take(uses_sigma(c->strategy) ? query_perm_workspace_bytes((int)hq, n, (int)d, b) : 0);
+  L.kp = take(uses_pi(c->strategy) ? (size_t)hq * n * d * es : 0);
+  L.vp = take(uses_pi(c->strategy) ? (size_t)hq * n * d * es : 0);
+  L.qp = take(uses_sigma(c->strategy) ? (size_t)hq * n * d * es : 0);
+  L.qbar = take((size_t)hq * t * d * 4);
+  L.kbar = take((size_t)hq * t * d * 4);
+  L.mask = take((size_t)hq * t * t);
+  L.kv_idx = take((size_t)hq * t * t * 4);
+  L.kv_cnt = take((size_t)hq * t * 4);
+  L.row_cov = take((size_t)hq * t * 8);
+  L.sched = take(attention_sm100_workspace_bytes((int)hq, n, b));
+  L.total = off + 256;
+  return L;
+}
+
+struct Timer {
+  bool on;
+  cudaStream_t st;
+  cudaEvent_t ev[6];
+  int k = 0;
+  Timer(bool enabled, cudaStream_t s) : on(enabled), st(s) {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  ~Timer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void mark() {
+    if (on && k < 6) cudaEventRecord(ev[k++], st);
+  }
+  double us(int a) const {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ev[a], ev[a + 1]);
+    return ms * 1000.0;
+  }
+};
+
+int run_attention(const AttnParams& p, void* sched, cudaStream_t st) {
+  if (attention_sm100_supported(p)) return launch_attention_sm100(p, sched, st);
+  return launch_attention_simt(p, st);
+}
+
+}  // namespace
+}  // namespace pbs_b200
+
+using namespace pbs_b200;
+
+extern "C" {
+
+const char* pbs_last_error(void) { return g_err.c_str(); }
+
+const char* pbs_version(void) { return "pbs-b200 0.1 (sm_100a)"; }
+
+size_t pbs_workspace_size(const pbs_shape* shape, const pbs_pipeline_config* cfg) {
+  if (check_shape(shape) || check_cfg(cfg)) return 0;
+  return plan(shape, cfg).total;
+}
+
+int pbs_estimate_key_importance(const void* q, const void* k, const pbs_shape* shape, int64_t block_size,
+                                double scale, float* scores, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  if (int rc = check_shape(shape)) return rc;
+  if (block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "block size must be >= 1");
+  if (scale < 0.0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "scale must be > 0");
+  return launch_importance(q, k, shape->dtype, shape->num_q_heads, shape->num_kv_heads, shape->seq_len,
+                           shape->head_dim, block_size, effective_scale(scale, shape->head_dim), scores, workspace,
+                           workspace_bytes, as_stream(stream));
+}
+
+int pbs_build_key_permutation(const float* scores, int32_t num_heads, int64_t seq_len, int64_t segment_size,
+                              int32_t* perm, int32_t* inv, void* stream) {
+  if (segment_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "build_key_permutation: segment size must be >= 1");
+  if (num_heads <= 0 || seq_len < 0) return fail(PBS_ERR_CONFIG, "E_SHAPE", "bad head count or length");
+  return launch_segmented_sort(scores, 0, num_heads, seq_len, segment_size, perm, inv, as_stream(stream));
+}
+
+int pbs_build_query_permutation(const void* q, const void* k, int32_t k_heads, const pbs_shape* shape,
+                                int64_t block_size, int64_t segment_size, int32_t* perm, int32_t* inv,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_shape(shape)) return rc;
+  if (segment_size <= 0)
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "build_query_permutation: segment size must be >= 1");
+  if (block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "block size must be >= 1");
+  if (k_heads <= 0 || shape->num_q_heads % k_heads != 0)
+    return fail(PBS_ERR_CONFIG, "E_SHAPE", "k_heads must divide num_q_heads");
+  const int64_t n = shape->seq_len;
+  const size_t need = query_perm_workspace_bytes(shape->num_q_heads, n, shape->head_dim, block_size) +
+                      al((size_t)shape->num_q_heads * n * 4);
+  if (workspace_bytes < need) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "query permutation workspace too small");
+  uint32_t* groups = static_cast<uint32_t*>(workspace);
+  void* rest = static_cast<char*>(workspace) + al((size_t)shape->num_q_heads * n * 4);
+  cudaStream_t st = as_stream(stream);
+  if (int rc = launch_query_groups(q, k, shape->dtype, shape->num_q_heads, k_heads, n, shape->head_dim,
+                                   block_size, groups, rest, workspace_bytes - al((size_t)shape->num_q_heads * n * 4),
+                                   st))
+    return rc;
+  return launch_segmented_sort(groups, 1, shape->num_q_heads, n, segment_size, perm, inv, st);
+}
+
+int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int32_t dst_heads, int64_t rows,
+                   int32_t cols, int32_t dtype, void* dst, void* stream) {
+  if (dtype != PBS_DTYPE_BF16 && dtype != PBS_DTYPE_F32) return fail(PBS_ERR_CONFIG, "E_CONFIG", "bad dtype");
+  return launch_apply_rows(perm, src, src_heads, dst_heads, rows, cols, esize_of(dtype), dst, as_stream(stream));
+}
+
+int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_shape* shape, int64_t block_size,
+                              int64_t segment_size, double scale, float* scores, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (int rc = check_shape(shape)) return rc;
+  if (block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "block size must be >= 1");
+  if (segment_size != 0 && (segment_size < block_size || segment_size % block_size != 0))
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size must be 0 or a multiple of the block size");
+  const int64_t n = shape->seq_len, t = ceil_div(n, block_size);
+  const int hq = shape->num_q_heads, d = shape->head_dim;
+  const size_t need = 2 * al((size_t)hq * t * d * 4);
+  if (workspace_bytes < need) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "meanpool workspace too small");
+  float* qbar = static_cast<float*>(workspace);
+  float* kbar = reinterpret_cast<float*>(static_cast<char*>(workspace) + al((size_t)hq * t * d * 4));
+  cudaStream_t st = as_stream(stream);
+  if (int rc = launch_pool(qp, shape->dtype, hq, hq, nullptr, n, d, block_size, qbar, st)) return rc;
+  if (int rc = launch_pool(kp, shape->dtype, shape->num_kv_heads, hq, nullptr, n, d, block_size, kbar, st)) return rc;
+  // selection with tau = 1 but no outputs: only the scores are produced
+  return launch_score_select(qbar, kbar, hq, t, d, block_size, segment_size, effective_scale(scale, d), 1.0, 0, 0,
+                             scores, nullptr, nullptr, nullptr, nullptr, st);
+}
+
+int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks, int64_t block_size,
+                      int64_t segment_size, double tau, int32_t forced_first_block, int32_t forced_diagonal_band,
+                      uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, void* stream) {
+  if (!(tau >= 0.0 && tau <= 1.0)) return fail(PBS_ERR_CONFIG, "E_CONFIG", "tau must lie in [0, 1]");
+  if (block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "block size must be >= 1");
+  if (segment_size != 0 && (segment_size < block_size || segment_size % block_size != 0))
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size must be 0 or a multiple of the block size");
+  return launch_select_from_scores(scores, num_heads, num_blocks, block_size, segment_size, tau, forced_first_block,
+                                   forced_diagonal_band, mask, kv_idx, kv_cnt, as_stream(stream));
+}
+
+int pbs_block_sparse_attention_fwd(const void* qp, const void* kp, const void* vp, int32_t kv_heads,
+                                   const pbs_shape* shape, int64_t block_size, double scale, const int32_t* kv_idx,
+                                   const int32_t* kv_cnt, const int32_t* q_orig, const int32_t* k_orig,
+                                   const int32_t* out_rows, void* out, int32_t* status, void* stream) {
+  if (int rc = check_shape(shape)) return rc;
+  if (block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention: block size must be >= 1");
+  if (kv_heads <= 0 || shape->num_q_heads % kv_heads != 0)
+    return fail(PBS_ERR_CONFIG, "E_SHAPE", "kv_heads must divide num_q_heads");
+  if ((kv_idx == nullptr) != (kv_cnt == nullptr))
+    return fail(PBS_ERR_CONFIG, "E_SHAPE", "kv_idx and kv_cnt must be given together");
+  AttnParams p{};
+  p.q = qp;
+  p.k = kp;
+  p.v = vp;
+  p.out = out;
+  p.dtype = shape->dtype;
+  p.hq = shape->num_q_heads;
+  p.kv_heads = kv_heads;
+  p.d = shape->head_dim;
+  p.n = shape->seq_len;
+  p.block = block_size;
+  p.scale = effective_scale(scale, shape->head_dim);
+  p.kv_idx = kv_idx;
+  p.kv_cnt = kv_cnt;
+  p.q_orig = q_orig;
+  p.k_orig = k_orig;
+  p.out_rows = out_rows;
+  p.status = status;
+  p.causal = 0;
+  return run_attention(p, nullptr, as_stream(stream));
+}
+
+int pbs_dense_causal_attention_fwd(const void* q, const void* k, const void* v, const pbs_shape* shape, double scale,
+                                   void* out, void* stream) {
+  if (int rc = check_shape(shape)) return rc;
+  AttnParams p{};
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.out = out;
+  p.dtype = shape->dtype;
+  p.hq = shape->num_q_heads;
+  p.kv_heads = shape->num_kv_heads;
+  p.d = shape->head_dim;
+  p.n = shape->seq_len;
+  p.block = 128;
+  p.scale = effective_scale(scale, shape->head_dim);
+  p.causal = 1;
+  return run_attention(p, nullptr, as_stream(stream));
+}
+
+int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream) {
+  int32_t h[2] = {0, 0};
+  PBS_CUDA_CHECK(cudaMemcpyAsync(h, status, sizeof h, cudaMemcpyDeviceToHost, as_stream(stream)));
+  PBS_CUDA_CHECK(cudaStreamSynchronize(as_stream(stream)));
+  if (h[0]) {
+    const int64_t qb = num_blocks > 0 ? h[1] % num_blocks : h[1];
+    const int64_t head = num_blocks > 0 ? h[1] / num_blocks : 0;
+    return fail(PBS_ERR_DEGENERATE, "E_DEGENERATE",
+                "query block " + std::to_string(qb) + " (head " + std::to_string(head) +
+                    ") has an empty softmax denominator (all keys masked)");
+  }
+  return PBS_OK;
+}
+
+int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* shape, const pbs_pipeline_config* cfg,
+                  void* out, int32_t* sigma_out, int32_t* pi_out, uint8_t* mask_out, void* workspace,
+                  size_t workspace_bytes, pbs_report* report, void* stream) {
+  if (int rc = check_shape(shape)) return rc;
+  if (int rc = check_cfg(cfg)) return rc;
+  const Layout L = plan(shape, cfg);
+  if (workspace_bytes < L.total || workspace == nullptr)
+    return fail(PBS_ERR_RESOURCE, "E_RESOURCE",
+                "workspace of " + std::to_string(workspace_bytes) + " bytes, need " + std::to_string(L.total));
+  cudaStream_t st = as_stream(stream);
+  char* ws = static_cast<char*>(workspace);
+  auto at = [&](size_t off) { return static_cast<void*>(ws + off); };
+  const int hq = shape->num_q_heads, hkv = shape->num_kv_heads, d = shape->head_dim, dt = shape->dtype;
+  const int64_t n = shape->seq_len, b = cfg->block_size, s = cfg->segment_size, t = ceil_div(n, b);
+  const int es = esize_of(dt);
+  const float scale = effective_scale(cfg->scale, d);
+  const int strategy = cfg->strategy;
+  int32_t* status = static_cast<int32_t*>(at(L.status));
+  int32_t* pi = pi_out ? pi_out : static_cast<int32_t*>(at(L.pi));
+  int32_t* sigma = sigma_out ? sigma_out : static_cast<int32_t*>(at(L.sigma));
+  uint8_t* mask = mask_out ? mask_out : static_cast<uint8_t*>(at(L.mask));
+  int32_t* kv_idx = static_cast<int32_t*>(at(L.kv_idx));
+  int32_t* kv_cnt = static_cast<int32_t*>(at(L.kv_cnt));
+  double* row_cov = static_cast<double*>(at(L.row_cov));
+  const int32_t init_status[2] = {0, 0x7fffffff};
+  PBS_CUDA_CHECK(cudaMemcpyAsync(status, init_status, sizeof init_status, cudaMemcpyHostToDevice, st));
+
+  Timer tm(report != nullptr, st);
+  tm.mark();
+  // ---- stage 1: estimate (pipeline.hpp:129-155)
+  const void* kp = k;
+  int kv_heads = hkv;
+  if (uses_pi(strategy)) {
+    float* scores = static_cast<float*>(at(L.scores));
+    if (int rc = launch_importance(q, k, dt, hq, hkv, n, d, b, scale, scores, at(L.imp),
+                                   importance_workspace_bytes(hq, n, b), st))
+      return rc;
+    if (int rc = launch_segmented_sort(scores, 0, hq, n, s, pi, static_cast<int32_t*>(at(L.pi_inv)), st)) return rc;
+  } else if (pi_out) {
+    if (int rc = launch_identity(pi_out, hq, n, st)) return rc;
+  }
+  if (strategy == PBS_STRATEGY_BOTH) {
+    // keys first; sigma is computed against K' = pi K (pipeline.hpp:144-153)
+    if (int rc = launch_apply_rows(pi, k, hkv, hq, n, d, es, at(L.kp), st)) return rc;
+    kp = at(L.kp);
+    kv_heads = hq;
+  }
+  if (uses_sigma(strategy)) {
+    uint32_t* groups = static_cast<uint32_t*>(at(L.groups));
+    if (int rc = launch_query_groups(q, kp, dt, hq, kv_heads, n, d, b, groups, at(L.qperm),
+                                     query_perm_workspace_bytes(hq, n, d, b), st))
+      return rc;
+    if (int rc = launch_segmented_sort(groups, 1, hq, n, s, sigma, static_cast<int32_t*>(at(L.sigma_inv)), st))
+      return rc;
+  } else if (sigma_out) {
+    if (int rc = launch_identity(sigma_out, hq, n, st)) return rc;
+  }
+  tm.mark();
+  // ---- stage 2: permute (pipeline.hpp:157-165)
+  const void* qp = q;
+  const void* vp = v;
+  if (uses_sigma(strategy)) {
+    if (int rc = launch_apply_rows(sigma, q, hq, hq, n, d, es, at(L.qp), st)) return rc;
+    qp = at(L.qp);
+  }
+  if (strategy == PBS_STRATEGY_KEY_PERMUTE) {
+    if (int rc = launch_apply_rows(pi, k, hkv, hq, n, d, es, at(L.kp), st)) return rc;
+    kp = at(L.kp);
+    kv_heads = hq;
+  }
+  if (uses_pi(strategy)) {
+    if (int rc = launch_apply_rows(pi, v, hkv, hq, n, d, es, at(L.vp), st)) return rc;
+    vp = at(L.vp);
+  }
+  tm.mark();
+  // ---- stage 3: select (pipeline.hpp:167-171)
+  float* qbar = static_cast<float*>(at(L.qbar));
+  float* kbar = static_cast<float*>(at(L.kbar));
+  if (int rc = launch_pool(qp, dt, hq, hq, nullptr, n, d, b, qbar, st)) return rc;
+  if (int rc = launch_pool(kp, dt, kv_heads, hq, nullptr, n, d, b, kbar, st)) return rc;
+  if (int rc = launch_score_select(qbar, kbar, hq, t, d, b, s, scale, cfg->tau, cfg->forced_first_block,
+                                   cfg->forced_diagonal_band, nullptr, mask, kv_idx, kv_cnt, row_cov, st))
+    return rc;
+  tm.mark();
+  // ---- stage 4: attention with the original-position element mask (173-176)
+  AttnParams p{};
+  p.q = qp;
+  p.k = kp;
+  p.v = vp;
+  p.out = out;
+  p.dtype = dt;
+  p.hq = hq;
+  p.kv_heads = kv_heads;
+  p.d = d;
+  p.n = n;
+  p.block = b;
+  p.scale = scale;
+  p.kv_idx = kv_idx;
+  p.kv_cnt = kv_cnt;
+  p.q_orig = uses_sigma(strategy) ? sigma : nullptr;
+  p.k_orig = uses_pi(strategy) ? pi : nullptr;
+  // ---- stage 5 fused: output row i of the permuted grid goes to row sigma[i]
+  p.out_rows = uses_sigma(strategy) ? sigma : nullptr;
+  p.status = status;
+  // ElementMask(sigma, pi) with both identities is exactly the causal mask
+  p.causal = (p.q_orig == nullptr && p.k_orig == nullptr) ? 1 : 0;
+  if (int rc = run_attention(p, at(L.sched), st)) return rc;
+  tm.mark();
+  tm.mark();  // un-permute is fused into the attention epilogue
+  if (!report) return PBS_OK;
+
+  // ---- report (pipeline.hpp:182-191)
+  std::vector<int32_t> cnt((size_t)hq * t);
+  std::vector<double> cov((size_t)hq * t);
+  int32_t hs[2];
+  PBS_CUDA_CHECK(cudaMemcpyAsync(cnt.data(), kv_cnt, cnt.size() * 4, cudaMemcpyDeviceToHost, st));
+  PBS_CUDA_CHECK(cudaMemcpyAsync(cov.data(), row_cov, cov.size() * 8, cudaMemcpyDeviceToHost, st));
+  PBS_CUDA_CHECK(cudaMemcpyAsync(hs, status, sizeof hs, cudaMemcpyDeviceToHost, st));
+  PBS_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (hs[0]) {
+    return fail(PBS_ERR_DEGENERATE, "E_DEGENERATE",
+                "query block " + std::to_string(hs[1] % t) + " (head " + std::to_string(hs[1] / t) +
+                    ") has an empty softmax denominator (all keys masked)");
+  }
+  memset(report, 0, sizeof *report);
+  int64_t adm = 0;
+  for (int64_t i = 0; i < t; ++i) adm += admissible_prefix(i, t, b, s);
+  double dens = 0.0, covsum = 0.0;
+  for (int h = 0; h < hq; ++h) {
+    int64_t sel = 0;
+    double c = 0.0;
+    for (int64_t i = 0; i < t; ++i) {
+      sel += cnt[(size_t)h * t + i];
+      c += cov[(size_t)h * t + i];
+    }
+    report->selected_blocks += sel;
+    dens += (double)sel / (double)(t * t);
+    covsum += c / (double)t;
+  }
+  report->block_density = dens / hq;
+  report->pooled_score_coverage = covsum / hq;
+  report->causal_density_baseline = (double)(t + 1) / (double)(2 * t);
+  report->total_admissible_blocks = adm * hq;
+  report->estimate_us = tm.us(0);
+  report->permute_us = tm.us(1);
+  report->select_us = tm.us(2);
+  report->attention_us = tm.us(3);
+  report->unpermute_us = tm.us(4);
+  return PBS_OK;
+}
+
+// ---- host-buffer entry: library-owned device arena --------------------------
+namespace {
+struct Arena {
+  std::mutex mu;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+};
+Arena g_arena;
+}  // namespace
+
+int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_shape* shape,
+                       const pbs_pipeline_config* cfg, void* out, int32_t* sigma, int32_t* pi, uint8_t* mask,
+                       pbs_report* report) {
+  if (int rc = check_shape(shape)) return rc;
+  if (int rc = check_cfg(cfg)) return rc;
+  const int64_t n = shape->seq_len, hq = shape->num_q_heads, hkv = shape->num_kv_heads, d = shape->head_dim;
+  const int64_t t = ceil_div(n, cfg->block_size);
+  const size_t es = esize_of(shape->dtype);
+  const size_t qb = (size_t)hq * n * d * es, kvb = (size_t)hkv * n * d * es;
+  const size_t ws = pbs_workspace_size(shape, cfg);
+  const size_t need = al(qb) * 2 + al(kvb) * 2 + al((size_t)hq * n * 4) * 2 + al((size_t)hq * t * t) + ws;
+  std::lock_guard<std::mutex> lk(g_arena.mu);
+  int dev = 0;
+  PBS_CUDA_CHECK(cudaGetDevice(&dev));
+  if (g_arena.bytes < need || g_arena.device != dev) {
+    if (g_arena.ptr) cudaFree(g_arena.ptr);
+    g_arena.ptr = nullptr;
+    g_arena.bytes = 0;
+    PBS_CUDA_CHECK(cudaMalloc(&g_arena.ptr, need));
+    g_arena.bytes = need;
+    g_arena.device = dev;
+  }
+  char* base = static_cast<char*>(g_arena.ptr);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base + off;
+    off += al(bytes);
+    return p;
+  };
+  void* dq = take(qb);
+  void* dk = take(kvb);
+  void* dv = take(kvb);
+  void* dout = take(qb);
+  int32_t* dsig = reinterpret_cast<int32_t*>(take((size_t)hq * n * 4));
+  int32_t* dpi = reinterpret_cast<int32_t*>(take((size_t)hq * n * 4));
+  uint8_t* dmask = reinterpret_cast<uint8_t*>(take((size_t)hq * t * t));
+  void* dws = take(ws);
+  cudaStream_t st = 0;
+  PBS_CUDA_CHECK(cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, st));
+  PBS_CUDA_CHECK(cudaMemcpyAsync(dk, k, kvb, cudaMemcpyHostToDevice, st));
+  PBS_CUDA_CHECK(cudaMemcpyAsync(dv, v, kvb, cudaMemcpyHostToDevice, st));
+  pbs_report local{};
+  if (int rc = pbs_attention(dq, dk, dv, shape, cfg, dout, sigma ? dsig : nullptr, pi ? dpi : nullptr,
+                             mask ? dmask : nullptr, dws, ws, &local, st))
+    return rc;
+  PBS_CUDA_CHECK(cudaMemcpyAsync(out, dout, qb, cudaMemcpyDeviceToHost, st));
+  if (sigma) PBS_CUDA_CHECK(cudaMemcpyAsync(sigma, dsig, (size_t)hq * n * 4, cudaMemcpyDeviceToHost, st));
+  if (pi) PBS_CUDA_CHECK(cudaMemcpyAsync(pi, dpi, (size_t)hq * n * 4, cudaMemcpyDeviceToHost, st));
+  if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask, dmask, (size_t)hq * t * t, cudaMemcpyDeviceToHost, st));
+  PBS_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (report) *report = local;
+  return PBS_OK;
+}
+
+int pbs_debug_expf(const float* x, float* y, int64_t n, void* stream) {
+  return launch_debug_expf(x, y, n, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// gather.cu -- K4/K7: apply_rows (permutation.hpp:79-89) batched over heads with
+// the GQA broadcast: dst[h][i][:] = src[h / G][perm[h][i]][:].
+//
+// HBM-bound row copy: algorithmic bytes = 2 * rows * cols * esize per head
+// (read + write).  One warp moves one row with 16-byte vector accesses; a
+// grid of 148 * 16 CTAs strides over all (head, row) pairs.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pbs_b200 {
+namespace {
+
+template <int kVecPerRow>
+__global__ void __launch_bounds__(256) apply_rows_vec_kernel(const int32_t* __restrict__ perm,
+                                                             const int4* __restrict__ src, int group,
+                                                             int64_t rows, int64_t total_rows,
+                                                             int4* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < total_rows; r += nwarps) {
+    const int64_t h = r / rows, i = r % rows;
+    const int64_t s = perm ? perm[r] : i;
+    const int4* sp = src + ((h / group) * rows + s) * kVecPerRow;
+    int4* dp = dst + r * kVecPerRow;
+#pragma unroll
+    for (int v = lane; v < kVecPerRow; v += 32) dp[v] = __ldg(sp + v);
+  }
+}
+
+__global__ void apply_rows_generic_kernel(const int32_t* __restrict__ perm, const char* __restrict__ src,
+                                          int group, int64_t rows, int64_t row_bytes, int64_t total_rows,
+                                          char* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < total_rows; r += nwarps) {
+    const int64_t h = r / rows, i = r % rows;
+    const int64_t s = perm ? perm[r] : i;
+    const char* sp = src + ((h / group) * rows + s) * row_bytes;
+    char* dp = dst + r * row_bytes;
+    for (int64_t b = lane; b < row_bytes; b += 32) dp[b] = sp[b];
+  }
+}
+
+}  // namespace
+
+int launch_apply_rows(const int32_t* perm, const void* src, int src_heads, int dst_heads, int64_t rows,
+                      int cols, int esize, void* dst, cudaStream_t st) {
+  if (rows == 0 || cols == 0 || dst_heads == 0) return PBS_OK;
+  if (src_heads <= 0 || dst_heads % src_heads != 0)
+    return fail(PBS_ERR_CONFIG, "E_SHAPE", "apply_rows: dst heads must be a multiple of src heads");
+  const int group = dst_heads / src_heads;
+  const int64_t total = rows * dst_heads;
+  const int64_t row_bytes = (int64_t)cols * esize;
+  const int blocks = (int)min64(ceil_div(total, 8), 148 * 16);
+  const bool aligned = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  if (aligned && row_bytes == 256) {
+    apply_rows_vec_kernel<16><<<blocks, 256, 0, st>>>(perm, static_cast<const int4*>(src), group, rows, total,
+                                                     static_cast<int4*>(dst));
+  } else if (aligned && row_bytes == 512) {
+    apply_rows_vec_kernel<32><<<blocks, 256, 0, st>>>(perm, static_cast<const int4*>(src), group, rows, total,
+                                                     static_cast<int4*>(dst));
+  } else {
+    apply_rows_generic_kernel<<<blocks, 256, 0, st>>>(perm, static_cast<const char*>(src), group, rows, row_bytes,
+                                                      total, static_cast<char*>(dst));
+  }
+  PBS_LAUNCH_CHECK("apply_rows_kernel");
+  return PBS_OK;
+}
+
+}  // namespace pbs_b200

@@ -1,0 +1,253 @@
+"""Host-side mirror of the reference operator API over device tensors.
+
+Function names, argument meaning and error behaviour follow the reference
+headers (/root/reference/proj/include/pbs/); every call goes through the C
+ABI of libpbs_b200.so (include/pbs_cabi.h) on the current CUDA stream.
+Tensors use the head-major [H, N, d] layout; permutations are int32
+``map[new] = old``; masks uint8 [H, T, T].  PyTorch is only the device-memory
+and stream plumbing here.
+
+    estimate_key_importance   permutation.hpp:143-178
+    build_key_permutation     permutation.hpp:182-201 (+ flatten, inverse)
+    build_query_permutation   permutation.hpp:206-275
+    apply_rows                permutation.hpp:79-89
+    meanpool_block_scores     block_selection.hpp:120-161
+    select_blocks             block_selection.hpp:171-206
+    attention_block_sparse    attention.hpp:259-310
+    dense_causal_attention    attention.hpp:314-321 (causal comparator)
+    pbs_attention             pipeline.hpp:107-193
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import PipelineConfig, Report, Shape, check
+
+_WS: dict = {}
+
+
+def lib():
+    return _lib.load()
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.DTYPE_BF16
+    if t.dtype == torch.float32:
+        return _lib.DTYPE_F32
+    raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, f"E_CONFIG: dtype {t.dtype} (need bfloat16 or float32)")
+
+
+def _check_dev(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: tensors must be contiguous CUDA tensors")
+
+
+def make_shape(q: torch.Tensor, k: torch.Tensor) -> Shape:
+    hq, n, d = q.shape
+    hkv = k.shape[0]
+    return Shape(_dtype_code(q), hq, hkv, d, n)
+
+
+def make_config(block_size=128, segment_size=256, tau=0.9, strategy="key_permute",
+                forced_first_block=True, forced_diagonal_band=True, scale=0.0) -> PipelineConfig:
+    """PipelineConfig defaults of the reference (pipeline.hpp:30-38)."""
+    if isinstance(strategy, str):
+        strategy = _lib.STRATEGIES[strategy]
+    return PipelineConfig(block_size, segment_size, tau, strategy, int(forced_first_block),
+                          int(forced_diagonal_band), 0, scale)
+
+
+def workspace(nbytes: int, device=None) -> torch.Tensor:
+    """A cached device scratch buffer of at least nbytes."""
+    device = torch.device(device or "cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    key = (device.type, device.index)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def estimate_key_importance(q, k, block_size, scale=0.0):
+    """scores [Hq, N] f32 (exact restatement of the reference's fp32 arithmetic)."""
+    _check_dev(q, k)
+    shape = make_shape(q, k)
+    n = q.shape[1]
+    take = min(block_size, n)
+    ws = workspace(q.shape[0] * n * take * 4 + q.shape[0] * take * 8 + 4096, q.device)
+    out = torch.empty(q.shape[0], n, dtype=torch.float32, device=q.device)
+    check(lib().pbs_estimate_key_importance(_ptr(q), _ptr(k), C.byref(shape), block_size, scale, _ptr(out),
+                                            _ptr(ws), ws.numel(), _stream()))
+    return out
+
+
+def build_key_permutation(scores, segment_size, with_inverse=True):
+    """(perm, inv) int32 [H, N]."""
+    _check_dev(scores)
+    h, n = scores.shape
+    perm = torch.empty(h, n, dtype=torch.int32, device=scores.device)
+    inv = torch.empty_like(perm) if with_inverse else None
+    check(lib().pbs_build_key_permutation(_ptr(scores), h, n, segment_size, _ptr(perm), _ptr(inv), _stream()))
+    return perm, inv
+
+
+def build_query_permutation(q, k, block_size, segment_size, with_inverse=True):
+    _check_dev(q, k)
+    shape = make_shape(q, k)
+    hq, n, d = q.shape
+    tc = -(-n // block_size)
+    need = hq * n * 4 + hq * tc * d * 4 + hq * tc * 4 + hq * n * 4 + hq * n * 8 + 8192
+    ws = workspace(need, q.device)
+    perm = torch.empty(hq, n, dtype=torch.int32, device=q.device)
+    inv = torch.empty_like(perm) if with_inverse else None
+    check(lib().pbs_build_query_permutation(_ptr(q), _ptr(k), k.shape[0], C.byref(shape), block_size,
+                                            segment_size, _ptr(perm), _ptr(inv), _ptr(ws), ws.numel(),
+                                            _stream()))
+    return perm, inv
+
+
+def apply_rows(perm, src, dst_heads=None):
+    """dst[h][i] = src[h // G][perm[h][i]] (perm None = identity broadcast)."""
+    _check_dev(perm, src)
+    hs, n, d = src.shape
+    hd = dst_heads or (perm.shape[0] if perm is not None else hs)
+    dst = torch.empty(hd, n, d, dtype=src.dtype, device=src.device)
+    check(lib().pbs_apply_rows(_ptr(perm), _ptr(src), hs, hd, n, d, _dtype_code(src), _ptr(dst), _stream()))
+    return dst
+
+
+def meanpool_block_scores(qp, kp, block_size, segment_size, scale=0.0):
+    """Block scores [Hq, T, T] f32 under the segment-band causal mask."""
+    _check_dev(qp, kp)
+    shape = make_shape(qp, kp)
+    hq, n, d = qp.shape
+    t = -(-n // block_size)
+    ws = workspace(2 * (hq * t * d * 4 + 256) + 4096, qp.device)
+    out = torch.empty(hq, t, t, dtype=torch.float32, device=qp.device)
+    check(lib().pbs_meanpool_block_scores(_ptr(qp), _ptr(kp), C.byref(shape), block_size, segment_size, scale,
+                                          _ptr(out), _ptr(ws), ws.numel(), _stream()))
+    return out
+
+
+def select_blocks(scores, block_size, segment_size, tau, forced_first_block=True, forced_diagonal_band=True):
+    """(mask uint8 [H,T,T], kv_idx int32 [H,T,T], kv_cnt int32 [H,T])."""
+    _check_dev(scores)
+    h, t, _ = scores.shape
+    mask = torch.empty(h, t, t, dtype=torch.uint8, device=scores.device)
+    kv_idx = torch.empty(h, t, t, dtype=torch.int32, device=scores.device)
+    kv_cnt = torch.empty(h, t, dtype=torch.int32, device=scores.device)
+    check(lib().pbs_select_blocks(_ptr(scores), h, t, block_size, segment_size, tau, int(forced_first_block),
+                                  int(forced_diagonal_band), _ptr(mask), _ptr(kv_idx), _ptr(kv_cnt), _stream()))
+    return mask, kv_idx, kv_cnt
+
+
+def attention_block_sparse(qp, kp, vp, block_size, kv_idx, kv_cnt, q_orig=None, k_orig=None, out_rows=None,
+                           scale=0.0, check_status=True):
+    """Permuted block-sparse attention; raises DegenerateRowError like finalize_into."""
+    _check_dev(qp, kp, vp, kv_idx, kv_cnt, q_orig, k_orig, out_rows)
+    shape = make_shape(qp, kp)
+    out = torch.empty_like(qp)
+    status = torch.tensor([0, 0x7FFFFFFF], dtype=torch.int32, device=qp.device)
+    check(lib().pbs_block_sparse_attention_fwd(_ptr(qp), _ptr(kp), _ptr(vp), kp.shape[0], C.byref(shape),
+                                               block_size, scale, _ptr(kv_idx), _ptr(kv_cnt), _ptr(q_orig),
+                                               _ptr(k_orig), _ptr(out_rows), _ptr(out), _ptr(status), _stream()))
+    if check_status:
+        t = -(-qp.shape[1] // block_size)
+        check(lib().pbs_check_status(_ptr(status), t, _stream()))
+    return out
+
+
+def dense_causal_attention(q, k, v, scale=0.0, out=None):
+    """The project's dense causal FlashAttention (GQA: kv head h // G)."""
+    _check_dev(q, k, v)
+    shape = make_shape(q, k)
+    out = torch.empty_like(q) if out is None else out
+    check(lib().pbs_dense_causal_attention_fwd(_ptr(q), _ptr(k), _ptr(v), C.byref(shape), scale, _ptr(out),
+                                               _stream()))
+    return out
+
+
+@dataclass
+class PipelineResult:
+    """PipelineResult (pipeline.hpp:76-83) with per-head device tensors."""
+
+    output: torch.Tensor
+    sigma: torch.Tensor
+    pi: torch.Tensor
+    mask: torch.Tensor
+    report: dict | None
+
+
+def workspace_size(q, k, cfg: PipelineConfig) -> int:
+    shape = make_shape(q, k)
+    return int(lib().pbs_workspace_size(C.byref(shape), C.byref(cfg)))
+
+
+def pbs_attention(q, k, v, cfg: PipelineConfig | None = None, report=True, out=None, return_perms=True,
+                  ws=None):
+    """Algorithm 1 on device tensors q [Hq,N,d], k/v [Hkv,N,d] (pipeline.hpp:107-193).
+
+    With report=True the call synchronises and fills the PipelineReport; with
+    report=False it is fully stream-ordered (graph-capturable)."""
+    cfg = cfg or make_config()
+    _check_dev(q, k, v)
+    shape = make_shape(q, k)
+    hq, n, d = q.shape
+    t = -(-n // max(int(cfg.block_size), 1))
+    need = lib().pbs_workspace_size(C.byref(shape), C.byref(cfg))
+    if need == 0:
+        check(_lib.PBS_ERR_CONFIG)
+    ws = workspace(need, q.device) if ws is None else ws
+    out = torch.empty_like(q) if out is None else out
+    sigma = pi = mask = None
+    if return_perms:
+        sigma = torch.empty(hq, n, dtype=torch.int32, device=q.device)
+        pi = torch.empty(hq, n, dtype=torch.int32, device=q.device)
+        mask = torch.empty(hq, t, t, dtype=torch.uint8, device=q.device)
+    rep = Report() if report else None
+    check(lib().pbs_attention(_ptr(q), _ptr(k), _ptr(v), C.byref(shape), C.byref(cfg), _ptr(out), _ptr(sigma),
+                              _ptr(pi), _ptr(mask), _ptr(ws), ws.numel(), C.byref(rep) if rep else None,
+                              _stream()))
+    return PipelineResult(out, sigma, pi, mask, rep.as_dict() if rep else None)
+
+
+def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=False):
+    """The reference-facing call on HOST (CPU) tensors: copies in, runs, copies out."""
+    cfg = cfg or make_config()
+    for x in (q, k, v):
+        if x.is_cuda or not x.is_contiguous():
+            raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: host tensors must be contiguous CPU tensors")
+    shape = make_shape(q, k)
+    hq, n, d = q.shape
+    t = -(-n // max(int(cfg.block_size), 1))
+    out = torch.empty_like(q)
+    sigma = pi = mask = None
+    if return_perms:
+        sigma = torch.empty(hq, n, dtype=torch.int32)
+        pi = torch.empty(hq, n, dtype=torch.int32)
+        mask = torch.empty(hq, t, t, dtype=torch.uint8)
+    rep = Report()
+    check(lib().pbs_attention_host(_ptr(q), _ptr(k), _ptr(v), C.byref(shape), C.byref(cfg), _ptr(out),
+                                   _ptr(sigma), _ptr(pi), _ptr(mask), C.byref(rep)))
+    return PipelineResult(out, sigma, pi, mask, rep.as_dict())
+
+
+def debug_expf(x: torch.Tensor) -> torch.Tensor:
+    _check_dev(x)
+    y = torch.empty_like(x)
+    check(lib().pbs_debug_expf(_ptr(x), _ptr(y), x.numel(), _stream()))
+    return y

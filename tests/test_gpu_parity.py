@@ -1,0 +1,238 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bar:
+  * bit-exact: importance scores, pi / sigma (+ inverses), block scores,
+    masks, selected-block counts;
+  * outputs: bf16 path vs the oracle run in fp32 on the bf16-upcast inputs,
+    |err|max <= 2e-2 and mean <= 2e-3 (unit-Gaussian V); f32 path <= 1e-4.
+The oracle itself is pinned by tests/test_oracle.py.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+BF16_MAX, BF16_MEAN = 2e-2, 2e-3
+F32_MAX = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2510_21270_b200 import ops as _ops
+
+    _ops.lib()
+    return _ops
+
+
+def bf16_inputs(rng, hq, hkv, n, d, kind="gaussian", lines=8, strength=30.0, block=128, segment=256):
+    """Synthetic Q/K/V (head-major) rounded to bf16; returns torch bf16 + numpy f32 upcasts."""
+    q = rng.standard_normal((hq, n, d)).astype(np.float32)
+    k = rng.standard_normal((hkv, n, d)).astype(np.float32)
+    v = rng.standard_normal((hkv, n, d)).astype(np.float32)
+    if kind == "vertical_lines":  # workload.hpp:182-194, one direction per kv head
+        g = hq // hkv
+        for kh in range(hkv):
+            u = rng.standard_normal(d)
+            u /= np.linalg.norm(u)
+            q[kh * g:(kh + 1) * g] += np.sqrt(d) * u
+            pos = rng.choice(n, size=min(lines, n), replace=False)
+            k[kh, pos] += strength * u
+    tq = torch.from_numpy(q).to(torch.bfloat16)
+    tk = torch.from_numpy(k).to(torch.bfloat16)
+    tv = torch.from_numpy(v).to(torch.bfloat16)
+    return (tq.cuda(), tk.cuda(), tv.cuda(), tq.float().numpy(), tk.float().numpy(), tv.float().numpy())
+
+
+def kv_of(h, hq, hkv):
+    return h // (hq // hkv)
+
+
+# ---------------------------------------------------------------------------
+def test_device_expf_matches_host_expf(ops):
+    """expf_glibc.cuh vs this host's glibc expf (the reference's std::exp)."""
+    from oracle import host_expf
+
+    rng = np.random.default_rng(0)
+    bits = rng.integers(0, 2**32, size=1 << 24, dtype=np.uint64).astype(np.uint32)
+    ranges = [np.linspace(-110.0, 0.0, 1 << 22, dtype=np.float32),
+              np.linspace(-1.0, 1.0, 1 << 20, dtype=np.float32),
+              np.array([0.0, -0.0, np.inf, -np.inf, 88.72, -103.97, -103.28, -87.3, 1e-30, -1e-30], np.float32)]
+    x = np.concatenate([bits.view(np.float32)] + ranges)
+    x = x[~np.isnan(x)]
+    dev = ops.debug_expf(torch.from_numpy(x).cuda()).cpu().numpy()
+    host = host_expf(x)
+    bad = np.flatnonzero(dev.view(np.uint32) != host.view(np.uint32))
+    assert bad.size == 0, f"{bad.size} mismatches, e.g. x={x[bad[:5]]}"
+
+
+@pytest.mark.parametrize("hq,hkv,n,d,b,dtype", [
+    (1, 1, 1024, 128, 128, "bf16"),
+    (4, 2, 777, 64, 64, "bf16"),
+    (2, 2, 300, 16, 16, "f32"),
+    (1, 1, 50, 32, 64, "bf16"),   # N < B: all queries
+    (1, 1, 4096, 128, 64, "f32"),  # config 1 (B=64)
+])
+def test_importance_and_key_permutation_bitexact(ops, oracle, hq, hkv, n, d, b, dtype):
+    rng = np.random.default_rng(n + d)
+    tq, tk, tv, q, k, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", block=b)
+    if dtype == "f32":
+        q = rng.standard_normal((hq, n, d)).astype(np.float32)
+        k = rng.standard_normal((hkv, n, d)).astype(np.float32)
+        tq, tk = torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda()
+    scores = ops.estimate_key_importance(tq, tk, b).cpu().numpy()
+    s = max(b, 4 * b) if n >= 4 * b else b
+    perm, inv = ops.build_key_permutation(torch.from_numpy(scores).cuda(), s)
+    perm, inv = perm.cpu().numpy(), inv.cpu().numpy()
+    for h in range(hq):
+        want, _ = oracle.estimate_key_importance(q[h], k[kv_of(h, hq, hkv)], b)
+        np.testing.assert_array_equal(scores[h].view(np.uint32), want.view(np.uint32))
+        wp = oracle.build_key_permutation(want, s)
+        np.testing.assert_array_equal(perm[h], wp)
+        np.testing.assert_array_equal(inv[h][perm[h]], np.arange(n))
+
+
+def test_key_permutation_ties_kat(ops):
+    """permutation_test.cpp:178-184 through the device sort."""
+    s = torch.tensor([[.1, .4, .2, .3, .05, .05, .6, .3]], dtype=torch.float32).cuda()
+    perm, inv = ops.build_key_permutation(s, 4)
+    assert perm.cpu().tolist() == [[1, 3, 2, 0, 6, 7, 4, 5]]
+    zeros = torch.zeros(1, 256 * 3 + 7, dtype=torch.float32).cuda()  # all ties + ragged tail
+    perm, _ = ops.build_key_permutation(zeros, 256)
+    assert perm.cpu().tolist()[0] == list(range(256 * 3 + 7))
+
+
+@pytest.mark.parametrize("n,d,b,s,tau", [(2048, 128, 128, 256, 0.9), (1000, 64, 32, 64, 0.5),
+                                         (640, 32, 64, 0, 0.7)])
+def test_block_scores_and_selection_bitexact(ops, oracle, n, d, b, s, tau):
+    rng = np.random.default_rng(7)
+    tq, tk, tv, q, k, v = bf16_inputs(rng, 2, 1, n, d, kind="vertical_lines")
+    scores = ops.meanpool_block_scores(tq, tk, b, s).cpu().numpy()
+    mask, kv_idx, kv_cnt = ops.select_blocks(torch.from_numpy(scores).cuda(), b, s, tau)
+    mask, kv_idx, kv_cnt = mask.cpu().numpy(), kv_idx.cpu().numpy(), kv_cnt.cpu().numpy()
+    t = -(-n // b)
+    causal = oracle.build_block_causal_mask(t, b, s)
+    for h in range(2):
+        want = oracle.meanpool_block_scores(q[h], k[0], b, causal)
+        np.testing.assert_array_equal(scores[h].view(np.uint32), want.view(np.uint32))
+        wm = oracle.select_blocks(want, causal, b, s, tau)
+        np.testing.assert_array_equal(mask[h], wm)
+        for i in range(t):
+            sel = np.flatnonzero(wm[i])
+            assert kv_cnt[h, i] == sel.size
+            np.testing.assert_array_equal(kv_idx[h, i, :sel.size], sel)
+
+
+@pytest.mark.parametrize("strategy", ["key_permute", "none", "query_permute", "both"])
+@pytest.mark.parametrize("hq,hkv,n,d,b,s,tau", [
+    (2, 1, 1024, 128, 128, 256, 0.9),
+    (4, 2, 1536 + 64, 128, 128, 256, 0.8),  # ragged final block
+    (1, 1, 512, 64, 32, 128, 0.7),
+])
+def test_pipeline_matches_oracle(ops, oracle, strategy, hq, hkv, n, d, b, s, tau):
+    from oracle import make_config as ocfg
+
+    rng = np.random.default_rng(11)
+    tq, tk, tv, q, k, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0, block=b)
+    if strategy == "none":
+        s = 0
+    cfg = ops.make_config(block_size=b, segment_size=s, tau=tau, strategy=strategy)
+    res = ops.pbs_attention(tq, tk, tv, cfg)
+    out = res.output.float().cpu().numpy()
+    sigma, pi, mask = res.sigma.cpu().numpy(), res.pi.cpu().numpy(), res.mask.cpu().numpy()
+    sel = 0
+    for h in range(hq):
+        kh = kv_of(h, hq, hkv)
+        r = oracle.pbs_attention(q[h], k[kh], v[kh], ocfg(block_size=b, segment_size=s, tau=tau, strategy=strategy))
+        np.testing.assert_array_equal(sigma[h], r.sigma)
+        np.testing.assert_array_equal(pi[h], r.pi)
+        np.testing.assert_array_equal(mask[h], r.mask)
+        err = np.abs(out[h] - r.output)
+        assert err.max() <= BF16_MAX and err.mean() <= BF16_MEAN, (h, err.max(), err.mean())
+        sel += r.report["selected_blocks"]
+    assert res.report["selected_blocks"] == sel
+
+
+@pytest.mark.parametrize("kind", ["vertical_lines", "mixed", "gaussian"])
+def test_reference_fixtures_f32(ops, kind):
+    """The committed reference runs (oracle/gen_golden.py) through the f32 device path."""
+    g = np.load(os.path.join(GOLDEN, f"ref_pipeline_f32_{kind}.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, "ref_pipeline_f32.json")))[kind]
+    cfg = ops.make_config(block_size=meta["block"], segment_size=meta["segment"], tau=meta["tau"],
+                          strategy=meta["strategy"])
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a[None])).cuda()  # noqa: E731
+    res = ops.pbs_attention(t(g["q"]), t(g["k"]), t(g["v"]), cfg)
+    np.testing.assert_array_equal(res.sigma.cpu().numpy()[0], g["sigma"])
+    np.testing.assert_array_equal(res.pi.cpu().numpy()[0], g["pi"])
+    np.testing.assert_array_equal(res.mask.cpu().numpy()[0], g["mask"])
+    assert np.abs(res.output.cpu().numpy()[0] - g["output"]).max() <= F32_MAX
+    for key in ("selected_blocks", "total_admissible_blocks"):
+        assert res.report[key] == meta["report"][key]
+    assert res.report["block_density"] == meta["report"]["block_density"]
+    assert abs(res.report["pooled_score_coverage"] - meta["report"]["pooled_score_coverage"]) <= 1e-9
+
+
+def test_causality_bitwise_on_device(ops):
+    """pipeline_test.cpp:105-128 / acceptance C5 on the device path."""
+    rng = np.random.default_rng(53)
+    tq, tk, tv, *_ = bf16_inputs(rng, 2, 1, 1024, 128, kind="vertical_lines")
+    cfg = ops.make_config(block_size=128, segment_size=256, tau=0.8)
+    base = ops.pbs_attention(tq, tk, tv, cfg).output.clone()
+    for j in (5, 300, 1023):
+        v2 = tv.clone()
+        v2[:, j] += 100.0
+        out = ops.pbs_attention(tq, tk, v2, cfg).output
+        assert torch.equal(out[:, :j], base[:, :j]), j
+
+
+def test_dense_causal_matches_sdpa(ops):
+    rng = np.random.default_rng(3)
+    tq, tk, tv, *_ = bf16_inputs(rng, 8, 2, 2048 + 77, 128)
+    out = ops.dense_causal_attention(tq, tk, tv).float()
+    kk = tk.float().repeat_interleave(4, dim=0)
+    vv = tv.float().repeat_interleave(4, dim=0)
+    ref = torch.nn.functional.scaled_dot_product_attention(tq.float()[None], kk[None], vv[None], is_causal=True)[0]
+    err = (out - ref).abs()
+    assert err.max().item() <= BF16_MAX and err.mean().item() <= BF16_MEAN
+
+
+def test_tau_one_is_causal_attention(ops):
+    """pipeline_test.cpp:27-58 (C4) on device: tau = 1 selects the full causal grid."""
+    rng = np.random.default_rng(5)
+    tq, tk, tv, *_ = bf16_inputs(rng, 4, 2, 1024 + 128, 128)
+    res = ops.pbs_attention(tq, tk, tv, ops.make_config(tau=1.0))
+    dense = ops.dense_causal_attention(tq, tk, tv)
+    err = (res.output.float() - dense.float()).abs()
+    assert err.max().item() <= BF16_MAX
+
+
+def test_degenerate_row_raises(ops):
+    from paper_2510_21270_b200 import DegenerateRowError
+
+    rng = np.random.default_rng(6)
+    tq, tk, tv, *_ = bf16_inputs(rng, 1, 1, 512, 128)
+    t = 4
+    kv_idx = torch.zeros(1, t, t, dtype=torch.int32).cuda()
+    kv_cnt = torch.tensor([[1, 0, 1, 1]], dtype=torch.int32).cuda()
+    kv_idx[0, :, 0] = 0
+    with pytest.raises(DegenerateRowError) as e:
+        ops.attention_block_sparse(tq, tk, tv, 128, kv_idx, kv_cnt)
+    assert "query block 1" in str(e.value)
+
+
+def test_host_entry_matches_device_entry(ops):
+    rng = np.random.default_rng(9)
+    tq, tk, tv, *_ = bf16_inputs(rng, 2, 1, 1024, 128, kind="vertical_lines")
+    cfg = ops.make_config()
+    dev = ops.pbs_attention(tq, tk, tv, cfg)
+    host = ops.pbs_attention_host(tq.cpu(), tk.cpu(), tv.cpu(), cfg, return_perms=True)
+    assert torch.equal(host.output, dev.output.cpu())
+    assert torch.equal(host.pi, dev.pi.cpu())
+    assert torch.equal(host.mask, dev.mask.cpu())
