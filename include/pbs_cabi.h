@@ -101,6 +101,8 @@ typedef struct pbs_report {
 /* ---- library ---------------------------------------------------------- */
 PBS_API const char* pbs_last_error(void);
 PBS_API const char* pbs_version(void);
+/* number of kernels this library has launched in the process (diagnostics) */
+PBS_API int64_t pbs_kernel_launches(void);
 
 /* Device scratch needed by pbs_attention / the estimate and select stages. */
 PBS_API size_t pbs_workspace_size(const pbs_shape* shape, const pbs_pipeline_config* cfg);

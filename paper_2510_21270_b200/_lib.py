@@ -26,7 +26,7 @@ STRATEGIES = {"none": 0, "key_permute": 1, "query_permute": 2, "both": 3}
 
 # every symbol include/pbs_cabi.h declares
 EXPORTS = [
-    "pbs_last_error", "pbs_version", "pbs_workspace_size", "pbs_estimate_key_importance",
+    "pbs_last_error", "pbs_version", "pbs_kernel_launches", "pbs_workspace_size", "pbs_estimate_key_importance",
     "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_apply_rows",
     "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_block_sparse_attention_fwd",
     "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
@@ -100,6 +100,7 @@ DBL = C.c_double
 _SIGS = {
     "pbs_last_error": (C.c_char_p, []),
     "pbs_version": (C.c_char_p, []),
+    "pbs_kernel_launches": (C.c_int64, []),
     "pbs_workspace_size": (SZ, [C.POINTER(Shape), C.POINTER(PipelineConfig)]),
     "pbs_estimate_key_importance": (C.c_int, [VP, VP, C.POINTER(Shape), I64, DBL, VP, VP, SZ, VP]),
     "pbs_build_key_permutation": (C.c_int, [VP, I32, I64, I64, VP, VP, VP]),

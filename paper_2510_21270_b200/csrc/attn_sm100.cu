@@ -641,13 +641,14 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
     const int64_t rows = (int64_t)p.hq * t;
     if (p.q_orig) {
       block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.q_orig, p.hq, p.n, t, mm);
+      PBS_LAUNCH_CHECK("block_minmax_kernel");
       a.q_mm = mm;
     }
     if (p.k_orig) {
       block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.k_orig, p.hq, p.n, t, mm + rows);
+      PBS_LAUNCH_CHECK("block_minmax_kernel");
       a.k_mm = mm + rows;
     }
-    PBS_LAUNCH_CHECK("block_minmax_kernel");
   }
   static bool attr = false;
   if (!attr) {

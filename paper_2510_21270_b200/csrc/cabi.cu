@@ -9,6 +9,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -21,7 +22,10 @@ namespace pbs_b200 {
 
 namespace {
 thread_local std::string g_err;
-}
+std::atomic<long long> g_launches{0};
+}  // namespace
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* prefix, const std::string& msg) { g_err = std::string(prefix) + ": " + msg; }
 
@@ -155,6 +159,8 @@ extern "C" {
 const char* pbs_last_error(void) { return g_err.c_str(); }
 
 const char* pbs_version(void) { return "pbs-b200 0.1 (sm_100a)"; }
+
+int64_t pbs_kernel_launches(void) { return (int64_t)g_launches.load(); }
 
 size_t pbs_workspace_size(const pbs_shape* shape, const pbs_pipeline_config* cfg) {
   if (check_shape(shape) || check_cfg(cfg)) return 0;

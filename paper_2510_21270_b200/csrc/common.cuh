@@ -22,8 +22,12 @@ int cuda_fail(cudaError_t e, const char* where);
     if (_e != cudaSuccess) return ::pbs_b200::cuda_fail(_e, #expr); \
   } while (0)
 
+// every kernel launch of the library is followed by exactly one of these;
+// it also feeds the process-wide launch counter (pbs_kernel_launches)
+void count_launch();
 #define PBS_LAUNCH_CHECK(where)                                       \
   do {                                                                \
+    ::pbs_b200::count_launch();                                       \
     cudaError_t _e = cudaGetLastError();                              \
     if (_e != cudaSuccess) return ::pbs_b200::cuda_fail(_e, where);   \
   } while (0)

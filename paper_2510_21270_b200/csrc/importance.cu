@@ -457,16 +457,20 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
   if (dtype == PBS_DTYPE_BF16) {
     centroid_kernel<__nv_bfloat16><<<dim3((unsigned)tc, (unsigned)k_heads), 128, csmem, st>>>(
         static_cast<const __nv_bfloat16*>(k), n, d, block, tc, cent, cn);
+    PBS_LAUNCH_CHECK("centroid_kernel");
     qnorm_kernel<__nv_bfloat16><<<(unsigned)ceil_div((int64_t)hq * n, 128), 128, 0, st>>>(
         static_cast<const __nv_bfloat16*>(q), (int64_t)hq * n, d, qn);
+    PBS_LAUNCH_CHECK("qnorm_kernel");
     query_group_kernel<__nv_bfloat16>
         <<<dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq), kThreads, 0,
            st>>>(static_cast<const __nv_bfloat16*>(q), cent, qn, cn, hq / k_heads, n, d, tc, best);
   } else {
     centroid_kernel<float><<<dim3((unsigned)tc, (unsigned)k_heads), 128, csmem, st>>>(
         static_cast<const float*>(k), n, d, block, tc, cent, cn);
+    PBS_LAUNCH_CHECK("centroid_kernel");
     qnorm_kernel<float><<<(unsigned)ceil_div((int64_t)hq * n, 128), 128, 0, st>>>(
         static_cast<const float*>(q), (int64_t)hq * n, d, qn);
+    PBS_LAUNCH_CHECK("qnorm_kernel");
     query_group_kernel<float>
         <<<dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq), kThreads, 0,
            st>>>(static_cast<const float*>(q), cent, qn, cn, hq / k_heads, n, d, tc, best);
