@@ -7,23 +7,38 @@
 // in the list of key blocks a query block visits.
 //
 // Tile: B = 128 query rows x 128 keys, d = 128, bf16 in, fp32 accumulate.
-// Persistent CTAs (one per SM) walk (head, query-block) work items, heaviest
-// query blocks first.  Warp roles (192 threads):
-//   warp 0      TMA producer: Q tile once per item, K/V tiles of each selected
-//               key block into a 2-stage ring (cp.async.bulk.tensor, SW128)
-//   warp 1      TMEM owner + MMA issuer: S = Q K^T into one of two TMEM
-//               S buffers (double-buffered so QK^T of block e+1 overlaps the
-//               softmax of block e), then O += P V into the TMEM O buffer
-//   warps 2..5  softmax / correction / epilogue, one thread per query row
-//               (TMEM lane = row): tcgen05.ld of S, block-class masking by
-//               original positions, online softmax in the exp2 domain with
-//               lazy rescaling (only when the running max grows by > 8),
-//               P -> bf16 -> SW128 smem for the PV MMA, and the final
-//               O / l written to row out_rows[i] (the fused un-permute).
+// Persistent CTAs (one per SM) walk (head, query-block) work items, one KV
+// source at a time for L2 locality, heaviest query blocks first.
+// Warp roles (384 threads):
+//   warp 0       TMA producer: Q tile once per item, K/V tiles of each visited
+//                key block into a 2-stage ring (cp.async.bulk.tensor, SW128)
+//   warp 1       TMEM owner + MMA issuer (one elected lane): S_w = Q K^T and
+//                O_w += P_w V with tcgen05.mma, completion via tcgen05.commit
+//   warps 2..3   idle
+//   warps 4..7   softmax warpgroup 0: even-numbered visited key blocks
+//   warps 8..11  softmax warpgroup 1: odd-numbered visited key blocks
+// (each group's four warps cover the four TMEM lane quadrants, warp % 4)
+// The two softmax warpgroups split the key blocks of the SAME query tile
+// (split-KV inside the CTA): each owns a TMEM S buffer and a TMEM O
+// accumulator and keeps its own running (m, l), so two softmaxes are in
+// flight while the tensor core alternates between them; the epilogue merges
+// the two partial states (m = max, l and O rescaled by exp2(m_w - m)).
+// Per block a softmax thread (= one query row = one TMEM lane) reads its S
+// row from TMEM twice (a max pass over two 64-column halves, then an exp pass
+// over 32-column chunks, so the thread holds at most 64 scores and stays under
+// the 168-register budget of 384 threads), masks by original positions
+// (partial blocks only: a separate code path), applies the online
+// softmax in the exp2 domain with lazy rescaling (only when the running max
+// grows by > 8), writes P as bf16 into a SW128 shared-memory tile for the PV
+// MMA, and finally writes O / l to row out_rows[i] (the fused un-permute).
 // Block classes follow AdmissibilityIndex::classify (attention.hpp:167-174):
 // per-block [min, max] of original positions; `none` blocks are skipped by
 // every role (an exact no-op, attention.hpp:286), `full` blocks skip the
-// per-element test, `partial` ones compare k_orig[j] <= q_orig[i].
+// per-element test, `partial` ones compare k_orig[j] <= q_orig[i].  A small
+// pre-pass (visit_kernel) writes, per (head, query block), the compacted list
+// of visited key blocks with the class packed in; every role prefetches it 32
+// entries at a time and broadcasts entries by warp shuffle, so the hot loop
+// has no dependent global loads.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -39,17 +54,19 @@ constexpr int kBM = 128;      // query rows per tile (= block size B)
 constexpr int kBN = 128;      // keys per tile (= block size B)
 constexpr int kD = 128;       // head dim
 constexpr int kStages = 2;    // K/V ring depth
-constexpr int kThreads = 192;
+constexpr int kThreads = 384;
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
-constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | spare
-constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
+constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O0 | O1
+__host__ __device__ constexpr uint32_t col_s(int w) { return w ? 128u : 0u; }
+__host__ __device__ constexpr uint32_t col_o(int w) { return w ? 384u : 256u; }
 
 struct __align__(8) Barriers {
   uint64_t q_full, q_empty;
   uint64_t kv_full[kStages], kv_empty[kStages];
   uint64_t s_full[2], s_free[2];
-  uint64_t p_full, pv_done, o_free;
+  uint64_t p_full[2], pv_done[2];
+  uint64_t o_free;
   uint32_t tmem_base;
 };
 
@@ -58,11 +75,12 @@ struct SmemLayout {
   static constexpr int q = 0;
   static constexpr int k = q + kTileBytes;
   static constexpr int v = k + kStages * kTileBytes;
-  static constexpr int p = v + kStages * kTileBytes;
-  static constexpr int korig = p + kTileBytes;                 // int[2][128]
+  static constexpr int p = v + kStages * kTileBytes;            // P0 | P1
+  static constexpr int korig = p + 2 * kTileBytes;              // int[2 WG][128]
   static constexpr int bars = korig + 2 * 128 * 4;
   static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
 };
+static_assert(SmemLayout::total <= 232448, "shared memory budget");
 
 // ---- PTX wrappers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -152,6 +170,23 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// 2^x on the FMA/ALU pipes (Cody-Waite split + degree-3 minimax on [-1/2, 1/2],
+// max relative error 7.7e-5, far below bf16 P's 2^-9): offloads the MUFU unit.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.5f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: round-to-nearest integer in the low bits
+  const float jf = t - 12582912.0f;
+  const float f = x - jf;
+  float p = fmaf(0.055219680070877075f, f, 0.2426094114780426f);
+  p = fmaf(p, f, 0.6932516694068909f);
+  p = fmaf(p, f, 0.9999279975891113f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -189,6 +224,8 @@ struct KernelArgs {
   int causal;   // identity element mask when q_orig/k_orig are null
   int dense;    // dense causal list (kb = 0..qb)
   int64_t items;
+  const int32_t* vis;   // [hq][t][t] visited blocks (kb | cls << 30), sparse mode
+  const int32_t* nvis;  // [hq][t]
 };
 
 struct Item {
@@ -197,10 +234,19 @@ struct Item {
 };
 
 __device__ __forceinline__ Item item_of(const KernelArgs& a, int64_t idx) {
-  // heaviest query blocks first: qb descending, heads interleaved
+  // L2 locality: all CTAs sweep one KV source at a time (per q head for the
+  // per-head permuted K'/V', per GQA group for shared K/V), heaviest query
+  // blocks first inside it.
   Item it;
-  it.qb = a.t - 1 - idx / a.hq;
-  it.h = (int)(idx % a.hq);
+  const int64_t per = a.t * (a.kv_heads == a.hq ? 1 : a.group);
+  const int64_t grp = idx / per, rem = idx % per;
+  if (a.kv_heads == a.hq) {
+    it.h = (int)grp;
+    it.qb = a.t - 1 - rem;
+  } else {
+    it.h = (int)(grp * a.group + rem % a.group);
+    it.qb = a.t - 1 - rem / a.group;
+  }
   return it;
 }
 
@@ -237,13 +283,128 @@ __device__ __forceinline__ int block_class(const KernelArgs& a, const Item& it, 
   return 1;
 }
 
+
+// visited-block cursor: dense causal lists are computed, sparse lists come from
+// the pre-pass (vis[h][qb][e] = kb | cls << 30), prefetched 32 entries per warp.
+struct Visit {
+  const int32_t* list;
+  int len;
+  int base;
+  uint32_t cache;
+};
+
+__device__ __forceinline__ Visit visit_begin(const KernelArgs& a, const Item& it) {
+  Visit v;
+  v.base = -64;
+  v.cache = 0;
+  if (a.dense) {
+    v.list = nullptr;
+    v.len = (int)(it.qb + 1);
+  } else {
+    v.list = a.vis + ((int64_t)it.h * a.t + it.qb) * a.t;
+    v.len = a.nvis[(int64_t)it.h * a.t + it.qb];
+  }
+  return v;
+}
+
+// all 32 lanes of the warp must call this with the same e (e non-decreasing)
+__device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, Visit& v, int e, int lane,
+                                          int64_t& kb, int& cls) {
+  if (a.dense) {
+    kb = e;
+    const bool ragged = (kb + 1) * kBN > a.n;
+    cls = (kb == it.qb || ragged) ? 1 : 2;
+    return;
+  }
+  if (e >= v.base + 32) {
+    v.base = e & ~31;
+    v.cache = (v.base + lane < v.len) ? (uint32_t)__ldg(v.list + v.base + lane) : 0u;
+  }
+  const uint32_t x = __shfl_sync(0xffffffffu, v.cache, e - v.base);
+  kb = x & 0x3fffffffu;
+  cls = (int)(x >> 30);
+}
+
+// Softmax of one visited block for one query row (a TMEM lane).  kPartial
+// adds the original-position mask; full blocks also route every fourth exp2
+// through the FMA-pipe polynomial.  Pass 1: block max -> running max.
+template <bool kPartial>
+__device__ __forceinline__ void softmax_max(uint32_t tS, const int* ko, int qo, float sc, float& m,
+                                            bool& need_rescale, float& factor) {
+  float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t r[64];
+    TMEM_LD32(tS + h * 64, r);
+    TMEM_LD32(tS + h * 64 + 32, (r + 32));
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      float x = __uint_as_float(r[j]);
+      if (kPartial && ko[h * 64 + j] > qo) x = -INFINITY;
+      mx4[j & 3] = fmaxf(mx4[j & 3], x);
+    }
+  }
+  const float bmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sc;
+  // online softmax in the log2 domain with lazy rescale (threshold 2^8)
+  const float m_new = fmaxf(m, bmax);
+  need_rescale = false;
+  factor = 1.0f;
+  if (m_new != -INFINITY) {
+    if (m == -INFINITY) {
+      m = m_new;  // O rows are still exactly 0 here
+    } else if (m_new > m + 8.0f) {
+      factor = ex2(m - m_new);
+      need_rescale = true;
+      m = m_new;
+    }
+  }
+}
+
+// Pass 2: p = exp2(s * scale_log2 - m) -> bf16 -> the SW128 P tile; returns sum p.
+template <bool kPartial>
+__device__ __forceinline__ float softmax_emit(uint32_t tS, const int* ko, int qo, float sc, float m, uint32_t p_row,
+                                              int row) {
+  const float neg_m = (m == -INFINITY) ? 0.0f : -m;
+  float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[32];
+    TMEM_LD32(tS + c * 32, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {  // 16-byte chunks of the P row (8 keys)
+      uint32_t pk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = q4 * 8 + 2 * u;
+        float x0 = __uint_as_float(r[j]), x1 = __uint_as_float(r[j + 1]);
+        if (kPartial) {
+          if (ko[c * 32 + j] > qo) x0 = -INFINITY;
+          if (ko[c * 32 + j + 1] > qo) x1 = -INFINITY;
+        }
+        const float p0 = ex2(fmaf(x0, sc, neg_m));
+        const float y1 = fmaf(x1, sc, neg_m);
+        const float p1 = (!kPartial && (u & 1)) ? exp2_poly(y1) : ex2(y1);
+        sum4[(2 * u) & 3] += p0;
+        sum4[(2 * u + 1) & 3] += p1;
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+        pk[u] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      const int c8 = c * 4 + q4;
+      const uint32_t addr = p_row + (c8 >> 3) * kPanelBytes + (((c8 & 7) ^ (row & 7)) << 4);
+      st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
+  return (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const KernelArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Barriers* bar = reinterpret_cast<Barriers*>(smem + SmemLayout::bars);
-  int* korig_s = reinterpret_cast<int*>(smem + SmemLayout::korig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -253,13 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar->kv_full[s], 1);
       mbar_init(&bar->kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&bar->s_full[s], 1);
-      mbar_init(&bar->s_free[s], 128);
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&bar->s_full[w], 1);
+      mbar_init(&bar->s_free[w], 128);
+      mbar_init(&bar->p_full[w], 128);
+      mbar_init(&bar->pv_done[w], 1);
     }
-    mbar_init(&bar->p_full, 128);
-    mbar_init(&bar->pv_done, 1);
-    mbar_init(&bar->o_free, 128);
+    mbar_init(&bar->o_free, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -273,22 +434,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = bar->tmem_base;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      uint32_t q_it = 0, kv_it = 0;
-      for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
-        const Item it = item_of(a, idx);
-        const int kvh = it.h / a.group;
+    // ===================== TMA producer (lane 0 issues) =====================
+    uint32_t q_it = 0, kv_it = 0;
+    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
+      const Item it = item_of(a, idx);
+      const int kvh = it.h / a.group;
+      Visit vis = visit_begin(a, it);
+      if (lane == 0) {
         mbar_wait(&bar->q_empty, (q_it & 1) ^ 1);
         mbar_expect_tx(&bar->q_full, kTileBytes);
         for (int p = 0; p < 2; ++p)
           tma_load_3d(smem + SmemLayout::q + p * kPanelBytes, &tm_q, &bar->q_full, p * 64, (int)(it.qb * kBM), it.h);
-        ++q_it;
-        const int len = list_len(a, it);
-        for (int e = 0; e < len; ++e) {
-          const int64_t kb = list_at(a, it, e);
-          if (block_class(a, it, kb) == 0) continue;
-          const int s = kv_it % kStages;
+      }
+      ++q_it;
+      for (int e = 0; e < vis.len; ++e) {
+        int64_t kb;
+        int cls;
+        visit_get(a, it, vis, e, lane, kb, cls);
+        const int s = kv_it % kStages;
+        if (lane == 0) {
           mbar_wait(&bar->kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
           mbar_expect_tx(&bar->kv_full[s], 2 * kTileBytes);
           unsigned char* kd = smem + SmemLayout::k + s * kTileBytes;
@@ -297,8 +461,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_3d(kd + p * kPanelBytes, &tm_k, &bar->kv_full[s], p * 64, (int)(kb * kBN), kvh);
             tma_load_3d(vd + p * kPanelBytes, &tm_v, &bar->kv_full[s], p * 64, (int)(kb * kBN), kvh);
           }
-          ++kv_it;
         }
+        ++kv_it;
       }
     }
   } else if (warp == 1) {
@@ -306,43 +470,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major, V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
-    const uint32_t p_base = smem_u32(smem + SmemLayout::p);
-    uint32_t q_it = 0, kv_it = 0, s_it = 0, pv_it = 0, item_no = 0;
+    uint32_t q_it = 0, kv_it = 0, item_no = 0;
+    uint32_t s_cnt[2] = {0, 0}, pv_cnt[2] = {0, 0};
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x, ++item_no) {
       const Item it = item_of(a, idx);
-      const int len = list_len(a, it);
+      const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
       mbar_wait(&bar->q_full, q_it & 1);
       ++q_it;
-      int processed = 0;
       uint32_t prev_stage = 0;
-      bool have_prev = false;
-      auto issue_pv = [&](uint32_t stage, bool first) {
-        mbar_wait(&bar->p_full, pv_it & 1);
-        if (first) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);
+      bool o_waited = false;
+      // PV of visited block number `pe` (warpgroup pe & 1)
+      auto issue_pv = [&](int pe, uint32_t stage) {
+        const int w = pe & 1;
+        mbar_wait(&bar->p_full[w], pv_cnt[w] & 1);
+        if (!o_waited) {  // the previous item's epilogue has read O0 and O1
+          mbar_wait(&bar->o_free, (item_no & 1) ^ 1);
+          o_waited = true;
+        }
         tc_fence_after();
         if (lane == 0) {
           const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
+          const uint32_t p_base = smem_u32(smem + SmemLayout::p + w * kTileBytes);
 #pragma unroll
           for (int k = 0; k < kBN / 16; ++k) {
             // A = P [128 q x 128 kv] K-major SW128: panel k/4, +32 B per 16 keys
             const uint64_t ad = sdesc(p_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
             // B = V [128 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
             const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-            tc_mma(tmem + kColO, ad, bd, idesc_pv, (first && k == 0) ? 0u : 1u);
+            tc_mma(tmem + col_o(w), ad, bd, idesc_pv, (pe < 2 && k == 0) ? 0u : 1u);
           }
-          tc_commit(&bar->pv_done);
+          tc_commit(&bar->pv_done[w]);
           tc_commit(&bar->kv_empty[stage]);
         }
         __syncwarp();
-        ++pv_it;
+        ++pv_cnt[w];
       };
       for (int e = 0; e < len; ++e) {
-        const int64_t kb = list_at(a, it, e);
-        if (block_class(a, it, kb) == 0) continue;
         const uint32_t stage = kv_it % kStages;
+        const int w = e & 1;
         mbar_wait(&bar->kv_full[stage], (kv_it / kStages) & 1);
-        const uint32_t sb = s_it & 1;
-        mbar_wait(&bar->s_free[sb], ((s_it >> 1) & 1) ^ 1);
+        mbar_wait(&bar->s_free[w], (s_cnt[w] & 1) ^ 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
@@ -350,171 +517,145 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kD / 16; ++k) {
             const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
             const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-            tc_mma(tmem + (sb ? kColS1 : kColS0), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
+            tc_mma(tmem + col_s(w), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
           }
-          tc_commit(&bar->s_full[sb]);
+          tc_commit(&bar->s_full[w]);
         }
         __syncwarp();
-        ++s_it;
+        ++s_cnt[w];
         ++kv_it;
-        if (have_prev) issue_pv(prev_stage, processed == 1);
+        if (e > 0) issue_pv(e - 1, prev_stage);
         prev_stage = stage;
-        have_prev = true;
-        ++processed;
       }
-      // Q is free once every S of this item has been issued and completed
+      // Q is free once every S of this item has completed
       if (lane == 0) tc_commit(&bar->q_empty);
       __syncwarp();
-      if (have_prev) issue_pv(prev_stage, processed == 1);
+      if (len > 0) issue_pv(len - 1, prev_stage);
+      if (!o_waited) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // keep the o_free phases in step
     }
-  } else {
-    // ===================== softmax / correction / epilogue =====================
+  } else if (warp >= 4) {
+    // ===================== softmax warpgroups =====================
+    const int wg = (warp - 4) >> 2;      // 0 or 1
     const int quad = warp & 3;           // TMEM lane quadrant of this warp
     const int row = quad * 32 + lane;    // query row within the tile
-    const int sm_tid = threadIdx.x - 64;  // 0..127
+    const int wg_tid = threadIdx.x - 128 - wg * 128;  // 0..127
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    unsigned char* p_smem = smem + SmemLayout::p;
-    uint32_t s_it = 0, pv_it = 0, part_it = 0;
+    const uint32_t tS = tmem + lane_off + col_s(wg);
+    const uint32_t tO = tmem + lane_off + col_o(wg);
+    const uint32_t p_row = smem_u32(smem + SmemLayout::p + wg * kTileBytes) + row * 128;
+    int* ko = reinterpret_cast<int*>(smem + SmemLayout::korig) + wg * 128;
+    float* xch = reinterpret_cast<float*>(smem + SmemLayout::p);  // epilogue exchange (P0 region)
+    const float sc = a.scale_log2;
+    const bool any_mask = a.causal || a.q_orig || a.k_orig;
+    uint32_t s_cnt = 0, pv_cnt = 0;
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
       const Item it = item_of(a, idx);
-      const int len = list_len(a, it);
+      Visit vis = visit_begin(a, it);
       const int64_t i = it.qb * kBM + row;
       const bool valid = i < a.n;
       const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
       float m = -INFINITY;  // running max in the log2 domain
       float l = 0.0f;
-      int processed = 0;
-      for (int e = 0; e < len; ++e) {
-        const int64_t kb = list_at(a, it, e);
-        const int cls = block_class(a, it, kb);
-        if (cls == 0) continue;
-        // key original positions of a partial block; the buffer alternates per
-        // partial block so that the barrier of the next partial block orders reuse
-        int* ko = korig_s + (part_it & 1) * 128;
+      int mine = 0;
+      for (int e = wg; e < vis.len; e += 2) {
+        int64_t kb;
+        int cls;
+        visit_get(a, it, vis, e, lane, kb, cls);
         if (cls == 1) {
-          ++part_it;
-          const int64_t j = kb * kBN + sm_tid;
+          const int64_t j = kb * kBN + wg_tid;
           int v = 0x7fffffff;
           if (j < a.n) v = a.k_orig ? a.k_orig[(int64_t)it.h * a.n + j] : (int)j;
-          if (!(a.causal || a.q_orig || a.k_orig) && j < a.n) v = -1;  // unmasked: only the ragged tail
-          ko[sm_tid] = v;
-          named_bar_sync(1, 128);
+          if (!any_mask && j < a.n) v = -1;  // unmasked: only the ragged tail
+          ko[wg_tid] = v;
+          named_bar_sync(1 + wg, 128);
         }
-        const uint32_t sb = s_it & 1;
-        mbar_wait(&bar->s_full[sb], (s_it >> 1) & 1);
+        mbar_wait(&bar->s_full[wg], s_cnt & 1);
         tc_fence_after();
-        float x[128];
-        {
-          uint32_t r[32];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            TMEM_LD32(tmem + lane_off + (sb ? kColS1 : kColS0) + c * 32, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) x[c * 32 + j] = __uint_as_float(r[j]);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&bar->s_free[sb]);
-        ++s_it;
-        float bmax = -INFINITY;
-        if (cls == 1) {
-#pragma unroll
-          for (int j = 0; j < 128; ++j) {
-            const bool adm = ko[j] <= qo;
-            x[j] = adm ? x[j] * a.scale_log2 : -INFINITY;
-            bmax = fmaxf(bmax, x[j]);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 128; ++j) {
-            x[j] *= a.scale_log2;
-            bmax = fmaxf(bmax, x[j]);
-          }
-        }
-        // online softmax with lazy rescale
-        const float m_new = fmaxf(m, bmax);
-        bool need_rescale = false;
-        float factor = 1.0f;
-        if (m_new != -INFINITY) {
-          if (m == -INFINITY) {
-            m = m_new;  // O rows are still exactly 0 here
-          } else if (m_new > m + 8.0f) {
-            factor = ex2(m - m_new);
-            need_rescale = true;
-            m = m_new;
-          }
-        }
-        // the previous PV must be complete before P is overwritten or O touched
-        if (processed > 0) {
-          mbar_wait(&bar->pv_done, pv_it & 1);
-          ++pv_it;
+        ++s_cnt;
+        bool need_rescale;
+        float factor;
+        if (cls == 1) softmax_max<true>(tS, ko, qo, sc, m, need_rescale, factor);
+        else softmax_max<false>(tS, ko, qo, sc, m, need_rescale, factor);
+        // the previous PV of this warpgroup must be complete before P_w is
+        // overwritten or O_w rescaled
+        if (mine > 0) {
+          mbar_wait(&bar->pv_done[wg], pv_cnt & 1);
+          ++pv_cnt;
         }
         if (__any_sync(0xffffffffu, need_rescale)) {
           tc_fence_after();
-          uint32_t r[32];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            TMEM_LD32(tmem + lane_off + kColO + c * 32, r);
+            uint32_t r[32];
+            TMEM_LD32(tO + c * 32, r);
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * factor);
-            TMEM_ST32(tmem + lane_off + kColO + c * 32, r);
+            TMEM_ST32(tO + c * 32, r);
           }
           tmem_wait_st();
           l *= factor;
         }
-        float rowsum = 0.0f;
-        const float mm = (m == -INFINITY) ? 0.0f : m;
-#pragma unroll
-        for (int c8 = 0; c8 < 16; ++c8) {
-          uint32_t packed[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float p0 = ex2(x[c8 * 8 + 2 * u] - mm);
-            const float p1 = ex2(x[c8 * 8 + 2 * u + 1] - mm);
-            rowsum += p0 + p1;
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            packed[u] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          const int panel = c8 >> 3, chunk = c8 & 7;
-          unsigned char* dst = p_smem + panel * kPanelBytes + row * 128 + ((chunk ^ (row & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        if (cls == 1) {
+          l += softmax_emit<true>(tS, ko, qo, sc, m, p_row, row);
+          named_bar_sync(1 + wg, 128);  // ko[] may be refilled after this
+        } else {
+          l += softmax_emit<false>(tS, ko, qo, sc, m, p_row, row);
         }
-        l += rowsum;
+        tc_fence_before();
+        mbar_arrive(&bar->s_free[wg]);  // S_w fully read: the next QK^T may overwrite it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
-        mbar_arrive(&bar->p_full);
-        ++processed;
+        mbar_arrive(&bar->p_full[wg]);
+        ++mine;
       }
-      // ---- epilogue: O / l -> out[out_rows[i]]
-      if (processed > 0) {
-        mbar_wait(&bar->pv_done, pv_it & 1);
-        ++pv_it;
+      // ---- epilogue: merge the two partial states, O / l -> out[out_rows[i]]
+      if (mine > 0) {
+        mbar_wait(&bar->pv_done[wg], pv_cnt & 1);
+        ++pv_cnt;
       }
+      // both warpgroups' P tiles are free now (their last PV is done): reuse P0 to exchange (m, l)
+      named_bar_sync(3, 256);
+      xch[wg * 256 + row] = m;
+      xch[wg * 256 + 128 + row] = l;
+      named_bar_sync(3, 256);
+      const float m0 = xch[row], l0 = xch[128 + row], m1 = xch[256 + row], l1 = xch[384 + row];
+      const float mt = fmaxf(m0, m1);
+      const float f0 = (m0 == -INFINITY) ? 0.0f : ex2(m0 - mt);
+      const float f1 = (m1 == -INFINITY) ? 0.0f : ex2(m1 - mt);
+      const float lt = l0 * f0 + l1 * f1;
       tc_fence_after();
-      const bool degenerate = valid && (processed == 0 || l == 0.0f);
-      if (degenerate && a.status) {
+      const bool degenerate = valid && !(lt > 0.0f);
+      if (degenerate && a.status && wg == 0) {
         a.status[0] = 1;
         atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
       }
-      const float inv = (l > 0.0f) ? 1.0f / l : 0.0f;
+      const float inv = (lt > 0.0f) ? 1.0f / lt : 0.0f;
+      const float g0 = f0 * inv, g1 = f1 * inv;
       const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
-      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD;
+      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + wg * 64;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        TMEM_LD32(tmem + lane_off + kColO + c * 32, r);
+      for (int c = 0; c < 2; ++c) {  // this warpgroup writes columns [64 wg, 64 wg + 64)
+        const uint32_t col = wg * 64 + c * 32;
+        uint32_t r0[32], r1[32];
+        TMEM_LD32(tmem + lane_off + col_o(0) + col, r0);
+        TMEM_LD32(tmem + lane_off + col_o(1) + col, r1);
         tmem_wait_ld();
-        if (valid && processed > 0) {
+        if (valid && lt > 0.0f) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             uint32_t pk[4];
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[u * 8 + 2 * w]) * inv,
-                                                        __uint_as_float(r[u * 8 + 2 * w + 1]) * inv);
-              pk[w] = *reinterpret_cast<uint32_t*>(&b2);
+            for (int w2 = 0; w2 < 4; ++w2) {
+              const int j = u * 8 + 2 * w2;
+              float o0 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(r0[j]) * g0;
+              float o1 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(r0[j + 1]) * g0;
+              if (m1 != -INFINITY) {
+                o0 = fmaf(__uint_as_float(r1[j]), g1, o0);
+                o1 = fmaf(__uint_as_float(r1[j + 1]), g1, o1);
+              }
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(o0, o1);
+              pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
             }
             *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
@@ -522,6 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bar->o_free);
+      named_bar_sync(3, 256);  // the exchange area (P0) is reused by the next item's softmax
     }
   }
   tc_fence_before();
@@ -530,6 +672,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
+}
+
+// per (head, query block): the compacted list of visited key blocks with their
+// class (AdmissibilityIndex::classify), one warp per item
+__global__ void visit_kernel(KernelArgs a, int32_t* __restrict__ vis, int32_t* __restrict__ nvis) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= (int64_t)a.hq * a.t) return;
+  Item it;
+  it.h = (int)(g / a.t);
+  it.qb = g % a.t;
+  const int len = list_len(a, it);
+  int32_t* out = vis + g * a.t;
+  int cnt = 0;
+  for (int e0 = 0; e0 < len; e0 += 32) {
+    const int e = e0 + lane;
+    int64_t kb = 0;
+    int cls = 0;
+    if (e < len) {
+      kb = list_at(a, it, e);
+      cls = block_class(a, it, kb);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, cls != 0);
+    if (cls != 0) out[cnt + __popc(bal & ((1u << lane) - 1))] = (int32_t)(kb | ((int64_t)cls << 30));
+    cnt += __popc(bal);
+  }
+  if (lane == 0) nvis[g] = cnt;
 }
 
 // per-block [min, max] of an original-position map (AdmissibilityIndex::build)
@@ -602,7 +771,8 @@ bool attention_sm100_supported(const AttnParams& p) {
 
 size_t attention_sm100_workspace_bytes(int hq, int64_t n, int64_t block) {
   const int64_t t = ceil_div(n, block);
-  return (size_t)2 * hq * t * sizeof(int2) + 256;
+  // block min/max of sigma and pi, then the visit lists and counts
+  return (size_t)2 * hq * t * sizeof(int2) + ((size_t)hq * t * t + (size_t)hq * t) * 4 + 256;
 }
 
 int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st) {
@@ -630,14 +800,14 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   a.dense = p.kv_idx == nullptr;
   if (a.dense && !p.causal) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention without a block list must be causal");
   a.items = (int64_t)p.hq * t;
-  // block min/max of the original positions (only when a map is given)
+  // scratch: block min/max of the original positions + visit lists
   void* own = nullptr;
+  if (!sched_ws && !a.dense) {
+    PBS_CUDA_CHECK(cudaMallocAsync(&own, attention_sm100_workspace_bytes(p.hq, p.n, p.block), st));
+    sched_ws = own;
+  }
   if (p.q_orig || p.k_orig) {
     int2* mm = static_cast<int2*>(sched_ws);
-    if (!mm) {
-      PBS_CUDA_CHECK(cudaMallocAsync(&own, attention_sm100_workspace_bytes(p.hq, p.n, p.block), st));
-      mm = static_cast<int2*>(own);
-    }
     const int64_t rows = (int64_t)p.hq * t;
     if (p.q_orig) {
       block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.q_orig, p.hq, p.n, t, mm);
@@ -649,6 +819,14 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
       PBS_LAUNCH_CHECK("block_minmax_kernel");
       a.k_mm = mm + rows;
     }
+  }
+  if (!a.dense) {
+    int32_t* vis = static_cast<int32_t*>(sched_ws) + (2 * (size_t)p.hq * t * sizeof(int2)) / sizeof(int32_t);
+    int32_t* nvis = vis + (size_t)p.hq * t * t;
+    visit_kernel<<<(unsigned)ceil_div((int64_t)p.hq * t, 8), 256, 0, st>>>(a, vis, nvis);
+    PBS_LAUNCH_CHECK("visit_kernel");
+    a.vis = vis;
+    a.nvis = nvis;
   }
   static bool attr = false;
   if (!attr) {

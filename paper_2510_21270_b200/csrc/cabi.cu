@@ -81,7 +81,7 @@ bool uses_sigma(int s) { return s == PBS_STRATEGY_QUERY_PERMUTE || s == PBS_STRA
 
 // workspace carve-up for pbs_attention
 struct Layout {
-  size_t status, imp, scores, pi, pi_inv, sigma, sigma_inv, groups, qperm, kp, vp, qp, qbar, kbar, mask,
+  size_t status, imp, scores, pi, pi_inv, sigma, sigma_inv, groups, qperm, kp, vp, qp, qbar, kbar, blog, mask,
       kv_idx, kv_cnt, row_cov, sched, total;
 };
 
@@ -112,6 +112,7 @@ Layout plan(const pbs_shape* s, const pbs_pipeline_config* c) {
   L.qp = take(uses_sigma(c->strategy) ? (size_t)hq * n * d * es : 0);
   L.qbar = take((size_t)hq * t * d * 4);
   L.kbar = take((size_t)hq * t * d * 4);
+  L.blog = take((size_t)hq * t * t * 4);
   L.mask = take((size_t)hq * t * t);
   L.kv_idx = take((size_t)hq * t * t * 4);
   L.kv_cnt = take((size_t)hq * t * 4);
@@ -223,16 +224,17 @@ int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_shape* s
     return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size must be 0 or a multiple of the block size");
   const int64_t n = shape->seq_len, t = ceil_div(n, block_size);
   const int hq = shape->num_q_heads, d = shape->head_dim;
-  const size_t need = 2 * al((size_t)hq * t * d * 4);
+  const size_t need = 2 * al((size_t)hq * t * d * 4) + al((size_t)hq * t * t * 4);
   if (workspace_bytes < need) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "meanpool workspace too small");
   float* qbar = static_cast<float*>(workspace);
   float* kbar = reinterpret_cast<float*>(static_cast<char*>(workspace) + al((size_t)hq * t * d * 4));
+  float* blog = reinterpret_cast<float*>(static_cast<char*>(workspace) + 2 * al((size_t)hq * t * d * 4));
   cudaStream_t st = as_stream(stream);
   if (int rc = launch_pool(qp, shape->dtype, hq, hq, nullptr, n, d, block_size, qbar, st)) return rc;
   if (int rc = launch_pool(kp, shape->dtype, shape->num_kv_heads, hq, nullptr, n, d, block_size, kbar, st)) return rc;
-  // selection with tau = 1 but no outputs: only the scores are produced
-  return launch_score_select(qbar, kbar, hq, t, d, block_size, segment_size, effective_scale(scale, d), 1.0, 0, 0,
-                             scores, nullptr, nullptr, nullptr, nullptr, st);
+  // scores only (no selection)
+  return launch_score_select(qbar, kbar, blog, hq, t, d, block_size, segment_size, effective_scale(scale, d), 1.0, 0,
+                             0, 0, scores, nullptr, nullptr, nullptr, nullptr, st);
 }
 
 int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks, int64_t block_size,
@@ -391,8 +393,9 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
   float* kbar = static_cast<float*>(at(L.kbar));
   if (int rc = launch_pool(qp, dt, hq, hq, nullptr, n, d, b, qbar, st)) return rc;
   if (int rc = launch_pool(kp, dt, kv_heads, hq, nullptr, n, d, b, kbar, st)) return rc;
-  if (int rc = launch_score_select(qbar, kbar, hq, t, d, b, s, scale, cfg->tau, cfg->forced_first_block,
-                                   cfg->forced_diagonal_band, nullptr, mask, kv_idx, kv_cnt, row_cov, st))
+  if (int rc = launch_score_select(qbar, kbar, static_cast<float*>(at(L.blog)), hq, t, d, b, s, scale, cfg->tau,
+                                   cfg->forced_first_block, cfg->forced_diagonal_band, 1, nullptr, mask, kv_idx,
+                                   kv_cnt, row_cov, st))
     return rc;
   tm.mark();
   // ---- stage 4: attention with the original-position element mask (173-176)

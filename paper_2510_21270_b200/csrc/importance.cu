@@ -20,78 +20,26 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "exact_gemm.cuh"
 #include "expf_glibc.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace pbs_b200 {
 
 namespace {
 
-constexpr int kTile = 128;   // rows of A and of B per CTA
-constexpr int kChunk = 16;   // d-chunk staged in smem
-constexpr int kPad = 4;      // smem row padding (floats)
-constexpr int kThreads = 256;
+using xgemm::kTile;
+using xgemm::tile_row;
 
-// acc[a][b] = dot(A[row_a], B[row_b]) over c = 0..d-1 in order.  A rows are
-// a_base[0..a_rows), B rows b_base[0..b_rows) (both row-major, stride d).
-// Thread (tx, ty) owns A rows {ty*4+r, 64+ty*4+r} and B rows {tx*4+r, 64+tx*4+r}.
-template <typename TA, typename TB, bool kExact>
-__device__ __forceinline__ void exact_dot_tile(const TA* __restrict__ a_base, int a_rows,
-                                               const TB* __restrict__ b_base, int b_rows, int d,
-                                               float (&acc)[8][8], float (*As)[kTile + kPad],
-                                               float (*Bs)[kTile + kPad]) {
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
-  const int lrow = tid >> 1;        // 0..127
-  const int lcol = (tid & 1) * 8;   // 0 or 8
-  for (int c0 = 0; c0 < d; c0 += kChunk) {
-    const int kc = min(kChunk, d - c0);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int c = c0 + lcol + u;
-      float av = 0.0f, bv = 0.0f;
-      if (lcol + u < kc) {
-        if (lrow < a_rows) av = to_f32(a_base[(int64_t)lrow * d + c]);
-        if (lrow < b_rows) bv = to_f32(b_base[(int64_t)lrow * d + c]);
-      }
-      As[lcol + u][lrow] = av;
-      Bs[lcol + u][lrow] = bv;
-    }
-    __syncthreads();
-    for (int cc = 0; cc < kc; ++cc) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[cc][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[cc][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cc][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cc][64 + tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (kExact) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-          else acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
-        }
-    }
-    __syncthreads();
-  }
-}
-
-__device__ __forceinline__ int tile_row(int idx, int t) { return (idx < 4 ? 0 : 64) + t * 4 + (idx & 3); }
-
-// K1a: E[h][j][i] = (q[r0+i] . k[j]) * scale, rowmax[h][i] = max_j.
-// grid (ceil(N/128), ceil(take/128), Hq).  E is key-major so that the
-// per-row denominator chains (K1c) read 128-byte lines per step.
-template <typename T, bool kExact>
-__global__ void __launch_bounds__(kThreads) importance_logits_kernel(
-    const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int d, int take,
-    float scale, float* __restrict__ E, unsigned* __restrict__ rowmax) {
-  __shared__ __align__(16) float As[kChunk][kTile + kPad];
-  __shared__ __align__(16) float Bs[kChunk][kTile + kPad];
+// K1a: L[h][j][i] = (q[r0+i] . k[j]) * scale and rowmax[h][i] = max_j L.
+// grid (ceil(N/128), ceil(take/128), Hq).  L is key-major ([j][i]) so that the
+// per-row denominator chains (K1bc) read 128-byte lines per step.
+template <typename T, bool kExact, bool kVec>
+__global__ void __launch_bounds__(xgemm::kThreads) importance_logits_kernel(
+    const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int d, int take, float scale,
+    float* __restrict__ L, unsigned* __restrict__ rowmax) {
+  __shared__ __align__(16) xgemm::Smem sm;
   const int h = blockIdx.z;
   const int64_t j0 = (int64_t)blockIdx.x * kTile;
   const int i0 = blockIdx.y * kTile;
@@ -101,102 +49,143 @@ __global__ void __launch_bounds__(kThreads) importance_logits_kernel(
   const int a_rows = min(kTile, take - i0);
   const int b_rows = (int)min64(kTile, n - j0);
   float acc[8][8];
-  exact_dot_tile<T, T, kExact>(a_base, a_rows, b_base, b_rows, d, acc, As, Bs);
+  xgemm::tile<T, T, kExact, kVec>(a_base, a_rows, b_base, b_rows, d, acc, sm);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  float* Eh = E + (int64_t)h * n * take;
+  float* Lh = L + (int64_t)h * n * take;
+  float rmax[8];
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii) rmax[ii] = -INFINITY;
+  const bool vec_store = (take % 4 == 0);
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = tile_row(jj, tx);
+    if (j >= b_rows) continue;
+    float v[8];
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) {
+      v[ii] = __fmul_rn(acc[ii][jj], scale);  // logits[j] = acc * scale (permutation.hpp:166)
+      if (tile_row(ii, ty) < a_rows) rmax[ii] = fmaxf(rmax[ii], v[ii]);
+    }
+    float* dst = Lh + (j0 + j) * take + i0;
+    if (vec_store && ty * 4 + 3 < a_rows && 64 + ty * 4 + 3 < a_rows) {
+      *reinterpret_cast<float4*>(dst + ty * 4) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(dst + 64 + ty * 4) = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii)
+        if (tile_row(ii, ty) < a_rows) dst[tile_row(ii, ty)] = v[ii];
+    }
+  }
 #pragma unroll
   for (int ii = 0; ii < 8; ++ii) {
-    const int i = tile_row(ii, ty);
-    float mx = -INFINITY;
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int j = tile_row(jj, tx);
-      const float v = __fmul_rn(acc[ii][jj], scale);  // logits[j] = acc * scale (line 166)
-      if (i < a_rows && j < b_rows) {
-        Eh[(j0 + j) * take + i0 + i] = v;
-        mx = fmaxf(mx, v);
-      }
-    }
-    // reduce over the 16 threads sharing this row (same ty, lanes tx)
+    float mx = rmax[ii];
 #pragma unroll
     for (int o = 1; o < 16; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int i = tile_row(ii, ty);
     if (tx == 0 && i < a_rows) atomic_max_float(&rowmax[(int64_t)h * take + i0 + i], mx);
   }
 }
 
-// K1b: E = expf(E - mx_i) in place (lines 170-171), all heads.
-template <int kTake>
-__global__ void importance_exp_kernel_t(float* __restrict__ E, const unsigned* __restrict__ rowmax,
-                                        int64_t n, int64_t total) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int i = (int)(e % kTake);
-    const int64_t h = e / ((int64_t)kTake * n);
-    const float mx = decode_order_key(rowmax[h * kTake + i]);
-    E[e] = expf_glibc(__fsub_rn(E[e], mx));
-  }
-}
+// K1bc: per row i, e_j = expf(L[j][i] - mx_i) (permutation.hpp:171) and
+// denom_i = sequential sum over j = 0..N-1 (line 172), then
+// w_i = 1 / (denom * take) (line 174).  One CTA per (head, 32 rows): warps
+// 1..kExpWarps compute the exps of 64-key tiles into a shared-memory ring;
+// warp 0 is the adder, one dependent chain of N fp32 adds per lane.
+constexpr int kExpWarps = 8;
+constexpr int kJT = 64;            // keys per ring tile
+constexpr int kRing = 2 * kExpWarps;
 
-__global__ void importance_exp_generic_kernel(float* __restrict__ E, const unsigned* __restrict__ rowmax,
-                                              int take, int64_t n, int64_t total) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int i = (int)(e % take);
-    const int64_t h = e / ((int64_t)take * n);
-    const float mx = decode_order_key(rowmax[h * take + i]);
-    E[e] = expf_glibc(__fsub_rn(E[e], mx));
+__global__ void __launch_bounds__(32 * (1 + kExpWarps)) importance_expsum_kernel(
+    const float* __restrict__ L, const unsigned* __restrict__ rowmax, int take, int64_t n, float* __restrict__ w) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float (*ring)[kJT][32] = reinterpret_cast<float (*)[kJT][32]>(dsm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + sizeof(float) * kRing * kJT * 32);
+  uint64_t* empty = full + kRing;
+  const int h = blockIdx.y;
+  const int i0 = blockIdx.x * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = i0 + lane;
+  const bool row_ok = i < take;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::fence_mbar_init();
   }
-}
-
-// K1c: denom_i = sum_j E[j][i] in order j = 0..N-1 (lines 169-173), then
-// w_i = 1 / (denom * take) (line 174).  One thread per (head, row): a
-// dependent chain of N fp32 adds; consecutive lanes read consecutive i.
-__global__ void importance_denom_kernel(const float* __restrict__ E, int hq, int take, int64_t n,
-                                        float* __restrict__ w) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (int64_t)hq * take) return;
-  const int64_t h = g / take;
-  const int i = (int)(g % take);
-  const float* p = E + h * n * take + i;
-  float denom = 0.0f;
-  int64_t j = 0;
-  constexpr int U = 16;
-  for (; j + U <= n; j += U) {
-    float v[U];
+  __syncthreads();
+  const int64_t ntiles = (n + kJT - 1) / kJT;
+  const float* Lh = L + (int64_t)h * n * take;
+  if (warp > 0) {
+    const float mx = row_ok ? decode_order_key(rowmax[(int64_t)h * take + i]) : 0.0f;
+    for (int64_t t = warp - 1; t < ntiles; t += kExpWarps) {
+      const int slot = (int)(t % kRing);
+      ptx::mbar_wait(&empty[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
+      const int64_t jb = t * kJT;
+      const int cnt = (int)min64(kJT, n - jb);
+      // all loads of the tile first (64 x 128 B in flight per warp), then the exps
+      float xv[kJT];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldg(p + (j + u) * take);
+      for (int jj = 0; jj < kJT; ++jj) xv[jj] = (row_ok && jj < cnt) ? __ldg(Lh + (jb + jj) * take + i) : 0.0f;
 #pragma unroll
-    for (int u = 0; u < U; ++u) denom = __fadd_rn(denom, v[u]);
+      for (int jj = 0; jj < kJT; ++jj) ring[slot][jj][lane] = expf_glibc(__fsub_rn(xv[jj], mx));
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&full[slot]);
+    }
+  } else {
+    float denom = 0.0f;
+    for (int64_t t = 0; t < ntiles; ++t) {
+      const int slot = (int)(t % kRing);
+      ptx::mbar_wait(&full[slot], (uint32_t)((t / kRing) & 1));
+      const int cnt = (int)min64(kJT, n - t * kJT);
+      if (cnt == kJT) {
+#pragma unroll 16
+        for (int jj = 0; jj < kJT; ++jj) denom = __fadd_rn(denom, ring[slot][jj][lane]);
+      } else {
+        for (int jj = 0; jj < cnt; ++jj) denom = __fadd_rn(denom, ring[slot][jj][lane]);
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+    }
+    if (row_ok) w[(int64_t)h * take + i] = __fdiv_rn(1.0f, __fmul_rn(denom, (float)take));
   }
-  for (; j < n; ++j) denom = __fadd_rn(denom, __ldg(p + j * take));
-  w[g] = __fdiv_rn(1.0f, __fmul_rn(denom, (float)take));
 }
 
-// K1d: s[j] = sum_i E[j][i] * w_i in order i = r0..N-1 (line 175), with the
-// product rounded before the add (no contraction in the reference build).
-// CTA = 128 keys; the [128 x 32] E tile is staged through smem so that the
-// global reads are 128-byte rows and each thread then walks its key's row.
-__global__ void __launch_bounds__(128) importance_scores_kernel(const float* __restrict__ E,
-                                                                const float* __restrict__ w,
-                                                                int take, int64_t n,
+// K1d: s[j] = sum_i e_ij * w_i in order i = 0..take-1 (line 175), the product
+// rounded before the add; e_ij recomputed as expf(L - mx_i) (bit-identical to
+// K1bc's).  CTA = 128 keys; [128 x 32] tiles staged through smem.
+__global__ void __launch_bounds__(128) importance_scores_kernel(const float* __restrict__ L,
+                                                                const unsigned* __restrict__ rowmax,
+                                                                const float* __restrict__ w, int take, int64_t n,
                                                                 float* __restrict__ scores) {
   __shared__ float tile[128][33];
-  __shared__ float ws[32];
+  __shared__ float ws[32], ms[32];
   const int h = blockIdx.y;
   const int64_t j0 = (int64_t)blockIdx.x * 128;
   const int tid = threadIdx.x;
-  const float* Eh = E + (int64_t)h * n * take;
+  const float* Lh = L + (int64_t)h * n * take;
   float s = 0.0f;
   for (int i0 = 0; i0 < take; i0 += 32) {
     const int ic = min(32, take - i0);
-    // load rows j0..j0+127, columns i0..i0+ic: thread t loads (row t/32*.., col t%32)
-    for (int e = tid; e < 128 * 32; e += 128) {
-      const int r = e >> 5, c = e & 31;
-      float v = 0.0f;
-      if (c < ic && j0 + r < n) v = Eh[(j0 + r) * take + i0 + c];
-      tile[r][c] = v;
+    if (tid < 32) {
+      ws[tid] = tid < ic ? w[(int64_t)h * take + i0 + tid] : 0.0f;
+      ms[tid] = tid < ic ? decode_order_key(rowmax[(int64_t)h * take + i0 + tid]) : 0.0f;
     }
-    if (tid < 32) ws[tid] = tid < ic ? w[(int64_t)h * take + i0 + tid] : 0.0f;
+    __syncthreads();
+    {
+      float xv[32];
+      const int c = tid & 31;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {  // rows r = (tid >> 5) + 4u: loads first, then the exps
+        const int r = (tid >> 5) + 4 * u;
+        xv[u] = (c < ic && j0 + r < n) ? __ldg(Lh + (j0 + r) * take + i0 + c) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int r = (tid >> 5) + 4 * u;
+        tile[r][c] = (c < ic && j0 + r < n) ? expf_glibc(__fsub_rn(xv[u], ms[c])) : 0.0f;
+      }
+    }
     __syncthreads();
     for (int c = 0; c < ic; ++c) s = __fadd_rn(s, __fmul_rn(tile[tid][c], ws[c]));
     __syncthreads();
@@ -302,13 +291,12 @@ __global__ void qnorm_kernel(const T* __restrict__ q, int64_t rows, int d, float
 // sims = dot / (qnorm * cnorm) over [N x tc] tiles; per-row argmax with the
 // first index winning ties, through a packed 64-bit atomicMax
 // (order(sim) << 32 | ~j).  Only sims > -1 can win (best_sim starts at -1).
-template <typename T>
-__global__ void __launch_bounds__(kThreads) query_group_kernel(
+template <typename T, bool kVec>
+__global__ void __launch_bounds__(xgemm::kThreads) query_group_kernel(
     const T* __restrict__ q, const float* __restrict__ cent, const float* __restrict__ qn,
     const float* __restrict__ cn, int k_group, int64_t n, int d, int64_t tc,
     unsigned long long* __restrict__ best) {
-  __shared__ __align__(16) float As[kChunk][kTile + kPad];
-  __shared__ __align__(16) float Bs[kChunk][kTile + kPad];
+  __shared__ __align__(16) xgemm::Smem sm;
   const int h = blockIdx.z;
   const int64_t i0 = (int64_t)blockIdx.x * kTile;
   const int64_t j0 = (int64_t)blockIdx.y * kTile;
@@ -317,8 +305,8 @@ __global__ void __launch_bounds__(kThreads) query_group_kernel(
   const int b_rows = (int)min64(kTile, tc - j0);
   float acc[8][8];
   // centroids are f32 (not bf16-exact): always the non-fused mul + add path
-  exact_dot_tile<T, float, false>(q + ((int64_t)h * n + i0) * d, a_rows,
-                                  cent + ((int64_t)hk * tc + j0) * d, b_rows, d, acc, As, Bs);
+  xgemm::tile<T, float, false, kVec>(q + ((int64_t)h * n + i0) * d, a_rows, cent + ((int64_t)hk * tc + j0) * d,
+                                     b_rows, d, acc, sm);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
 #pragma unroll
   for (int ii = 0; ii < 8; ++ii) {
@@ -374,30 +362,35 @@ int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, 
   const int take = (int)min64(block, n);
   if (ws_bytes < importance_workspace_bytes(hq, n, block))
     return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "importance workspace too small");
-  float* E = static_cast<float*>(ws);
-  unsigned* rowmax = reinterpret_cast<unsigned*>(E + (size_t)hq * n * take);
+  float* L = static_cast<float*>(ws);
+  unsigned* rowmax = reinterpret_cast<unsigned*>(L + (size_t)hq * n * take);
   float* w = reinterpret_cast<float*>(rowmax + (size_t)hq * take);
   PBS_CUDA_CHECK(cudaMemsetAsync(rowmax, 0, sizeof(unsigned) * hq * take, st));
   const int group = hq / hkv;
+  const bool vec = (d % 16 == 0) && ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0);
   dim3 grid((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(take, kTile), (unsigned)hq);
-  if (dtype == PBS_DTYPE_BF16)
-    importance_logits_kernel<__nv_bfloat16, true><<<grid, kThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), group, n, d, take,
-        scale, E, rowmax);
-  else
-    importance_logits_kernel<float, false><<<grid, kThreads, 0, st>>>(
-        static_cast<const float*>(q), static_cast<const float*>(k), group, n, d, take, scale, E, rowmax);
+  if (dtype == PBS_DTYPE_BF16) {
+    auto qq = static_cast<const __nv_bfloat16*>(q);
+    auto kk = static_cast<const __nv_bfloat16*>(k);
+    if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
+    else importance_logits_kernel<__nv_bfloat16, true, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
+  } else {
+    auto qq = static_cast<const float*>(q);
+    auto kk = static_cast<const float*>(k);
+    if (vec) importance_logits_kernel<float, false, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
+    else importance_logits_kernel<float, false, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
+  }
   PBS_LAUNCH_CHECK("importance_logits_kernel");
-  const int64_t total = (int64_t)hq * n * take;
-  if (take == 128)
-    importance_exp_kernel_t<128><<<grid_for(total, 256), 256, 0, st>>>(E, rowmax, n, total);
-  else
-    importance_exp_generic_kernel<<<grid_for(total, 256), 256, 0, st>>>(E, rowmax, take, n, total);
-  PBS_LAUNCH_CHECK("importance_exp_kernel");
-  const int64_t rows = (int64_t)hq * take;
-  importance_denom_kernel<<<(unsigned)ceil_div(rows, 32), 32, 0, st>>>(E, hq, take, n, w);
-  PBS_LAUNCH_CHECK("importance_denom_kernel");
-  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, 128), (unsigned)hq), 128, 0, st>>>(E, w, take, n,
+  const size_t smem = sizeof(float) * kRing * kJT * 32 + 2 * kRing * sizeof(uint64_t);
+  static bool attr = false;
+  if (!attr) {
+    PBS_CUDA_CHECK(cudaFuncSetAttribute(importance_expsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  importance_expsum_kernel<<<dim3((unsigned)ceil_div(take, 32), (unsigned)hq), 32 * (1 + kExpWarps), smem, st>>>(
+      L, rowmax, take, n, w);
+  PBS_LAUNCH_CHECK("importance_expsum_kernel");
+  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, 128), (unsigned)hq), 128, 0, st>>>(L, rowmax, w, take, n,
                                                                                          scores);
   PBS_LAUNCH_CHECK("importance_scores_kernel");
   return PBS_OK;
@@ -461,9 +454,13 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
     qnorm_kernel<__nv_bfloat16><<<(unsigned)ceil_div((int64_t)hq * n, 128), 128, 0, st>>>(
         static_cast<const __nv_bfloat16*>(q), (int64_t)hq * n, d, qn);
     PBS_LAUNCH_CHECK("qnorm_kernel");
-    query_group_kernel<__nv_bfloat16>
-        <<<dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq), kThreads, 0,
-           st>>>(static_cast<const __nv_bfloat16*>(q), cent, qn, cn, hq / k_heads, n, d, tc, best);
+    const dim3 g3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq);
+    if (d % 16 == 0)
+      query_group_kernel<__nv_bfloat16, true><<<g3, xgemm::kThreads, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(q), cent, qn, cn, hq / k_heads, n, d, tc, best);
+    else
+      query_group_kernel<__nv_bfloat16, false><<<g3, xgemm::kThreads, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(q), cent, qn, cn, hq / k_heads, n, d, tc, best);
   } else {
     centroid_kernel<float><<<dim3((unsigned)tc, (unsigned)k_heads), 128, csmem, st>>>(
         static_cast<const float*>(k), n, d, block, tc, cent, cn);
@@ -471,9 +468,13 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
     qnorm_kernel<float><<<(unsigned)ceil_div((int64_t)hq * n, 128), 128, 0, st>>>(
         static_cast<const float*>(q), (int64_t)hq * n, d, qn);
     PBS_LAUNCH_CHECK("qnorm_kernel");
-    query_group_kernel<float>
-        <<<dim3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq), kThreads, 0,
-           st>>>(static_cast<const float*>(q), cent, qn, cn, hq / k_heads, n, d, tc, best);
+    const dim3 g3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq);
+    if (d % 16 == 0)
+      query_group_kernel<float, true><<<g3, xgemm::kThreads, 0, st>>>(static_cast<const float*>(q), cent, qn, cn,
+                                                                      hq / k_heads, n, d, tc, best);
+    else
+      query_group_kernel<float, false><<<g3, xgemm::kThreads, 0, st>>>(static_cast<const float*>(q), cent, qn, cn,
+                                                                       hq / k_heads, n, d, tc, best);
   }
   PBS_LAUNCH_CHECK("query_group_kernel");
   query_group_finalize_kernel<<<(unsigned)ceil_div((int64_t)hq * n, 256), 256, 0, st>>>(

@@ -34,11 +34,12 @@ size_t select_workspace_bytes(int hq, int64_t n, int d, int64_t block);
 // K or read directly from a per-q-head K'); k_perm == nullptr means identity.
 int launch_pool(const void* x, int dtype, int src_heads, int dst_heads, const int32_t* perm,
                 int64_t n, int d, int64_t block, float* pooled, cudaStream_t st);
-// block scores (+ optional dense score output) + selection + CSR
-int launch_score_select(const float* qbar, const float* kbar, int hq, int64_t t, int d,
-                        int64_t block, int64_t segment, float scale, double tau, int forced_first,
-                        int forced_band, float* scores_out, uint8_t* mask, int32_t* kv_idx,
-                        int32_t* kv_cnt, double* row_cov, cudaStream_t st);
+// block logits GEMM into logits_ws [hq, t, t] + softmax (+ optional dense
+// score output) + (select != 0) selection and CSR
+int launch_score_select(const float* qbar, const float* kbar, float* logits_ws, int hq, int64_t t, int d,
+                        int64_t block, int64_t segment, float scale, double tau, int forced_first, int forced_band,
+                        int select, float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
+                        double* row_cov, cudaStream_t st);
 // selection from precomputed scores (pbs_select_blocks)
 int launch_select_from_scores(const float* scores, int hq, int64_t t, int64_t block,
                               int64_t segment, double tau, int forced_first, int forced_band,

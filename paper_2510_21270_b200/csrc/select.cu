@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "exact_gemm.cuh"
 #include "expf_glibc.cuh"
 #include "kernels.h"
 
@@ -45,7 +46,42 @@ __global__ void pool_kernel(const T* __restrict__ x, int group, const int32_t* _
   }
 }
 
-constexpr int kSelThreads = 256;
+constexpr int kSelThreads = 128;
+
+// block logits: Lb[h][i][j] = (qbar_i . kbar_j) * s for the admissible prefix
+// j < A_i only (matrix.hpp:87-94 then block_selection.hpp:152-153).
+__global__ void __launch_bounds__(xgemm::kThreads) block_logits_kernel(const float* __restrict__ qbar,
+                                                                      const float* __restrict__ kbar, int64_t t, int d,
+                                                                      int64_t block, int64_t segment, float scale,
+                                                                      float* __restrict__ lb) {
+  __shared__ __align__(16) xgemm::Smem sm;
+  const int64_t h = blockIdx.z;
+  const int64_t i0 = (int64_t)blockIdx.x * xgemm::kTile;
+  const int64_t j0 = (int64_t)blockIdx.y * xgemm::kTile;
+  const int a_rows = (int)min64(xgemm::kTile, t - i0);
+  if (j0 >= admissible_prefix(i0 + a_rows - 1, t, block, segment)) return;  // tile above the band
+  const int b_rows = (int)min64(xgemm::kTile, t - j0);
+  float acc[8][8];
+  if (d % 16 == 0)
+    xgemm::tile<float, float, false, true>(qbar + (h * t + i0) * d, a_rows, kbar + (h * t + j0) * d, b_rows, d, acc,
+                                            sm);
+  else
+    xgemm::tile<float, float, false, false>(qbar + (h * t + i0) * d, a_rows, kbar + (h * t + j0) * d, b_rows, d,
+                                             acc, sm);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii) {
+    const int64_t i = i0 + xgemm::tile_row(ii, ty);
+    if (i >= i0 + a_rows) continue;
+    const int64_t a = admissible_prefix(i, t, block, segment);
+    float* row = lb + (h * t + i) * t;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int64_t j = j0 + xgemm::tile_row(jj, tx);
+      if (j < a) row[j] = __fmul_rn(acc[ii][jj], scale);
+    }
+  }
+}
 
 __device__ __forceinline__ float block_max(float v, float* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -63,47 +99,44 @@ __device__ __forceinline__ float block_max(float v, float* red) {
   return v;
 }
 
-// One CTA per (query block i, head h).  mode 0: compute scores from pooled
-// Q/K; mode 1: read precomputed scores (pbs_select_blocks).
-__global__ void __launch_bounds__(kSelThreads) score_select_kernel(
-    int mode, const float* __restrict__ qbar, const float* __restrict__ kbar,
-    const float* __restrict__ scores_in, int64_t t, int d, int64_t block, int64_t segment, float scale,
-    double tau, int forced_first, int forced_band, int pow2, float* __restrict__ scores_out,
-    uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx, int32_t* __restrict__ kv_cnt,
-    double* __restrict__ row_cov) {
+// One CTA per (query block i, head h).  mode 0: softmax of the block logits
+// row; mode 1: precomputed scores (pbs_select_blocks).  Sequential chains
+// (the softmax denominator, the double cumulative sum, the coverage sum) run
+// in warp 0 as a broadcast chain: every lane pulls element k with a shuffle
+// and performs the identical add, so the order is exactly the reference's.
+__global__ void __launch_bounds__(kSelThreads) select_kernel(
+    int mode, const float* __restrict__ rows_in, int64_t t, int64_t block, int64_t segment, double tau,
+    int forced_first, int forced_band, int select, float* __restrict__ scores_out, uint8_t* __restrict__ mask,
+    int32_t* __restrict__ kv_idx, int32_t* __restrict__ kv_cnt, double* __restrict__ row_cov) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t h = blockIdx.y, i = blockIdx.x;
+  const int64_t a = admissible_prefix(i, t, block, segment);
+  int pow2 = 1;
+  while (pow2 < a) pow2 <<= 1;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);  // [pow2]
-  float* sv = reinterpret_cast<float*>(keys + pow2);                      // [t]
-  float* qs = sv + t;                                                      // [d]
-  uint8_t* mrow = reinterpret_cast<uint8_t*>(qs + d);                      // [t]
+  float* sv = reinterpret_cast<float*>(keys + pow2);                      // [a]
+  uint8_t* mrow = reinterpret_cast<uint8_t*>(sv + ((a + 3) & ~3));        // [t]
   __shared__ float red[32];
   __shared__ float s_denom;
   __shared__ int s_take;
-
-  const int64_t h = blockIdx.y, i = blockIdx.x;
-  const int tid = threadIdx.x;
-  const int64_t a = admissible_prefix(i, t, block, segment);
-
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* in = rows_in + (h * t + i) * t;
+  for (int64_t j = tid; j < a; j += blockDim.x) sv[j] = in[j];
+  __syncthreads();
   if (mode == 0) {
-    for (int c = tid; c < d; c += blockDim.x) qs[c] = qbar[(h * t + i) * d + c];
-    __syncthreads();
-    const float* kb = kbar + h * t * d;
     float mx = -INFINITY;
-    for (int64_t j = tid; j < a; j += blockDim.x) {
-      const float* kr = kb + j * d;
-      float acc = 0.0f;
-      for (int c = 0; c < d; ++c) acc = __fadd_rn(acc, __fmul_rn(qs[c], kr[c]));
-      const float v = __fmul_rn(acc, scale);
-      sv[j] = v;
-      mx = fmaxf(mx, v);
-    }
+    for (int64_t j = tid; j < a; j += blockDim.x) mx = fmaxf(mx, sv[j]);
     mx = block_max(mx, red);
     for (int64_t j = tid; j < a; j += blockDim.x) sv[j] = expf_glibc(__fsub_rn(sv[j], mx));
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
       float denom = 0.0f;
-      for (int64_t j = 0; j < a; ++j) denom = __fadd_rn(denom, sv[j]);
-      s_denom = denom;
+      for (int64_t j0 = 0; j0 < a; j0 += 32) {
+        const float val = (j0 + lane < a) ? sv[j0 + lane] : 0.0f;
+        const int cnt = (int)min64(32, a - j0);
+        for (int kk = 0; kk < cnt; ++kk) denom = __fadd_rn(denom, __shfl_sync(0xffffffffu, val, kk));
+      }
+      if (lane == 0) s_denom = denom;
     }
     __syncthreads();
     const float denom = s_denom;
@@ -113,13 +146,10 @@ __global__ void __launch_bounds__(kSelThreads) score_select_kernel(
       float* so = scores_out + (h * t + i) * t;
       for (int64_t j = tid; j < t; j += blockDim.x) so[j] = j < a ? sv[j] : 0.0f;
     }
-  } else {
-    const float* si = scores_in + (h * t + i) * t;
-    for (int64_t j = tid; j < a; j += blockDim.x) sv[j] = si[j];
-    __syncthreads();
   }
+  if (!select) return;
 
-  // descending stable order of the admissible blocks
+  // descending stable order of the admissible blocks (composite unique keys)
   for (int j = tid; j < pow2; j += blockDim.x)
     keys[j] = j < a ? (((unsigned long long)(~float_order_key(sv[j])) << 32) | (unsigned)j) : ~0ull;
   for (int64_t j = tid; j < t; j += blockDim.x) mrow[j] = 0;
@@ -138,17 +168,23 @@ __global__ void __launch_bounds__(kSelThreads) score_select_kernel(
       }
       __syncthreads();
     }
-  if (tid == 0) {
+  if (warp == 0) {
     double cum = 0.0;
     int take = (int)a;  // fallback: every admissible block (line 188)
-    for (int k = 0; k < a; ++k) {
-      cum += (double)sv[keys[k] & 0xffffffffu];
-      if (cum >= tau) {
-        take = k + 1;
-        break;
+    bool done = false;
+    for (int64_t k0 = 0; k0 < a && !done; k0 += 32) {
+      const double val = (k0 + lane < a) ? (double)sv[keys[k0 + lane] & 0xffffffffu] : 0.0;
+      const int cnt = (int)min64(32, a - k0);
+      for (int kk = 0; kk < cnt; ++kk) {
+        cum += __shfl_sync(0xffffffffu, val, kk);
+        if (cum >= tau) {
+          take = (int)(k0 + kk + 1);
+          done = true;
+          break;
+        }
       }
     }
-    s_take = take;
+    if (lane == 0) s_take = take;
   }
   __syncthreads();
   const int take = s_take;
@@ -164,7 +200,7 @@ __global__ void __launch_bounds__(kSelThreads) score_select_kernel(
       } else {
         const int64_t per = segment / block;
         lo = (i / per) * per;
-        hi = min(lo + per, t);
+        hi = min64(lo + per, t);
       }
       for (int64_t j = lo; j < hi; ++j) mrow[j] = 1;
     }
@@ -175,37 +211,45 @@ __global__ void __launch_bounds__(kSelThreads) score_select_kernel(
     for (int64_t j = tid; j < t; j += blockDim.x) mo[j] = mrow[j];
   }
   // warp 0: ascending compaction of the selected blocks + coverage partial
-  if (tid < 32) {
+  // (pipeline.hpp:186-191, j ascending, double accumulation)
+  if (warp == 0) {
     int cnt = 0;
     double cov = 0.0;
     int32_t* out = kv_idx ? kv_idx + (h * t + i) * t : nullptr;
     for (int64_t j0 = 0; j0 < t; j0 += 32) {
-      const int64_t j = j0 + tid;
+      const int64_t j = j0 + lane;
       const bool sel = j < t && mrow[j];
       const unsigned bal = __ballot_sync(0xffffffffu, sel);
-      if (sel && out) out[cnt + __popc(bal & ((1u << tid) - 1))] = (int32_t)j;
+      if (sel && out) out[cnt + __popc(bal & ((1u << lane) - 1))] = (int32_t)j;
       cnt += __popc(bal);
+      if (mode == 0 && j0 < a) {
+        const double val = (sel && j < a) ? (double)sv[j] : 0.0;
+        unsigned bits = bal & (j0 + 32 <= a ? 0xffffffffu : ((1u << (a - j0)) - 1));
+        while (bits) {
+          const int kk = __ffs(bits) - 1;
+          bits &= bits - 1;
+          cov += __shfl_sync(0xffffffffu, val, kk);
+        }
+      }
     }
-    if (tid == 0) {
-      // pooled_score_coverage partial (pipeline.hpp:186-191), j ascending
-      if (mode == 0)
-        for (int64_t j = 0; j < a; ++j)
-          if (mrow[j]) cov += (double)sv[j];
+    if (lane == 0) {
       if (kv_cnt) kv_cnt[h * t + i] = cnt;
       if (row_cov) row_cov[h * t + i] = cov;
     }
   }
 }
 
-inline size_t select_smem(int64_t t, int d, int pow2) {
-  return (size_t)pow2 * 8 + (size_t)t * 4 + (size_t)d * 4 + (size_t)t + 16;
+inline size_t select_smem(int64_t t) {
+  int64_t pow2 = 1;
+  while (pow2 < t) pow2 <<= 1;
+  return (size_t)pow2 * 8 + (size_t)((t + 3) & ~3) * 4 + (size_t)t + 16;
 }
 
 }  // namespace
 
 size_t select_workspace_bytes(int hq, int64_t n, int d, int64_t block) {
   const int64_t t = ceil_div(n, block);
-  return 2 * (size_t)hq * t * d * 4 + (size_t)hq * t * 8 + 1024;
+  return 2 * (size_t)hq * t * d * 4 + (size_t)hq * t * t * 4 + (size_t)hq * t * 8 + 1024;
 }
 
 int launch_pool(const void* x, int dtype, int src_heads, int dst_heads, const int32_t* perm, int64_t n, int d,
@@ -224,40 +268,42 @@ int launch_pool(const void* x, int dtype, int src_heads, int dst_heads, const in
   return PBS_OK;
 }
 
-static int launch_select_common(int mode, const float* qbar, const float* kbar, const float* scores_in, int hq,
-                                int64_t t, int d, int64_t block, int64_t segment, float scale, double tau,
-                                int forced_first, int forced_band, float* scores_out, uint8_t* mask,
-                                int32_t* kv_idx, int32_t* kv_cnt, double* row_cov, cudaStream_t st) {
+static int launch_select_common(int mode, const float* rows_in, int hq, int64_t t, int64_t block,
+                                int64_t segment, double tau, int forced_first, int forced_band, int select,
+                                float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, double* row_cov,
+                                cudaStream_t st) {
   if (t == 0 || hq == 0) return PBS_OK;
   if (t > 16384) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "block grid wider than 16384 blocks");
-  int pow2 = 1;
-  while (pow2 < t) pow2 <<= 1;
-  const size_t smem = select_smem(t, d, pow2);
+  const size_t smem = select_smem(t);
   static bool attr_set = false;
   if (!attr_set) {
-    PBS_CUDA_CHECK(cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    PBS_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
-  score_select_kernel<<<dim3((unsigned)t, (unsigned)hq), kSelThreads, smem, st>>>(
-      mode, qbar, kbar, scores_in, t, d, block, segment, scale, tau, forced_first, forced_band, pow2, scores_out,
-      mask, kv_idx, kv_cnt, row_cov);
-  PBS_LAUNCH_CHECK("score_select_kernel");
+  select_kernel<<<dim3((unsigned)t, (unsigned)hq), kSelThreads, smem, st>>>(
+      mode, rows_in, t, block, segment, tau, forced_first, forced_band, select, scores_out, mask, kv_idx, kv_cnt,
+      row_cov);
+  PBS_LAUNCH_CHECK("select_kernel");
   return PBS_OK;
 }
 
-int launch_score_select(const float* qbar, const float* kbar, int hq, int64_t t, int d, int64_t block,
-                        int64_t segment, float scale, double tau, int forced_first, int forced_band,
-                        float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, double* row_cov,
-                        cudaStream_t st) {
-  return launch_select_common(0, qbar, kbar, nullptr, hq, t, d, block, segment, scale, tau, forced_first,
-                              forced_band, scores_out, mask, kv_idx, kv_cnt, row_cov, st);
+int launch_score_select(const float* qbar, const float* kbar, float* logits_ws, int hq, int64_t t, int d,
+                        int64_t block, int64_t segment, float scale, double tau, int forced_first, int forced_band,
+                        int select, float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
+                        double* row_cov, cudaStream_t st) {
+  if (t == 0 || hq == 0) return PBS_OK;
+  const dim3 grid((unsigned)ceil_div(t, xgemm::kTile), (unsigned)ceil_div(t, xgemm::kTile), (unsigned)hq);
+  block_logits_kernel<<<grid, xgemm::kThreads, 0, st>>>(qbar, kbar, t, d, block, segment, scale, logits_ws);
+  PBS_LAUNCH_CHECK("block_logits_kernel");
+  return launch_select_common(0, logits_ws, hq, t, block, segment, tau, forced_first, forced_band, select,
+                              scores_out, mask, kv_idx, kv_cnt, row_cov, st);
 }
 
 int launch_select_from_scores(const float* scores, int hq, int64_t t, int64_t block, int64_t segment, double tau,
                               int forced_first, int forced_band, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
                               cudaStream_t st) {
-  return launch_select_common(1, nullptr, nullptr, scores, hq, t, 0, block, segment, 0.0f, tau, forced_first,
-                              forced_band, nullptr, mask, kv_idx, kv_cnt, nullptr, st);
+  return launch_select_common(1, scores, hq, t, block, segment, tau, forced_first, forced_band, 1, nullptr, mask,
+                              kv_idx, kv_cnt, nullptr, st);
 }
 
 }  // namespace pbs_b200

@@ -136,7 +136,7 @@ def meanpool_block_scores(qp, kp, block_size, segment_size, scale=0.0):
     shape = make_shape(qp, kp)
     hq, n, d = qp.shape
     t = -(-n // block_size)
-    ws = workspace(2 * (hq * t * d * 4 + 256) + 4096, qp.device)
+    ws = workspace(2 * (hq * t * d * 4 + 256) + hq * t * t * 4 + 8192, qp.device)
     out = torch.empty(hq, t, t, dtype=torch.float32, device=qp.device)
     check(lib().pbs_meanpool_block_scores(_ptr(qp), _ptr(kp), C.byref(shape), block_size, segment_size, scale,
                                           _ptr(out), _ptr(ws), ws.numel(), _stream()))
