@@ -60,6 +60,18 @@ def parse():
     return ap.parse_args()
 
 
+# ------------------------------------------------------------------ sharding
+def shard_of(rank, world):
+    """Query heads split along KV groups: rank r owns KV heads
+    [r*HKV/world, (r+1)*HKV/world) and their HQ/HKV query heads each.
+    Returns (kv_head0, kv_heads, q_head0, q_heads)."""
+    if HKV % world:
+        raise ValueError(f"{HKV} KV groups do not split over {world} ranks")
+    kv_local = HKV // world
+    g = HQ // HKV
+    return rank * kv_local, kv_local, rank * kv_local * g, kv_local * g
+
+
 # ------------------------------------------------------------------ workload
 def make_inputs(torch, n, heads_q, heads_kv, kv_head0, device, seed=1234):
     """Synthetic vertical-lines Q/K/V for KV heads [kv_head0, kv_head0 + heads_kv).
@@ -226,10 +238,8 @@ def main():
 
     lib = ops.lib()
     n = args.seq
-    assert HKV % world == 0, "KV groups must split evenly across ranks"
-    kv_local = HKV // world
-    hq_local = kv_local * (HQ // HKV)
-    q, k, v = make_inputs(torch, n, hq_local, kv_local, rank * kv_local, "cuda")
+    kv0, kv_local, _, hq_local = shard_of(rank, world)
+    q, k, v = make_inputs(torch, n, hq_local, kv_local, kv0, "cuda")
     torch.cuda.synchronize()
     cfg = ops.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy="key_permute")
     ws = ops.workspace(ops.workspace_size(q, k, cfg))
@@ -298,13 +308,14 @@ def main():
     e2e = None
     if not args.no_e2e:
         hq_, hk_, hv_ = (x.cpu().pin_memory() for x in (q, k, v))
+        hout = torch.empty_like(hq_).pin_memory()
         for _ in range(2):
-            ops.pbs_attention_host(hq_, hk_, hv_, cfg)
+            ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout)
         barrier()
         t0 = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 5))
         for _ in range(e2e_steps):
-            ops.pbs_attention_host(hq_, hk_, hv_, cfg)
+            ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout)
         barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
         if world > 1:

@@ -21,7 +21,7 @@ namespace pbs_b200 {
 
 // __exp2f_data.tab (N = 32): asuint64(2^(i/32)) - (i << 47); identical to the
 // table found in this image's libm.so.6 (checked by oracle tests).
-static __constant__ uint64_t kExp2fTab[32] = {
+static __device__ const uint64_t kExp2fTab[32] = {
     0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
     0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
     0x3fef06fe0a31b715ULL, 0x3feef1a7373aa9cbULL, 0x3feedea64c123422ULL, 0x3feece086061892dULL,
@@ -31,15 +31,13 @@ static __constant__ uint64_t kExp2fTab[32] = {
     0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
     0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
 
-__device__ __forceinline__ float expf_glibc(float x) {
-  const uint32_t ux = __float_as_uint(x);
-  const uint32_t abstop = (ux >> 20) & 0x7ffu;
-  if (abstop >= 0x42bu) {                 // top12(88.0f): |x| >= 88 or x is nan/inf
-    if (ux == 0xff800000u) return 0.0f;   // -inf
-    if (abstop >= 0x7f8u) return x + x;   // inf or nan
-    if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);  // overflow -> +inf
-    if (x < -0x1.9fe368p6f) return 0.0f;                        // underflow -> +0
-  }
+// `tab` is the 2^(i/32) table: a shared-memory copy in the hot kernels (the
+// per-lane index makes constant-cache reads serialise), else the global one.
+__device__ __forceinline__ float expf_glibc(float x, const uint64_t* tab) {
+  // glibc evaluates the table + cubic formula for every x in [-103.97, 88.72]
+  // (including the subnormal-result range) and special-cases the rest; here
+  // the formula runs unconditionally and the special cases are selects, so
+  // independent calls interleave (no branches).
   const double xd = (double)x;
   const double kInvLn2N = 0x1.71547652b82fep+5;  // 32 / ln 2
   const double kShift = 0x1.8p+52;
@@ -47,7 +45,7 @@ __device__ __forceinline__ float expf_glibc(float x) {
   const uint64_t ki = (uint64_t)__double_as_longlong(kd);
   kd -= kShift;
   const double r = __fma_rn(kInvLn2N, xd, -kd);
-  uint64_t t = kExp2fTab[ki & 31u];
+  uint64_t t = tab[ki & 31u];
   t += ki << 47;
   const double s = __longlong_as_double((long long)t);
   const double z = __fma_rn(0x1.c6af84b912394p-20, r, 0x1.ebfce50fac4f3p-13);  // C0/N^3, C1/N^2
@@ -55,7 +53,19 @@ __device__ __forceinline__ float expf_glibc(float x) {
   double y = __fma_rn(0x1.62e42ff0c52d6p-6, r, 1.0);  // C2/N
   y = __fma_rn(z, r2, y);
   y = y * s;
-  return __double2float_rn(y);
+  float res = __double2float_rn(y);
+  // special cases of e_expf.c (|x| >= 88 branch)
+  res = (x > 0x1.62e42ep6f) ? __int_as_float(0x7f800000) : res;  // overflow -> +inf
+  res = (x < -0x1.9fe368p6f) ? 0.0f : res;                        // underflow (and -inf) -> +0
+  res = (x != x) ? x + x : res;                                   // nan
+  return res;
+}
+
+__device__ __forceinline__ float expf_glibc(float x) { return expf_glibc(x, kExp2fTab); }
+
+// stage the table in shared memory (call with all threads, then __syncthreads)
+__device__ __forceinline__ void load_exp2f_table(uint64_t* smem_tab) {
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) smem_tab[i] = kExp2fTab[i];
 }
 
 }  // namespace pbs_b200

@@ -32,11 +32,16 @@ namespace {
 using xgemm::kTile;
 using xgemm::tile_row;
 
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // K1a: L[h][j][i] = (q[r0+i] . k[j]) * scale and rowmax[h][i] = max_j L.
 // grid (ceil(N/128), ceil(take/128), Hq).  L is key-major ([j][i]) so that the
 // per-row denominator chains (K1bc) read 128-byte lines per step.
 template <typename T, bool kExact, bool kVec>
-__global__ void __launch_bounds__(xgemm::kThreads) importance_logits_kernel(
+__global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
     const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int d, int take, float scale,
     float* __restrict__ L, unsigned* __restrict__ rowmax) {
   __shared__ __align__(16) xgemm::Smem sm;
@@ -106,6 +111,8 @@ __global__ void __launch_bounds__(32 * (1 + kExpWarps)) importance_expsum_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = i0 + lane;
   const bool row_ok = i < take;
+  __shared__ uint64_t tab[32];
+  load_exp2f_table(tab);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -123,12 +130,14 @@ __global__ void __launch_bounds__(32 * (1 + kExpWarps)) importance_expsum_kernel
       ptx::mbar_wait(&empty[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
       const int64_t jb = t * kJT;
       const int cnt = (int)min64(kJT, n - jb);
-      // all loads of the tile first (64 x 128 B in flight per warp), then the exps
-      float xv[kJT];
-#pragma unroll
-      for (int jj = 0; jj < kJT; ++jj) xv[jj] = (row_ok && jj < cnt) ? __ldg(Lh + (jb + jj) * take + i) : 0.0f;
-#pragma unroll
-      for (int jj = 0; jj < kJT; ++jj) ring[slot][jj][lane] = expf_glibc(__fsub_rn(xv[jj], mx));
+      // the whole tile in flight (cp.async straight into the ring slot), then exps in place
+      for (int jj = 0; jj < cnt; ++jj) {
+        if (row_ok) cp_async4(&ring[slot][jj][lane], Lh + (jb + jj) * take + i);
+        else ring[slot][jj][lane] = 0.0f;
+      }
+      cp_async_wait_all();
+#pragma unroll 8
+      for (int jj = 0; jj < cnt; ++jj) ring[slot][jj][lane] = expf_glibc(__fsub_rn(ring[slot][jj][lane], mx), tab);
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&full[slot]);
     }
@@ -160,6 +169,8 @@ __global__ void __launch_bounds__(128) importance_scores_kernel(const float* __r
                                                                 float* __restrict__ scores) {
   __shared__ float tile[128][33];
   __shared__ float ws[32], ms[32];
+  __shared__ uint64_t tab[32];
+  load_exp2f_table(tab);
   const int h = blockIdx.y;
   const int64_t j0 = (int64_t)blockIdx.x * 128;
   const int tid = threadIdx.x;
@@ -173,17 +184,16 @@ __global__ void __launch_bounds__(128) importance_scores_kernel(const float* __r
     }
     __syncthreads();
     {
-      float xv[32];
       const int c = tid & 31;
-#pragma unroll
-      for (int u = 0; u < 32; ++u) {  // rows r = (tid >> 5) + 4u: loads first, then the exps
+      for (int u = 0; u < 32; ++u) {  // rows r = (tid >> 5) + 4u: the tile in flight, then the exps
         const int r = (tid >> 5) + 4 * u;
-        xv[u] = (c < ic && j0 + r < n) ? __ldg(Lh + (j0 + r) * take + i0 + c) : 0.0f;
+        if (c < ic && j0 + r < n) cp_async4(&tile[r][c], Lh + (j0 + r) * take + i0 + c);
       }
-#pragma unroll
+      cp_async_wait_all();
+#pragma unroll 8
       for (int u = 0; u < 32; ++u) {
         const int r = (tid >> 5) + 4 * u;
-        tile[r][c] = (c < ic && j0 + r < n) ? expf_glibc(__fsub_rn(xv[u], ms[c])) : 0.0f;
+        tile[r][c] = (c < ic && j0 + r < n) ? expf_glibc(__fsub_rn(tile[r][c], ms[c]), tab) : 0.0f;
       }
     }
     __syncthreads();

@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
   __shared__ float red[32];
   __shared__ float s_denom;
   __shared__ int s_take;
+  __shared__ uint64_t tab[32];
+  load_exp2f_table(tab);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* in = rows_in + (h * t + i) * t;
   for (int64_t j = tid; j < a; j += blockDim.x) sv[j] = in[j];
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     float mx = -INFINITY;
     for (int64_t j = tid; j < a; j += blockDim.x) mx = fmaxf(mx, sv[j]);
     mx = block_max(mx, red);
-    for (int64_t j = tid; j < a; j += blockDim.x) sv[j] = expf_glibc(__fsub_rn(sv[j], mx));
+    for (int64_t j = tid; j < a; j += blockDim.x) sv[j] = expf_glibc(__fsub_rn(sv[j], mx), tab);
     __syncthreads();
     if (warp == 0) {
       float denom = 0.0f;

@@ -225,8 +225,9 @@ def pbs_attention(q, k, v, cfg: PipelineConfig | None = None, report=True, out=N
     return PipelineResult(out, sigma, pi, mask, rep.as_dict() if rep else None)
 
 
-def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=False):
-    """The reference-facing call on HOST (CPU) tensors: copies in, runs, copies out."""
+def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=False, out=None):
+    """The reference-facing call on HOST (CPU) tensors: copies in, runs, copies out.
+    Pass pinned host tensors (and a pinned `out`) for full PCIe bandwidth."""
     cfg = cfg or make_config()
     for x in (q, k, v):
         if x.is_cuda or not x.is_contiguous():
@@ -234,7 +235,7 @@ def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=
     shape = make_shape(q, k)
     hq, n, d = q.shape
     t = -(-n // max(int(cfg.block_size), 1))
-    out = torch.empty_like(q)
+    out = torch.empty_like(q) if out is None else out
     sigma = pi = mask = None
     if return_perms:
         sigma = torch.empty(hq, n, dtype=torch.int32)

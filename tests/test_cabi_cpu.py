@@ -98,3 +98,22 @@ def test_product_has_no_oracle_dependency():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "pbs_oracle" not in text and "libpbsref" not in text, f
+
+
+def test_cpp_dropin_compiles_and_links(lib, tmp_path):
+    """A C++ caller of include/pbs_b200.hpp (the reference-facing wrapper)
+    compiles and links against libpbs_b200.so; without a GPU it must fail
+    loudly with a single-line E_* error, never fall back to the CPU."""
+    import subprocess
+
+    exe = tmp_path / "cpp_dropin"
+    pkg = os.path.join(ROOT, "paper_2510_21270_b200")
+    cmd = ["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "cpp_dropin.cpp"), "-L", pkg, "-lpbs_b200",
+           f"-Wl,-rpath,{pkg}", "-o", str(exe)]
+    subprocess.run(cmd, check=True)
+    import torch
+
+    if not torch.cuda.is_available():
+        r = subprocess.run([str(exe), "256", "64"], capture_output=True, text=True)
+        assert r.returncode == 1 and r.stderr.startswith("E_CUDA:") and r.stderr.count("\n") == 1

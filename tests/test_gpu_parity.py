@@ -236,3 +236,19 @@ def test_host_entry_matches_device_entry(ops):
     assert torch.equal(host.output, dev.output.cpu())
     assert torch.equal(host.pi, dev.pi.cpu())
     assert torch.equal(host.mask, dev.mask.cpu())
+
+
+def test_cpp_dropin_runs(ops, tmp_path):
+    """The C++ drop-in (examples/cpp_dropin.cpp) on the reference's configs[0] shape."""
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = tmp_path / "cpp_dropin"
+    pkg = os.path.join(ROOT, "paper_2510_21270_b200")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "cpp_dropin.cpp"), "-L", pkg, "-lpbs_b200",
+                    f"-Wl,-rpath,{pkg}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe), "4096", "128"], capture_output=True, text=True, check=True)
+    rep = json.loads(r.stdout)
+    assert 0 < rep["block_density"] <= rep["causal_density_baseline"] + 1e-9
