@@ -9,28 +9,31 @@
 // Tile: B = 128 query rows x 128 keys, d = 128, bf16 in, fp32 accumulate.
 // Persistent CTAs (one per SM) walk (head, query-block) work items, one KV
 // source at a time for L2 locality, heaviest query blocks first.
-// Warp roles (384 threads):
-//   warp 0       TMA producer: Q tile once per item, K/V tiles of each visited
-//                key block into a 2-stage ring (cp.async.bulk.tensor, SW128)
-//   warp 1       TMEM owner + MMA issuer (one elected lane): S_w = Q K^T and
-//                O_w += P_w V with tcgen05.mma, completion via tcgen05.commit
-//   warps 2..3   idle
-//   warps 4..7   softmax warpgroup 0: even-numbered visited key blocks
-//   warps 8..11  softmax warpgroup 1: odd-numbered visited key blocks
-// (each group's four warps cover the four TMEM lane quadrants, warp % 4)
-// The two softmax warpgroups split the key blocks of the SAME query tile
-// (split-KV inside the CTA): each owns a TMEM S buffer and a TMEM O
-// accumulator and keeps its own running (m, l), so two softmaxes are in
-// flight while the tensor core alternates between them; the epilogue merges
-// the two partial states (m = max, l and O rescaled by exp2(m_w - m)).
-// Per block a softmax thread (= one query row = one TMEM lane) reads its S
-// row from TMEM twice (a max pass over two 64-column halves, then an exp pass
-// over 32-column chunks, so the thread holds at most 64 scores and stays under
-// the 168-register budget of 384 threads), masks by original positions
-// (partial blocks only: a separate code path), applies the online
-// softmax in the exp2 domain with lazy rescaling (only when the running max
-// grows by > 8), writes P as bf16 into a SW128 shared-memory tile for the PV
-// MMA, and finally writes O / l to row out_rows[i] (the fused un-permute).
+// Warp roles (640 threads):
+//   warp 0       TMA producer for Q (once per item) and K (3-stage ring, a
+//                stage is released as soon as its QK^T completes)
+//   warp 2       TMA producer for V (2-stage ring, released after PV)
+//                (cp.async.bulk.tensor through 3-D [H, N, d] maps, SW128)
+//   warp 1       TMEM owner + MMA issuer (one elected lane):
+//                  S[e & 1] = Q K_e^T          (SS: Q, K K-major in smem)
+//                  O       += P_e V_e          (TS: P in TMEM, V MN-major smem)
+//                completion via tcgen05.commit onto mbarriers
+//   warp 3       idle
+//   warps 4..19  softmax: four threads per query row (TMEM lane), each owning
+//                32 of the 128 key columns (warps 4+4q..7+4q take columns
+//                [32q, 32q+32); each group of four covers the four TMEM lane
+//                quadrants, warp % 4).
+// TMEM holds S0 | S1 | O: S is double-buffered across visited blocks, so
+// QK^T of block e+1 runs on the tensor core while block e is in softmax, and
+// P_e is written back into TMEM over S_e (bf16, the TS-MMA A layout) and
+// consumed by the PV MMA from there (no shared-memory round trip for P).
+// Per block a softmax thread loads its 32 scores (tcgen05.ld 32x32b.x32),
+// masks partial blocks by original positions, exchanges its partial row max
+// with the row's other three threads through shared memory, applies the online softmax in the exp2
+// domain with lazy rescaling (O rescaled only when the running max grows by
+// more than 8), routes a quarter of the exp2s of full blocks through an
+// FMA-pipe polynomial, and stores P with tcgen05.st.  The epilogue writes
+// O / l straight to row out_rows[i] (the fused un-permute, pipeline.hpp:178).
 // Block classes follow AdmissibilityIndex::classify (attention.hpp:167-174):
 // per-block [min, max] of original positions; `none` blocks are skipped by
 // every role (an exact no-op, attention.hpp:286), `full` blocks skip the
@@ -53,20 +56,24 @@ namespace {
 constexpr int kBM = 128;      // query rows per tile (= block size B)
 constexpr int kBN = 128;      // keys per tile (= block size B)
 constexpr int kD = 128;       // head dim
-constexpr int kStages = 2;    // K/V ring depth
-constexpr int kThreads = 384;
+constexpr int kKStages = 3;   // K ring depth (freed as soon as QK^T completes)
+constexpr int kVStages = 2;   // V ring depth (freed when PV completes)
+constexpr int kSplit = 2;                         // threads per query row
+constexpr int kCols = kBN / kSplit;               // key columns per softmax thread
+constexpr int kSoftmaxThreads = 128 * kSplit;
+constexpr int kThreads = 128 + kSoftmaxThreads;
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
-constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O0 | O1
-__host__ __device__ constexpr uint32_t col_s(int w) { return w ? 128u : 0u; }
-__host__ __device__ constexpr uint32_t col_o(int w) { return w ? 384u : 256u; }
+constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | unused
+__host__ __device__ constexpr uint32_t col_s(int b) { return b ? 128u : 0u; }
+constexpr uint32_t kColO = 256;
 
 struct __align__(8) Barriers {
   uint64_t q_full, q_empty;
-  uint64_t kv_full[kStages], kv_empty[kStages];
-  uint64_t s_full[2], s_free[2];
-  uint64_t p_full[2], pv_done[2];
-  uint64_t o_free;
+  uint64_t k_full[kKStages], k_empty[kKStages];
+  uint64_t v_full[kVStages], v_empty[kVStages];
+  uint64_t s_full[2];
+  uint64_t p_full, pv_done, o_free;
   uint32_t tmem_base;
 };
 
@@ -74,10 +81,11 @@ struct SmemLayout {
   // 1024-byte aligned tiles (SW128 atoms)
   static constexpr int q = 0;
   static constexpr int k = q + kTileBytes;
-  static constexpr int v = k + kStages * kTileBytes;
-  static constexpr int p = v + kStages * kTileBytes;            // P0 | P1
-  static constexpr int korig = p + 2 * kTileBytes;              // int[2 WG][128]
-  static constexpr int bars = korig + 2 * 128 * 4;
+  static constexpr int v = k + kKStages * kTileBytes;
+  static constexpr int korig = v + kVStages * kTileBytes;      // int[128]
+  static constexpr int xmax = korig + 128 * 4;                 // float[2 parity][kSplit][128]
+  static constexpr int xl = xmax + 2 * kSplit * 128 * 4;       // float[kSplit][128]
+  static constexpr int bars = xl + kSplit * 128 * 4;
   static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
 };
 static_assert(SmemLayout::total <= 232448, "shared memory budget");
@@ -138,6 +146,27 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+
+// D[tmem] (+)= A[tmem] * B[smem]  (A = P written back into TMEM)
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+#define TMEM_ST16(taddr, r)                                                                                     \
+  asm volatile(                                                                                                 \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "  \
+      "%14, %15, %16};" ::"r"(taddr),                                                                          \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),        \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])                         \
+      : "memory")
 
 #define TMEM_LD32(taddr, r)                                                                                     \
   asm volatile(                                                                                                 \
@@ -285,6 +314,7 @@ __device__ __forceinline__ int block_class(const KernelArgs& a, const Item& it, 
 
 
 // visited-block cursor: dense causal lists are computed, sparse lists come from
+// visited-block cursor: dense causal lists are computed, sparse lists come from
 // the pre-pass (vis[h][qb][e] = kb | cls << 30), prefetched 32 entries per warp.
 struct Visit {
   const int32_t* list;
@@ -325,76 +355,40 @@ __device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, V
   cls = (int)(x >> 30);
 }
 
-// Softmax of one visited block for one query row (a TMEM lane).  kPartial
-// adds the original-position mask; full blocks also route every fourth exp2
-// through the FMA-pipe polynomial.  Pass 1: block max -> running max.
+// Pass 1 (per visited block): this thread's kCols scores, masked, and their max.
 template <bool kPartial>
-__device__ __forceinline__ void softmax_max(uint32_t tS, const int* ko, int qo, float sc, float& m,
-                                            bool& need_rescale, float& factor) {
+__device__ __forceinline__ float load_scores(uint32_t tS, const int* ko, int qo, uint32_t (&r)[kCols]) {
+#pragma unroll
+  for (int c = 0; c < kCols / 32; ++c) TMEM_LD32(tS + c * 32, (r + c * 32));
+  tmem_wait_ld();
   float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t r[64];
-    TMEM_LD32(tS + h * 64, r);
-    TMEM_LD32(tS + h * 64 + 32, (r + 32));
-    tmem_wait_ld();
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      float x = __uint_as_float(r[j]);
-      if (kPartial && ko[h * 64 + j] > qo) x = -INFINITY;
-      mx4[j & 3] = fmaxf(mx4[j & 3], x);
-    }
+  for (int j = 0; j < kCols; ++j) {
+    if (kPartial && ko[j] > qo) r[j] = 0xff800000u;  // -inf: inadmissible (attention.hpp:298-300)
+    mx4[j & 3] = fmaxf(mx4[j & 3], __uint_as_float(r[j]));
   }
-  const float bmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sc;
-  // online softmax in the log2 domain with lazy rescale (threshold 2^8)
-  const float m_new = fmaxf(m, bmax);
-  need_rescale = false;
-  factor = 1.0f;
-  if (m_new != -INFINITY) {
-    if (m == -INFINITY) {
-      m = m_new;  // O rows are still exactly 0 here
-    } else if (m_new > m + 8.0f) {
-      factor = ex2(m - m_new);
-      need_rescale = true;
-      m = m_new;
-    }
-  }
+  return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
 }
 
-// Pass 2: p = exp2(s * scale_log2 - m) -> bf16 -> the SW128 P tile; returns sum p.
-template <bool kPartial>
-__device__ __forceinline__ float softmax_emit(uint32_t tS, const int* ko, int qo, float sc, float m, uint32_t p_row,
-                                              int row) {
-  const float neg_m = (m == -INFINITY) ? 0.0f : -m;
+// Pass 2: p = exp2(s * scale_log2 - m) -> bf16, written into TMEM as the A
+// operand of the PV MMA (two keys per 32-bit column); returns sum p.
+template <bool kPoly>
+__device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, float neg_m, uint32_t tP) {
   float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint32_t r[32];
-    TMEM_LD32(tS + c * 32, r);
-    tmem_wait_ld();
+  for (int c = 0; c < kCols / 32; ++c) {
+    uint32_t pk[16];
 #pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {  // 16-byte chunks of the P row (8 keys)
-      uint32_t pk[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = q4 * 8 + 2 * u;
-        float x0 = __uint_as_float(r[j]), x1 = __uint_as_float(r[j + 1]);
-        if (kPartial) {
-          if (ko[c * 32 + j] > qo) x0 = -INFINITY;
-          if (ko[c * 32 + j + 1] > qo) x1 = -INFINITY;
-        }
-        const float p0 = ex2(fmaf(x0, sc, neg_m));
-        const float y1 = fmaf(x1, sc, neg_m);
-        const float p1 = (!kPartial && (u & 1)) ? exp2_poly(y1) : ex2(y1);
-        sum4[(2 * u) & 3] += p0;
-        sum4[(2 * u + 1) & 3] += p1;
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-        pk[u] = *reinterpret_cast<uint32_t*>(&b2);
-      }
-      const int c8 = c * 4 + q4;
-      const uint32_t addr = p_row + (c8 >> 3) * kPanelBytes + (((c8 & 7) ^ (row & 7)) << 4);
-      st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
+    for (int j = 0; j < 32; j += 2) {
+      const float p0 = ex2(fmaf(__uint_as_float(r[c * 32 + j]), sc, neg_m));
+      const float y1 = fmaf(__uint_as_float(r[c * 32 + j + 1]), sc, neg_m);
+      const float p1 = (kPoly && (j & 2)) ? exp2_poly(y1) : ex2(y1);
+      sum4[j & 3] += p0;
+      sum4[(j + 1) & 3] += p1;
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+      pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
     }
+    TMEM_ST16(tP + c * 16, pk);
   }
   return (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
 }
@@ -410,17 +404,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bar->q_full, 1);
     mbar_init(&bar->q_empty, 1);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&bar->kv_full[s], 1);
-      mbar_init(&bar->kv_empty[s], 1);
+    for (int s = 0; s < kKStages; ++s) {
+      mbar_init(&bar->k_full[s], 1);
+      mbar_init(&bar->k_empty[s], 1);
     }
-    for (int w = 0; w < 2; ++w) {
-      mbar_init(&bar->s_full[w], 1);
-      mbar_init(&bar->s_free[w], 128);
-      mbar_init(&bar->p_full[w], 128);
-      mbar_init(&bar->pv_done[w], 1);
+    for (int s = 0; s < kVStages; ++s) {
+      mbar_init(&bar->v_full[s], 1);
+      mbar_init(&bar->v_empty[s], 1);
     }
-    mbar_init(&bar->o_free, 256);
+    mbar_init(&bar->s_full[0], 1);
+    mbar_init(&bar->s_full[1], 1);
+    mbar_init(&bar->p_full, kSoftmaxThreads);
+    mbar_init(&bar->pv_done, 1);
+    mbar_init(&bar->o_free, kSoftmaxThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -433,14 +429,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
 
-  if (warp == 0) {
-    // ===================== TMA producer (lane 0 issues) =====================
-    uint32_t q_it = 0, kv_it = 0;
+  if (warp == 0 || warp == 2) {
+    // ===================== TMA producers (lane 0 issues) =====================
+    // warp 0: Q + K ring; warp 2: V ring
+    const bool kp = (warp == 0);
+    uint32_t q_it = 0, it_k = 0;
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
       const Item it = item_of(a, idx);
       const int kvh = it.h / a.group;
       Visit vis = visit_begin(a, it);
-      if (lane == 0) {
+      if (kp && lane == 0) {
         mbar_wait(&bar->q_empty, (q_it & 1) ^ 1);
         mbar_expect_tx(&bar->q_full, kTileBytes);
         for (int p = 0; p < 2; ++p)
@@ -451,65 +449,59 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t kb;
         int cls;
         visit_get(a, it, vis, e, lane, kb, cls);
-        const int s = kv_it % kStages;
         if (lane == 0) {
-          mbar_wait(&bar->kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
-          mbar_expect_tx(&bar->kv_full[s], 2 * kTileBytes);
-          unsigned char* kd = smem + SmemLayout::k + s * kTileBytes;
-          unsigned char* vd = smem + SmemLayout::v + s * kTileBytes;
-          for (int p = 0; p < 2; ++p) {
-            tma_load_3d(kd + p * kPanelBytes, &tm_k, &bar->kv_full[s], p * 64, (int)(kb * kBN), kvh);
-            tma_load_3d(vd + p * kPanelBytes, &tm_v, &bar->kv_full[s], p * 64, (int)(kb * kBN), kvh);
-          }
+          const int nst = kp ? kKStages : kVStages;
+          const int s = (int)(it_k % nst);
+          uint64_t* empty = kp ? &bar->k_empty[s] : &bar->v_empty[s];
+          uint64_t* full = kp ? &bar->k_full[s] : &bar->v_full[s];
+          mbar_wait(empty, ((it_k / nst) & 1) ^ 1);
+          mbar_expect_tx(full, kTileBytes);
+          unsigned char* dst = smem + (kp ? SmemLayout::k : SmemLayout::v) + s * kTileBytes;
+          for (int p = 0; p < 2; ++p)
+            tma_load_3d(dst + p * kPanelBytes, kp ? &tm_k : &tm_v, full, p * 64, (int)(kb * kBN), kvh);
         }
-        ++kv_it;
+        ++it_k;
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
-    const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major, V MN-major
+    const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
-    uint32_t q_it = 0, kv_it = 0, item_no = 0;
-    uint32_t s_cnt[2] = {0, 0}, pv_cnt[2] = {0, 0};
+    uint32_t q_it = 0, k_it = 0, v_it = 0, pv_it = 0, item_no = 0;
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x, ++item_no) {
       const Item it = item_of(a, idx);
       const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
       mbar_wait(&bar->q_full, q_it & 1);
       ++q_it;
-      uint32_t prev_stage = 0;
-      bool o_waited = false;
-      // PV of visited block number `pe` (warpgroup pe & 1)
-      auto issue_pv = [&](int pe, uint32_t stage) {
-        const int w = pe & 1;
-        mbar_wait(&bar->p_full[w], pv_cnt[w] & 1);
-        if (!o_waited) {  // the previous item's epilogue has read O0 and O1
-          mbar_wait(&bar->o_free, (item_no & 1) ^ 1);
-          o_waited = true;
-        }
+      // PV of visited block `pe` (its P lives in S[pe & 1])
+      auto issue_pv = [&](int pe) {
+        const uint32_t stage = v_it % kVStages;
+        mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
+        mbar_wait(&bar->p_full, pv_it & 1);
+        if (pe == 0) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // previous item's epilogue read O
         tc_fence_after();
         if (lane == 0) {
           const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
-          const uint32_t p_base = smem_u32(smem + SmemLayout::p + w * kTileBytes);
 #pragma unroll
           for (int k = 0; k < kBN / 16; ++k) {
-            // A = P [128 q x 128 kv] K-major SW128: panel k/4, +32 B per 16 keys
-            const uint64_t ad = sdesc(p_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
+            // A = P [128 q x 128 kv] in TMEM: 16 keys = 8 columns
             // B = V [128 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
             const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-            tc_mma(tmem + col_o(w), ad, bd, idesc_pv, (pe < 2 && k == 0) ? 0u : 1u);
+            tc_mma_ts(tmem + kColO, tmem + col_s(pe & 1) + k * 8, bd, idesc_pv, (pe == 0 && k == 0) ? 0u : 1u);
           }
-          tc_commit(&bar->pv_done[w]);
-          tc_commit(&bar->kv_empty[stage]);
+          tc_commit(&bar->pv_done);
+          tc_commit(&bar->v_empty[stage]);
         }
         __syncwarp();
-        ++pv_cnt[w];
+        ++pv_it;
+        ++v_it;
       };
       for (int e = 0; e < len; ++e) {
-        const uint32_t stage = kv_it % kStages;
-        const int w = e & 1;
-        mbar_wait(&bar->kv_full[stage], (kv_it / kStages) & 1);
-        mbar_wait(&bar->s_free[w], (s_cnt[w] & 1) ^ 1);
+        const uint32_t stage = k_it % kKStages;
+        mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
+        // S[e & 1] held P_{e-2}; its PV was issued before this point and
+        // tcgen05.mma executes in issue order
         tc_fence_after();
         if (lane == 0) {
           const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
@@ -517,129 +509,138 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kD / 16; ++k) {
             const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
             const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-            tc_mma(tmem + col_s(w), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
+            tc_mma(tmem + col_s(e & 1), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
           }
-          tc_commit(&bar->s_full[w]);
+          tc_commit(&bar->s_full[e & 1]);
+          tc_commit(&bar->k_empty[stage]);
         }
         __syncwarp();
-        ++s_cnt[w];
-        ++kv_it;
-        if (e > 0) issue_pv(e - 1, prev_stage);
-        prev_stage = stage;
+        ++k_it;
+        if (e > 0) issue_pv(e - 1);
       }
       // Q is free once every S of this item has completed
       if (lane == 0) tc_commit(&bar->q_empty);
       __syncwarp();
-      if (len > 0) issue_pv(len - 1, prev_stage);
-      if (!o_waited) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // keep the o_free phases in step
+      if (len > 0) issue_pv(len - 1);
+      else mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // keep the o_free phases in step
     }
   } else if (warp >= 4) {
-    // ===================== softmax warpgroups =====================
-    const int wg = (warp - 4) >> 2;      // 0 or 1
+    // ===================== softmax: kSplit threads per row =====================
+    const int part = (warp - 4) >> 2;    // key columns [kCols part, kCols part + kCols)
     const int quad = warp & 3;           // TMEM lane quadrant of this warp
     const int row = quad * 32 + lane;    // query row within the tile
-    const int wg_tid = threadIdx.x - 128 - wg * 128;  // 0..127
+    const int st = threadIdx.x - 128;    // 0..255
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_off + col_s(wg);
-    const uint32_t tO = tmem + lane_off + col_o(wg);
-    const uint32_t p_row = smem_u32(smem + SmemLayout::p + wg * kTileBytes) + row * 128;
-    int* ko = reinterpret_cast<int*>(smem + SmemLayout::korig) + wg * 128;
-    float* xch = reinterpret_cast<float*>(smem + SmemLayout::p);  // epilogue exchange (P0 region)
+    int* ko_all = reinterpret_cast<int*>(smem + SmemLayout::korig);
+    const int* ko = ko_all + part * kCols;
+    float* xmax = reinterpret_cast<float*>(smem + SmemLayout::xmax);
+    float* xl = reinterpret_cast<float*>(smem + SmemLayout::xl);
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
-    uint32_t s_cnt = 0, pv_cnt = 0;
+    uint32_t s_cnt[2] = {0, 0};
+    uint32_t pv_cnt = 0, blk = 0;
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
       const Item it = item_of(a, idx);
       Visit vis = visit_begin(a, it);
       const int64_t i = it.qb * kBM + row;
       const bool valid = i < a.n;
       const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
-      float m = -INFINITY;  // running max in the log2 domain
-      float l = 0.0f;
-      int mine = 0;
-      for (int e = wg; e < vis.len; e += 2) {
+      float m = -INFINITY;  // running max in the log2 domain (shared by the row's threads)
+      float l = 0.0f;       // this thread's partial running sum
+      for (int e = 0; e < vis.len; ++e, ++blk) {
         int64_t kb;
         int cls;
         visit_get(a, it, vis, e, lane, kb, cls);
         if (cls == 1) {
-          const int64_t j = kb * kBN + wg_tid;
-          int v = 0x7fffffff;
-          if (j < a.n) v = a.k_orig ? a.k_orig[(int64_t)it.h * a.n + j] : (int)j;
-          if (!any_mask && j < a.n) v = -1;  // unmasked: only the ragged tail
-          ko[wg_tid] = v;
-          named_bar_sync(1 + wg, 128);
+          if (st < 128) {
+            const int64_t j = kb * kBN + st;
+            int v = 0x7fffffff;
+            if (j < a.n) v = a.k_orig ? a.k_orig[(int64_t)it.h * a.n + j] : (int)j;
+            if (!any_mask && j < a.n) v = -1;  // unmasked: only the ragged tail
+            ko_all[st] = v;
+          }
+          named_bar_sync(1, kSoftmaxThreads);
         }
-        mbar_wait(&bar->s_full[wg], s_cnt & 1);
+        const int b = e & 1;
+        mbar_wait(&bar->s_full[b], s_cnt[b] & 1);
+        ++s_cnt[b];
         tc_fence_after();
-        ++s_cnt;
-        bool need_rescale;
-        float factor;
-        if (cls == 1) softmax_max<true>(tS, ko, qo, sc, m, need_rescale, factor);
-        else softmax_max<false>(tS, ko, qo, sc, m, need_rescale, factor);
-        // the previous PV of this warpgroup must be complete before P_w is
-        // overwritten or O_w rescaled
-        if (mine > 0) {
-          mbar_wait(&bar->pv_done[wg], pv_cnt & 1);
+        const uint32_t tS = tmem + lane_off + col_s(b) + part * kCols;
+        uint32_t r[kCols];
+        const float hmax = (cls == 1) ? load_scores<true>(tS, ko, qo, r) : load_scores<false>(tS, ko, qo, r);
+        // the row's threads agree on the block max
+        float* xm = xmax + (blk & 1) * (kSplit * 128);
+        xm[part * 128 + row] = hmax;
+        named_bar_sync(2, kSoftmaxThreads);
+        float bm = xm[row];
+#pragma unroll
+        for (int q2 = 1; q2 < kSplit; ++q2) bm = fmaxf(bm, xm[q2 * 128 + row]);
+        const float bmax = bm * sc;
+        // online softmax in the log2 domain with lazy rescale (threshold 2^8)
+        const float m_new = fmaxf(m, bmax);
+        bool need_rescale = false;
+        float factor = 1.0f;
+        if (m_new != -INFINITY) {
+          if (m == -INFINITY) {
+            m = m_new;  // O rows are still exactly 0 here
+          } else if (m_new > m + 8.0f) {
+            factor = ex2(m - m_new);
+            need_rescale = true;
+            m = m_new;
+          }
+        }
+        const float neg_m = (m == -INFINITY) ? 0.0f : -m;
+        // P over the consumed S columns: keys [kCols part, +kCols) -> columns [kCols/2 part, +kCols/2)
+        const uint32_t tP = tmem + lane_off + col_s(b) + part * (kCols / 2);
+        const float rs = (cls == 2) ? emit_p<true>(r, sc, neg_m, tP) : emit_p<false>(r, sc, neg_m, tP);
+        tmem_wait_st();
+        if (cls == 1) named_bar_sync(1, kSoftmaxThreads);  // ko[] may be refilled after this
+        // O may only be rescaled once the previous PV has completed
+        if (e > 0) {
+          mbar_wait(&bar->pv_done, pv_cnt & 1);
           ++pv_cnt;
         }
         if (__any_sync(0xffffffffu, need_rescale)) {
           tc_fence_after();
+          const uint32_t tO = tmem + lane_off + kColO + part * kCols;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            TMEM_LD32(tO + c * 32, r);
+          for (int c = 0; c < kCols / 32; ++c) {
+            uint32_t o[32];
+            TMEM_LD32(tO + c * 32, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * factor);
-            TMEM_ST32(tO + c * 32, r);
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * factor);
+            TMEM_ST32(tO + c * 32, o);
           }
           tmem_wait_st();
-          l *= factor;
         }
-        if (cls == 1) {
-          l += softmax_emit<true>(tS, ko, qo, sc, m, p_row, row);
-          named_bar_sync(1 + wg, 128);  // ko[] may be refilled after this
-        } else {
-          l += softmax_emit<false>(tS, ko, qo, sc, m, p_row, row);
-        }
+        l = l * factor + rs;
         tc_fence_before();
-        mbar_arrive(&bar->s_free[wg]);  // S_w fully read: the next QK^T may overwrite it
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_fence_before();
-        mbar_arrive(&bar->p_full[wg]);
-        ++mine;
+        mbar_arrive(&bar->p_full);
       }
-      // ---- epilogue: merge the two partial states, O / l -> out[out_rows[i]]
-      if (mine > 0) {
-        mbar_wait(&bar->pv_done[wg], pv_cnt & 1);
+      // ---- epilogue: O / l -> out[out_rows[i]] (each thread writes its kCols columns)
+      if (vis.len > 0) {
+        mbar_wait(&bar->pv_done, pv_cnt & 1);
         ++pv_cnt;
       }
-      // both warpgroups' P tiles are free now (their last PV is done): reuse P0 to exchange (m, l)
-      named_bar_sync(3, 256);
-      xch[wg * 256 + row] = m;
-      xch[wg * 256 + 128 + row] = l;
-      named_bar_sync(3, 256);
-      const float m0 = xch[row], l0 = xch[128 + row], m1 = xch[256 + row], l1 = xch[384 + row];
-      const float mt = fmaxf(m0, m1);
-      const float f0 = (m0 == -INFINITY) ? 0.0f : ex2(m0 - mt);
-      const float f1 = (m1 == -INFINITY) ? 0.0f : ex2(m1 - mt);
-      const float lt = l0 * f0 + l1 * f1;
+      xl[part * 128 + row] = l;
+      named_bar_sync(2, kSoftmaxThreads);
+      float lt = xl[row];
+#pragma unroll
+      for (int q2 = 1; q2 < kSplit; ++q2) lt += xl[q2 * 128 + row];
+      named_bar_sync(2, kSoftmaxThreads);  // xl is rewritten by the next item
       tc_fence_after();
-      const bool degenerate = valid && !(lt > 0.0f);
-      if (degenerate && a.status && wg == 0) {
+      if (valid && !(lt > 0.0f) && a.status && part == 0) {
         a.status[0] = 1;
         atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
       }
       const float inv = (lt > 0.0f) ? 1.0f / lt : 0.0f;
-      const float g0 = f0 * inv, g1 = f1 * inv;
       const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
-      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + wg * 64;
+      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + part * kCols;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {  // this warpgroup writes columns [64 wg, 64 wg + 64)
-        const uint32_t col = wg * 64 + c * 32;
-        uint32_t r0[32], r1[32];
-        TMEM_LD32(tmem + lane_off + col_o(0) + col, r0);
-        TMEM_LD32(tmem + lane_off + col_o(1) + col, r1);
+      for (int c = 0; c < kCols / 32; ++c) {
+        uint32_t o[32];
+        TMEM_LD32(tmem + lane_off + kColO + part * kCols + c * 32, o);
         tmem_wait_ld();
         if (valid && lt > 0.0f) {
 #pragma unroll
@@ -648,13 +649,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int w2 = 0; w2 < 4; ++w2) {
               const int j = u * 8 + 2 * w2;
-              float o0 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(r0[j]) * g0;
-              float o1 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(r0[j + 1]) * g0;
-              if (m1 != -INFINITY) {
-                o0 = fmaf(__uint_as_float(r1[j]), g1, o0);
-                o1 = fmaf(__uint_as_float(r1[j + 1]), g1, o1);
-              }
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(o0, o1);
+              __nv_bfloat162 b2 =
+                  __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
               pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
             }
             *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -663,7 +659,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bar->o_free);
-      named_bar_sync(3, 256);  // the exchange area (P0) is reused by the next item's softmax
     }
   }
   tc_fence_before();
