@@ -31,8 +31,8 @@
 // masks partial blocks by original positions, exchanges its partial row max
 // with the row's other three threads through shared memory, applies the online softmax in the exp2
 // domain with lazy rescaling (O rescaled only when the running max grows by
-// more than 8), routes a quarter of the exp2s of full blocks through an
-// FMA-pipe polynomial, and stores P with tcgen05.st.  The epilogue writes
+// more than 8), and stores P with tcgen05.st (exp2 on the MUFU; an FMA-pipe
+// polynomial path, kPolyExp2, is kept for MUFU-bound configurations).  The epilogue writes
 // O / l straight to row out_rows[i] (the fused un-permute, pipeline.hpp:178).
 // Block classes follow AdmissibilityIndex::classify (attention.hpp:167-174):
 // per-block [min, max] of original positions; `none` blocks are skipped by
@@ -59,6 +59,10 @@ constexpr int kD = 128;       // head dim
 constexpr int kKStages = 3;   // K ring depth (freed as soon as QK^T completes)
 constexpr int kVStages = 2;   // V ring depth (freed when PV completes)
 constexpr int kSplit = 2;                         // threads per query row
+// route every fourth exp2 of a block through the FMA-pipe polynomial; off:
+// with two threads per row the MUFU is ~1/3 busy and the polynomial's ~10
+// instructions per element cost more issue slots than they save
+constexpr bool kPolyExp2 = false;
 constexpr int kCols = kBN / kSplit;               // key columns per softmax thread
 constexpr int kSoftmaxThreads = 128 * kSplit;
 constexpr int kThreads = 128 + kSoftmaxThreads;
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float neg_m = (m == -INFINITY) ? 0.0f : -m;
         // P over the consumed S columns: keys [kCols part, +kCols) -> columns [kCols/2 part, +kCols/2)
         const uint32_t tP = tmem + lane_off + col_s(b) + part * (kCols / 2);
-        const float rs = (cls == 2) ? emit_p<true>(r, sc, neg_m, tP) : emit_p<false>(r, sc, neg_m, tP);
+        const float rs = emit_p<kPolyExp2>(r, sc, neg_m, tP);
         tmem_wait_st();
         if (cls == 1) named_bar_sync(1, kSoftmaxThreads);  // ko[] may be refilled after this
         // O may only be rescaled once the previous PV has completed
