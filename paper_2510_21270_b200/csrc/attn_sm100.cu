@@ -15,25 +15,30 @@
 //   warp 2       TMA producer for V (2-stage ring, released after PV)
 //                (cp.async.bulk.tensor through 3-D [H, N, d] maps, SW128)
 //   warp 1       TMEM owner + MMA issuer (one elected lane):
-//                  S[e & 1] = Q K_e^T          (SS: Q, K K-major in smem)
-//                  O       += P_e V_e          (TS: P in TMEM, V MN-major smem)
+//                  S[e & 1] = Q K_e^T               (SS: Q, K K-major in smem)
+//                  O0 += P_e[:, :64]  V_e[:64]      (TS: P in TMEM,
+//                  O1 += P_e[:, 64:]  V_e[64:]       V MN-major in smem)
 //                completion via tcgen05.commit onto mbarriers
 //   warp 3       idle
-//   warps 4..19  softmax: four threads per query row (TMEM lane), each owning
-//                32 of the 128 key columns (warps 4+4q..7+4q take columns
-//                [32q, 32q+32); each group of four covers the four TMEM lane
-//                quadrants, warp % 4).
-// TMEM holds S0 | S1 | O: S is double-buffered across visited blocks, so
+//   warps 4..11  softmax: two threads per query row (TMEM lane), each owning
+//                64 of the 128 key columns of every block (warps 4..7 the low
+//                half, 8..11 the high half; each group of four covers the
+//                four TMEM lane quadrants, warp % 4).
+// TMEM holds S0 | S1 | O0 | O1: S is double-buffered across visited blocks, so
 // QK^T of block e+1 runs on the tensor core while block e is in softmax, and
 // P_e is written back into TMEM over S_e (bf16, the TS-MMA A layout) and
 // consumed by the PV MMA from there (no shared-memory round trip for P).
-// Per block a softmax thread loads its 32 scores (tcgen05.ld 32x32b.x32),
-// masks partial blocks by original positions, exchanges its partial row max
-// with the row's other three threads through shared memory, applies the online softmax in the exp2
-// domain with lazy rescaling (O rescaled only when the running max grows by
-// more than 8), and stores P with tcgen05.st (exp2 on the MUFU; an FMA-pipe
-// polynomial path, kPolyExp2, is kept for MUFU-bound configurations).  The epilogue writes
-// O / l straight to row out_rows[i] (the fused un-permute, pipeline.hpp:178).
+// Each half-row thread runs its own online softmax over its 64 keys of every
+// block (its own running max m and sum l; the PV is split into the two key
+// halves accumulating into O0 / O1), so there is no per-block exchange between
+// threads; the epilogue merges the two states once (m = max, O and l scaled by
+// exp2(m_h - m)).  Per block a thread loads its 64 scores (2 x tcgen05.ld
+// 32x32b.x32), masks partial blocks by original positions, applies the online
+// softmax in the exp2 domain with lazy rescaling (O_h rescaled only when the
+// running max grows by more than 8), and stores P with tcgen05.st (exp2 on the
+// MUFU; an FMA-pipe polynomial path, kPolyExp2, is kept for MUFU-bound
+// configurations).  The epilogue writes O / l straight to row out_rows[i]
+// (the fused un-permute, pipeline.hpp:178).
 // Block classes follow AdmissibilityIndex::classify (attention.hpp:167-174):
 // per-block [min, max] of original positions; `none` blocks are skipped by
 // every role (an exact no-op, attention.hpp:286), `full` blocks skip the
@@ -68,9 +73,9 @@ constexpr int kSoftmaxThreads = 128 * kSplit;
 constexpr int kThreads = 128 + kSoftmaxThreads;
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
-constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | unused
+constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O0 | O1
 __host__ __device__ constexpr uint32_t col_s(int b) { return b ? 128u : 0u; }
-constexpr uint32_t kColO = 256;
+__host__ __device__ constexpr uint32_t col_o(int h) { return h ? 384u : 256u; }
 
 struct __align__(8) Barriers {
   uint64_t q_full, q_empty;
@@ -87,9 +92,8 @@ struct SmemLayout {
   static constexpr int k = q + kTileBytes;
   static constexpr int v = k + kKStages * kTileBytes;
   static constexpr int korig = v + kVStages * kTileBytes;      // int[128]
-  static constexpr int xmax = korig + 128 * 4;                 // float[2 parity][kSplit][128]
-  static constexpr int xl = xmax + 2 * kSplit * 128 * 4;       // float[kSplit][128]
-  static constexpr int bars = xl + kSplit * 128 * 4;
+  static constexpr int xch = korig + 128 * 4;                  // float[2 (m, l)][2 half][128] epilogue exchange
+  static constexpr int bars = xch + 2 * 2 * 128 * 4;
   static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
 };
 static_assert(SmemLayout::total <= 232448, "shared memory budget");
@@ -489,10 +493,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
 #pragma unroll
           for (int k = 0; k < kBN / 16; ++k) {
-            // A = P [128 q x 128 kv] in TMEM: 16 keys = 8 columns
-            // B = V [128 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
+            // keys [0, 64) accumulate into O0, keys [64, 128) into O1: each half
+            // of the row runs its own online softmax (no per-block exchange)
+            // A = P [128 q x 16 kv] in TMEM: 16 keys = 8 columns
+            // B = V [16 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
             const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-            tc_mma_ts(tmem + kColO, tmem + col_s(pe & 1) + k * 8, bd, idesc_pv, (pe == 0 && k == 0) ? 0u : 1u);
+            tc_mma_ts(tmem + col_o(k >> 2), tmem + col_s(pe & 1) + k * 8, bd, idesc_pv,
+                      (pe == 0 && (k & 3) == 0) ? 0u : 1u);
           }
           tc_commit(&bar->pv_done);
           tc_commit(&bar->v_empty[stage]);
@@ -537,8 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     int* ko_all = reinterpret_cast<int*>(smem + SmemLayout::korig);
     const int* ko = ko_all + part * kCols;
-    float* xmax = reinterpret_cast<float*>(smem + SmemLayout::xmax);
-    float* xl = reinterpret_cast<float*>(smem + SmemLayout::xl);
+    float* xch = reinterpret_cast<float*>(smem + SmemLayout::xch);
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
     uint32_t s_cnt[2] = {0, 0};
@@ -549,8 +555,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t i = it.qb * kBM + row;
       const bool valid = i < a.n;
       const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
-      float m = -INFINITY;  // running max in the log2 domain (shared by the row's threads)
-      float l = 0.0f;       // this thread's partial running sum
+      float m = -INFINITY;  // this half-row's running max (log2 domain)
+      float l = 0.0f;       // this half-row's running sum
       for (int e = 0; e < vis.len; ++e, ++blk) {
         int64_t kb;
         int cls;
@@ -572,21 +578,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tS = tmem + lane_off + col_s(b) + part * kCols;
         uint32_t r[kCols];
         const float hmax = (cls == 1) ? load_scores<true>(tS, ko, qo, r) : load_scores<false>(tS, ko, qo, r);
-        // the row's threads agree on the block max
-        float* xm = xmax + (blk & 1) * (kSplit * 128);
-        xm[part * 128 + row] = hmax;
-        named_bar_sync(2, kSoftmaxThreads);
-        float bm = xm[row];
-#pragma unroll
-        for (int q2 = 1; q2 < kSplit; ++q2) bm = fmaxf(bm, xm[q2 * 128 + row]);
-        const float bmax = bm * sc;
-        // online softmax in the log2 domain with lazy rescale (threshold 2^8)
+        // this half-row's own online softmax (log2 domain, lazy rescale by 2^8)
+        const float bmax = hmax * sc;
         const float m_new = fmaxf(m, bmax);
         bool need_rescale = false;
         float factor = 1.0f;
         if (m_new != -INFINITY) {
           if (m == -INFINITY) {
-            m = m_new;  // O rows are still exactly 0 here
+            m = m_new;  // this half's O rows are still exactly 0 here
           } else if (m_new > m + 8.0f) {
             factor = ex2(m - m_new);
             need_rescale = true;
@@ -606,9 +605,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (__any_sync(0xffffffffu, need_rescale)) {
           tc_fence_after();
-          const uint32_t tO = tmem + lane_off + kColO + part * kCols;
+          const uint32_t tO = tmem + lane_off + col_o(part);
 #pragma unroll
-          for (int c = 0; c < kCols / 32; ++c) {
+          for (int c = 0; c < kD / 32; ++c) {
             uint32_t o[32];
             TMEM_LD32(tO + c * 32, o);
             tmem_wait_ld();
@@ -622,29 +621,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&bar->p_full);
       }
-      // ---- epilogue: O / l -> out[out_rows[i]] (each thread writes its kCols columns)
+      // ---- epilogue: merge the two half-row states, O / l -> out[out_rows[i]]
       if (vis.len > 0) {
         mbar_wait(&bar->pv_done, pv_cnt & 1);
         ++pv_cnt;
       }
-      xl[part * 128 + row] = l;
+      xch[part * 128 + row] = m;
+      xch[256 + part * 128 + row] = l;
       named_bar_sync(2, kSoftmaxThreads);
-      float lt = xl[row];
-#pragma unroll
-      for (int q2 = 1; q2 < kSplit; ++q2) lt += xl[q2 * 128 + row];
-      named_bar_sync(2, kSoftmaxThreads);  // xl is rewritten by the next item
+      const float m0 = xch[row], m1 = xch[128 + row], l0 = xch[256 + row], l1 = xch[384 + row];
+      named_bar_sync(2, kSoftmaxThreads);  // xch is rewritten by the next item
+      const float mt = fmaxf(m0, m1);
+      const float f0 = (m0 == -INFINITY) ? 0.0f : ex2(m0 - mt);
+      const float f1 = (m1 == -INFINITY) ? 0.0f : ex2(m1 - mt);
+      const float lt = l0 * f0 + l1 * f1;
       tc_fence_after();
       if (valid && !(lt > 0.0f) && a.status && part == 0) {
         a.status[0] = 1;
         atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
       }
       const float inv = (lt > 0.0f) ? 1.0f / lt : 0.0f;
+      const float g0 = f0 * inv, g1 = f1 * inv;
       const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
       __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + part * kCols;
 #pragma unroll
-      for (int c = 0; c < kCols / 32; ++c) {
-        uint32_t o[32];
-        TMEM_LD32(tmem + lane_off + kColO + part * kCols + c * 32, o);
+      for (int c = 0; c < kCols / 32; ++c) {  // this thread writes output columns [kCols part, +kCols)
+        uint32_t o0[32], o1[32];
+        TMEM_LD32(tmem + lane_off + col_o(0) + part * kCols + c * 32, o0);
+        TMEM_LD32(tmem + lane_off + col_o(1) + part * kCols + c * 32, o1);
         tmem_wait_ld();
         if (valid && lt > 0.0f) {
 #pragma unroll
@@ -653,8 +657,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int w2 = 0; w2 < 4; ++w2) {
               const int j = u * 8 + 2 * w2;
-              __nv_bfloat162 b2 =
-                  __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
+              float v0 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j]) * g0;
+              float v1 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j + 1]) * g0;
+              if (m1 != -INFINITY) {
+                v0 = fmaf(__uint_as_float(o1[j]), g1, v0);
+                v1 = fmaf(__uint_as_float(o1[j + 1]), g1, v1);
+              }
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
               pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
             }
             *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
