@@ -465,15 +465,33 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
   return PBS_OK;
 }
 
-// ---- host-buffer entry: library-owned device arena --------------------------
+// ---- host-buffer entry: library-owned device arena, pipelined by KV group ------
+//
+// The host call streams the problem through the GPU one KV group (a KV head
+// and its Hq/Hkv query heads) at a time, double-buffered on three streams:
+// H2D of group g+1 and D2H of group g-1 overlap the compute of group g.  Heads
+// share nothing, so the result is identical to one whole call.
 namespace {
 struct Arena {
   std::mutex mu;
   void* ptr = nullptr;
   size_t bytes = 0;
   int device = -1;
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
 };
 Arena g_arena;
+
+int arena_streams(Arena& A) {
+  if (A.st[0]) return PBS_OK;
+  for (auto& x : A.st) PBS_CUDA_CHECK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_in[i], cudaEventDisableTiming));
+    PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_done[i], cudaEventDisableTiming));
+    PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_out[i], cudaEventDisableTiming));
+  }
+  return PBS_OK;
+}
 }  // namespace
 
 int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_shape* shape,
@@ -482,51 +500,109 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   if (int rc = check_shape(shape)) return rc;
   if (int rc = check_cfg(cfg)) return rc;
   const int64_t n = shape->seq_len, hq = shape->num_q_heads, hkv = shape->num_kv_heads, d = shape->head_dim;
+  const int64_t g = hq / hkv;  // query heads per chunk (one KV head)
   const int64_t t = ceil_div(n, cfg->block_size);
   const size_t es = esize_of(shape->dtype);
-  const size_t qb = (size_t)hq * n * d * es, kvb = (size_t)hkv * n * d * es;
-  const size_t ws = pbs_workspace_size(shape, cfg);
-  const size_t need = al(qb) * 2 + al(kvb) * 2 + al((size_t)hq * n * 4) * 2 + al((size_t)hq * t * t) + ws;
+  pbs_shape cs = *shape;  // chunk shape
+  cs.num_q_heads = (int32_t)g;
+  cs.num_kv_heads = 1;
+  const size_t qb = (size_t)g * n * d * es, kvb = (size_t)n * d * es;
+  const size_t pb = (size_t)g * n * 4, mb = (size_t)g * t * t;
+  const size_t ws = pbs_workspace_size(&cs, cfg);
+  const size_t slot = al(qb) * 2 + al(kvb) * 2 + al(pb) * 2 + al(mb) + al(ws);
+  const int nslots = hkv > 1 ? 2 : 1;
   std::lock_guard<std::mutex> lk(g_arena.mu);
+  Arena& A = g_arena;
   int dev = 0;
   PBS_CUDA_CHECK(cudaGetDevice(&dev));
-  if (g_arena.bytes < need || g_arena.device != dev) {
-    if (g_arena.ptr) cudaFree(g_arena.ptr);
-    g_arena.ptr = nullptr;
-    g_arena.bytes = 0;
-    PBS_CUDA_CHECK(cudaMalloc(&g_arena.ptr, need));
-    g_arena.bytes = need;
-    g_arena.device = dev;
+  if (A.device != dev) {  // streams and events belong to the device they were made on
+    A.st[0] = A.st[1] = A.st[2] = nullptr;
+    if (A.ptr) cudaFree(A.ptr);
+    A.ptr = nullptr;
+    A.bytes = 0;
   }
-  char* base = static_cast<char*>(g_arena.ptr);
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    char* p = base + off;
-    off += al(bytes);
-    return p;
+  if (int rc = arena_streams(A)) return rc;
+  if (A.bytes < slot * nslots) {
+    if (A.ptr) cudaFree(A.ptr);
+    A.ptr = nullptr;
+    A.bytes = 0;
+    PBS_CUDA_CHECK(cudaMalloc(&A.ptr, slot * nslots));
+    A.bytes = slot * nslots;
+  }
+  A.device = dev;
+  struct Slot {
+    char *q, *k, *v, *out, *ws;
+    int32_t *sig, *pi;
+    uint8_t* mask;
+  } sl[2];
+  for (int i = 0; i < nslots; ++i) {
+    char* p = static_cast<char*>(A.ptr) + (size_t)i * slot;
+    auto take = [&](size_t bytes) {
+      char* r = p;
+      p += al(bytes);
+      return r;
+    };
+    sl[i].q = take(qb);
+    sl[i].k = take(kvb);
+    sl[i].v = take(kvb);
+    sl[i].out = take(qb);
+    sl[i].sig = reinterpret_cast<int32_t*>(take(pb));
+    sl[i].pi = reinterpret_cast<int32_t*>(take(pb));
+    sl[i].mask = reinterpret_cast<uint8_t*>(take(mb));
+    sl[i].ws = take(ws);
+  }
+  cudaStream_t s_in = A.st[0], s_run = A.st[1], s_out = A.st[2];
+  const char* hq_ = static_cast<const char*>(q);
+  const char* hk_ = static_cast<const char*>(k);
+  const char* hv_ = static_cast<const char*>(v);
+  char* ho_ = static_cast<char*>(out);
+  pbs_report total{};
+  double dens = 0.0, cov = 0.0;
+  auto copy_in = [&](int64_t c) -> int {
+    Slot& S = sl[c % nslots];
+    if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_in, A.ev_out[c % nslots], 0));  // slot drained
+    PBS_CUDA_CHECK(cudaMemcpyAsync(S.q, hq_ + (size_t)c * qb, qb, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaMemcpyAsync(S.k, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaMemcpyAsync(S.v, hv_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_in[c % nslots], s_in));
+    return PBS_OK;
   };
-  void* dq = take(qb);
-  void* dk = take(kvb);
-  void* dv = take(kvb);
-  void* dout = take(qb);
-  int32_t* dsig = reinterpret_cast<int32_t*>(take((size_t)hq * n * 4));
-  int32_t* dpi = reinterpret_cast<int32_t*>(take((size_t)hq * n * 4));
-  uint8_t* dmask = reinterpret_cast<uint8_t*>(take((size_t)hq * t * t));
-  void* dws = take(ws);
-  cudaStream_t st = 0;
-  PBS_CUDA_CHECK(cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, st));
-  PBS_CUDA_CHECK(cudaMemcpyAsync(dk, k, kvb, cudaMemcpyHostToDevice, st));
-  PBS_CUDA_CHECK(cudaMemcpyAsync(dv, v, kvb, cudaMemcpyHostToDevice, st));
-  pbs_report local{};
-  if (int rc = pbs_attention(dq, dk, dv, shape, cfg, dout, sigma ? dsig : nullptr, pi ? dpi : nullptr,
-                             mask ? dmask : nullptr, dws, ws, &local, st))
-    return rc;
-  PBS_CUDA_CHECK(cudaMemcpyAsync(out, dout, qb, cudaMemcpyDeviceToHost, st));
-  if (sigma) PBS_CUDA_CHECK(cudaMemcpyAsync(sigma, dsig, (size_t)hq * n * 4, cudaMemcpyDeviceToHost, st));
-  if (pi) PBS_CUDA_CHECK(cudaMemcpyAsync(pi, dpi, (size_t)hq * n * 4, cudaMemcpyDeviceToHost, st));
-  if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask, dmask, (size_t)hq * t * t, cudaMemcpyDeviceToHost, st));
-  PBS_CUDA_CHECK(cudaStreamSynchronize(st));
-  if (report) *report = local;
+  if (int rc = copy_in(0)) return rc;
+  for (int64_t c = 0; c < hkv; ++c) {
+    Slot& S = sl[c % nslots];
+    if (c + 1 < hkv && nslots > 1)
+      if (int rc = copy_in(c + 1)) return rc;
+    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_in[c % nslots], 0));
+    pbs_report r{};
+    if (int rc = pbs_attention(S.q, S.k, S.v, &cs, cfg, S.out, sigma ? S.sig : nullptr, pi ? S.pi : nullptr,
+                               mask ? S.mask : nullptr, S.ws, ws, &r, s_run))
+      return rc;  // (the report path synchronises s_run)
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_done[c % nslots], s_run));
+    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_out, A.ev_done[c % nslots], 0));
+    PBS_CUDA_CHECK(cudaMemcpyAsync(ho_ + (size_t)c * qb, S.out, qb, cudaMemcpyDeviceToHost, s_out));
+    if (sigma) PBS_CUDA_CHECK(cudaMemcpyAsync(sigma + (size_t)c * g * n, S.sig, pb, cudaMemcpyDeviceToHost, s_out));
+    if (pi) PBS_CUDA_CHECK(cudaMemcpyAsync(pi + (size_t)c * g * n, S.pi, pb, cudaMemcpyDeviceToHost, s_out));
+    if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask + (size_t)c * mb, S.mask, mb, cudaMemcpyDeviceToHost, s_out));
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_out[c % nslots], s_out));
+    if (nslots == 1 && c + 1 < hkv) {
+      PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
+      if (int rc = copy_in(c + 1)) return rc;
+    }
+    total.selected_blocks += r.selected_blocks;
+    total.total_admissible_blocks += r.total_admissible_blocks;
+    dens += r.block_density;
+    cov += r.pooled_score_coverage;
+    total.causal_density_baseline = r.causal_density_baseline;
+    total.estimate_us += r.estimate_us;
+    total.permute_us += r.permute_us;
+    total.select_us += r.select_us;
+    total.attention_us += r.attention_us;
+    total.unpermute_us += r.unpermute_us;
+  }
+  PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
+  total.block_density = dens / (double)hkv;
+  total.pooled_score_coverage = cov / (double)hkv;
+  if (report) *report = total;
   return PBS_OK;
 }
 
