@@ -29,6 +29,32 @@ struct Smem {
 
 __device__ __forceinline__ int tile_row(int idx, int t) { return (idx < 4 ? 0 : 64) + t * 4 + (idx & 3); }
 
+// Two independent outputs per instruction (Blackwell f32x2 SIMD, FFMA2) for
+// the exact-product path: each lane is an ordinary IEEE round-to-nearest FMA,
+// so every output keeps its own sequential accumulation order.
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
+}
+template <bool kExact>
+__device__ __forceinline__ void acc2(float& c0, float& c1, float a, float b0, float b1) {
+  if (kExact) {
+    uint64_t rc = pk2(c0, c1);
+    const uint64_t ra = pk2(a, a), rb = pk2(b0, b1);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rc) : "l"(ra), "l"(rb));
+    upk2(rc, c0, c1);
+  } else {
+    // scalar: ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2, which
+    // would change the rounding of non-exact products
+    c0 = __fadd_rn(c0, __fmul_rn(a, b0));
+    c1 = __fadd_rn(c1, __fmul_rn(a, b1));
+  }
+}
+
 // load 8 consecutive elements [c, c+8) of row `row` (zero beyond rows/d)
 template <typename T, bool kVec>
 __device__ __forceinline__ void load8(const T* __restrict__ base, int rows, int d, int row, int c, float (&v)[8]) {
@@ -101,10 +127,7 @@ __device__ __forceinline__ void tile(const TA* __restrict__ a_base, int a_rows, 
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (kExact) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-          else acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
-        }
+        for (int j = 0; j < 8; j += 2) acc2<kExact>(acc[i][j], acc[i][j + 1], a[i], b[j], b[j + 1]);
     }
     if (more) {
 #pragma unroll

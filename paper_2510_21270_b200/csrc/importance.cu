@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
 // w_i = 1 / (denom * take) (line 174).  One CTA per (head, 32 rows): warps
 // 1..kExpWarps compute the exps of 64-key tiles into a shared-memory ring;
 // warp 0 is the adder, one dependent chain of N fp32 adds per lane.
-constexpr int kExpWarps = 8;
-constexpr int kJT = 64;            // keys per ring tile
+constexpr int kExpWarps = 16;
+constexpr int kJT = 32;            // keys per ring tile
 constexpr int kRing = 2 * kExpWarps;
 
 __global__ void __launch_bounds__(32 * (1 + kExpWarps)) importance_expsum_kernel(
