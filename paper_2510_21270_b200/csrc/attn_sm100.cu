@@ -52,6 +52,7 @@
 
 #include <cstdio>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -83,7 +84,7 @@ struct __align__(8) Barriers {
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[2];
-  uint64_t p_full, pv_done, o_free;
+  uint64_t p_full, pv_done, o_full, o_free;
   uint32_t tmem_base;
 };
 
@@ -155,6 +156,44 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// Warp-collective forms: the whole (converged) warp executes these and one
+// elected lane issues.  Keeping the issuing code warp-uniform lets the
+// descriptors live in uniform registers; a `lane == 0` branch instead makes the
+// compiler wrap every tcgen05.mma in a waterfall loop of R2UR conversions.
+__device__ __forceinline__ void tc_mma_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 // D[tmem] (+)= A[smem] * B[smem]
@@ -278,7 +317,14 @@ struct KernelArgs {
   int64_t items;
   const int32_t* vis;   // [hq][t][t] visited blocks (kb | cls << 30), sparse mode
   const int32_t* nvis;  // [hq][t]
+  unsigned long long* trace;  // debug timeline of CTA 0 (PBS_ATTN_TRACE), else nullptr
 };
+
+// debug timeline (PBS_ATTN_TRACE=file): CTA 0 records clock64 at pipeline events
+constexpr int kTraceEvents = 4096;
+__device__ __forceinline__ void trace_event(const KernelArgs& a, int kind, uint32_t n) {
+  if (a.trace && blockIdx.x == 0 && n < kTraceEvents) a.trace[kind * kTraceEvents + n] = clock64();
+}
 
 struct Item {
   int h;
@@ -439,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bar->s_full[1], 1);
     mbar_init(&bar->p_full, kSoftmaxThreads);
     mbar_init(&bar->pv_done, 1);
+    mbar_init(&bar->o_full, 1);
     mbar_init(&bar->o_free, kSoftmaxThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -487,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (warp-collective, one elected lane) ========
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
@@ -502,24 +549,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t stage = v_it % kVStages;
         mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
         mbar_wait(&bar->p_full, pv_it & 1);
+        if (lane == 0) trace_event(a, 0, pv_it);
         if (pe == 0) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // previous item's epilogue read O
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
+        const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
 #pragma unroll
-          for (int k = 0; k < kBN / 16; ++k) {
-            // keys [0, 64) accumulate into O0, keys [64, 128) into O1: each half
-            // of the row runs its own online softmax (no per-block exchange)
-            // A = P [128 q x 16 kv] in TMEM: 16 keys = 8 columns
-            // B = V [16 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
-            const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-            tc_mma_ts(tmem + col_o(k >> 2), tmem + col_s(pe & 1) + k * 8, bd, idesc_pv,
+        for (int k = 0; k < kBN / 16; ++k) {
+          // keys [0, 64) accumulate into O0, keys [64, 128) into O1: each half
+          // of the row runs its own online softmax (no per-block exchange)
+          // A = P [128 q x 16 kv] in TMEM: 16 keys = 8 columns
+          // B = V [16 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
+          const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
+          tc_mma_ts_w(tmem + col_o(k >> 2), tmem + col_s(pe & 1) + (k >> 2) * kCols + (k & 3) * 8, bd, idesc_pv,
                       (pe == 0 && (k & 3) == 0) ? 0u : 1u);
-          }
-          tc_commit(&bar->pv_done);
-          tc_commit(&bar->v_empty[stage]);
         }
-        __syncwarp();
+        if (lane == 0) trace_event(a, 2, pv_it);
+        tc_commit_w(&bar->pv_done);
+        tc_commit_w(&bar->v_empty[stage]);
+        if (pe == len - 1) tc_commit_w(&bar->o_full);
         ++pv_it;
         ++v_it;
       };
@@ -529,24 +576,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         // S[e & 1] held P_{e-2}; its PV was issued before this point and
         // tcgen05.mma executes in issue order
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
+        const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
 #pragma unroll
-          for (int k = 0; k < kD / 16; ++k) {
-            const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-            const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-            tc_mma(tmem + col_s(e & 1), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
-          }
-          tc_commit(&bar->s_full[e & 1]);
-          tc_commit(&bar->k_empty[stage]);
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
+          tc_mma_w(tmem + col_s(e & 1), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
         }
-        __syncwarp();
+        if (lane == 0) trace_event(a, 4, k_it);
+        tc_commit_w(&bar->s_full[e & 1]);
+        tc_commit_w(&bar->k_empty[stage]);
         ++k_it;
         if (e > 0) issue_pv(e - 1);
       }
       // Q is free once every S of this item has completed
-      if (lane == 0) tc_commit(&bar->q_empty);
-      __syncwarp();
+      tc_commit_w(&bar->q_empty);
       if (len > 0) issue_pv(len - 1);
       else mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // keep the o_free phases in step
     }
@@ -563,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
     uint32_t s_cnt[2] = {0, 0};
-    uint32_t pv_cnt = 0, blk = 0;
+    uint32_t blk = 0, o_cnt = 0;
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
       const Item it = item_of(a, idx);
       Visit vis = visit_begin(a, it);
@@ -588,11 +632,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int b = e & 1;
         mbar_wait(&bar->s_full[b], s_cnt[b] & 1);
+        if (st == 0) trace_event(a, 6, blk);
         ++s_cnt[b];
         tc_fence_after();
         const uint32_t tS = tmem + lane_off + col_s(b) + part * kCols;
         uint32_t r[kCols];
         const float hmax = (cls == 1) ? load_scores<true>(tS, ko, qo, r) : load_scores<false>(tS, ko, qo, r);
+        if (st == 0) trace_event(a, 10, blk);
         // this half-row's own online softmax (log2 domain, lazy rescale by 2^8)
         const float bmax = hmax * sc;
         const float m_new = fmaxf(m, bmax);
@@ -608,17 +654,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         const float neg_m = (m == -INFINITY) ? 0.0f : -m;
-        // P over the consumed S columns: keys [kCols part, +kCols) -> columns [kCols/2 part, +kCols/2)
-        const uint32_t tP = tmem + lane_off + col_s(b) + part * (kCols / 2);
+        // P over this thread's own consumed S columns: keys [kCols part, +kCols) ->
+        // columns [kCols part, +kCols/2).  (Packing both halves into columns
+        // [0, kCols) would let part 1 overwrite scores part 0 has not read yet.)
+        const uint32_t tP = tmem + lane_off + col_s(b) + part * kCols;
         const float rs = emit_p<kPolyExp2>(r, sc, neg_m, tP);
         tmem_wait_st();
+        if (st == 0) trace_event(a, 8, blk);
         if (cls == 1) named_bar_sync(1, kSoftmaxThreads);  // ko[] may be refilled after this
-        // O may only be rescaled once the previous PV has completed
-        if (e > 0) {
-          mbar_wait(&bar->pv_done, pv_cnt & 1);
-          ++pv_cnt;
-        }
+        // O may only be rescaled once the previous PV has completed.  Only then is
+        // pv_done waited on: S(blk) ready implies PV(blk - 2) complete (it was
+        // issued before QK(blk)) and PV(blk) cannot complete before this thread's
+        // P, so the barrier has completed blk - 1 or blk phases and the parity of
+        // PV(blk - 1) identifies it without waiting on every block.
         if (__any_sync(0xffffffffu, need_rescale)) {
+          mbar_wait(&bar->pv_done, (blk - 1) & 1);
           tc_fence_after();
           const uint32_t tO = tmem + lane_off + col_o(part);
 #pragma unroll
@@ -637,9 +687,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&bar->p_full);
       }
       // ---- epilogue: merge the two half-row states, O / l -> out[out_rows[i]]
-      if (vis.len > 0) {
-        mbar_wait(&bar->pv_done, pv_cnt & 1);
-        ++pv_cnt;
+      if (vis.len > 0) {  // the item's last PV (o_full: one phase per non-empty item)
+        mbar_wait(&bar->o_full, o_cnt & 1);
+        ++o_cnt;
       }
       xch[part * 128 + row] = m;
       xch[256 + part * 128 + row] = l;
@@ -860,9 +910,25 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
     PBS_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     attr = true;
   }
-  const int grid = (int)min64(a.items, g_num_sms);
+  int grid = (int)min64(a.items, g_num_sms);
+  if (const char* e = getenv("PBS_ATTN_GRID")) grid = (int)min64(grid, atoi(e) > 0 ? atoi(e) : grid);  // debug
+  const char* trace_path = getenv("PBS_ATTN_TRACE");
+  if (trace_path) {
+    PBS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), 12 * kTraceEvents * 8, st));
+    PBS_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 12 * kTraceEvents * 8, st));
+  }
   attn_sm100_kernel<<<grid, kThreads, SmemLayout::total, st>>>(mq, mk, mv, a);
   PBS_LAUNCH_CHECK("attn_sm100_kernel");
+  if (trace_path) {  // debug only: synchronous dump of CTA 0's timeline
+    std::vector<unsigned long long> h(12 * kTraceEvents);
+    PBS_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    PBS_CUDA_CHECK(cudaStreamSynchronize(st));
+    PBS_CUDA_CHECK(cudaFree(a.trace));
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   if (own) PBS_CUDA_CHECK(cudaFreeAsync(own, st));
   return PBS_OK;
 }

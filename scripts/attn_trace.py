@@ -1,0 +1,44 @@
+"""Debug: record CTA 0's attention pipeline timeline (PBS_ATTN_TRACE) on the
+C3 bench workload and print per-block phase latencies (SM clocks)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2510_21270_b200 import ops  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
+dense = len(sys.argv) > 2 and sys.argv[2] == "dense"
+q, k, v = bench.make_inputs(torch, n, 32, 8, 0, "cuda")
+cfg = ops.make_config(block_size=128, segment_size=256, tau=0.9, strategy="key_permute")
+path = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "attn_trace.bin")
+os.makedirs(os.path.dirname(path), exist_ok=True)
+for _ in range(2):
+    (ops.dense_causal_attention(q, k, v) if dense else ops.pbs_attention(q, k, v, cfg, report=False))
+torch.cuda.synchronize()
+os.environ["PBS_ATTN_TRACE"] = path
+(ops.dense_causal_attention(q, k, v) if dense else ops.pbs_attention(q, k, v, cfg, report=False))
+torch.cuda.synchronize()
+t = np.fromfile(path, dtype=np.uint64).reshape(12, 4096).astype(np.int64)
+names = ["mma_sees_p0", "mma_sees_p1", "pv_issue0", "pv_issue1", "qk_issue0", "qk_issue1", "s_ready0", "s_ready1",
+         "p_done0", "p_done1", "max_done0", "max_done1"]
+t0 = t[t > 0].min()
+lo, hi = 100, 1500
+sr, pd, md, qk, pv, ms = (t[6], t[8], t[10], t[4], t[2], t[0])
+b = np.arange(lo, hi)
+ok = (sr[b] > 0) & (pd[b] > 0) & (qk[b] > 0) & (pv[b] > 0) & (ms[b] > 0) & (sr[b + 1] > 0)
+b = b[ok]
+print(f"CTA 0: blocks {len(b)}")
+print("  softmax: S ready -> max done  ", np.median(md[b] - sr[b]))
+print("  softmax: max done -> P written", np.median(pd[b] - md[b]))
+print("  P written -> MMA sees P       ", np.median(ms[b] - pd[b]))
+print("  (old design) S(b+1) ready - P(b) written", np.median(sr[b + 1] - pd[b]))
+print("  QK(b+1) issued -> S(b+1) ready (old: b+1)", np.median(sr[b + 1] - qk[b + 1]))
+print("  MMA sees P -> PV issued       ", np.median(pv[b] - ms[b]))
+print("  PV(b) issued -> QK(b+1) issued", np.median(qk[b + 1] - pv[b]))
+print("  QK(b+1) issued -> S(b+1) ready", np.median(sr[b + 1] - qk[b + 1]))
+print("  period S(b) -> S(b+1)         ", np.median(sr[b + 1] - sr[b]))

@@ -252,3 +252,80 @@ def test_cpp_dropin_runs(ops, tmp_path):
     r = subprocess.run([str(exe), "4096", "128"], capture_output=True, text=True, check=True)
     rep = json.loads(r.stdout)
     assert 0 < rep["block_density"] <= rep["causal_density_baseline"] + 1e-9
+
+
+def _torch_block_sparse_ref(q, k, v, b, kv_idx, kv_cnt, q_orig, k_orig, out_rows, scale):
+    """attention_block_sparse (attention.hpp:259-310) restated densely in torch fp32:
+    selected blocks AND the element mask k_orig[j] <= q_orig[i], then the row scatter."""
+    hq, n, d = q.shape
+    g = hq // k.shape[0]
+    t = -(-n // b)
+    out = torch.empty(hq, n, d, dtype=torch.float32, device=q.device)
+    for h in range(hq):
+        blk = torch.zeros(t, t, dtype=torch.bool, device=q.device)
+        for i in range(t):
+            c = int(kv_cnt[h, i])
+            blk[i, kv_idx[h, i, :c].long()] = True
+        sel = blk.repeat_interleave(b, 0).repeat_interleave(b, 1)[:n, :n]
+        adm = k_orig[h][None, :] <= q_orig[h][:, None]
+        s = (q[h].float() @ k[h // g].float().T) * scale
+        s = s.masked_fill(~(sel & adm), float("-inf"))
+        o = torch.softmax(s, dim=1) @ v[h // g].float()
+        out[h, out_rows[h].long()] = o
+    return out
+
+
+@pytest.mark.parametrize("n", [4096 + 50, 6144])
+def test_block_sparse_many_items_per_slot(ops, n):
+    """Several (head, query block) items per tensor-core slot (32 heads x 33-48
+    blocks over 148 x 2 slots): Q reloads, O hand-over between items, K/V ring
+    wrap-around, ragged final blocks, permuted original positions and the fused
+    un-permute, against a dense torch restatement."""
+    torch.manual_seed(0)
+    hq, hkv, d, b, seg = 32, 8, 128, 128, 256
+    t = -(-n // b)
+    q = torch.randn(hq, n, d, device="cuda").to(torch.bfloat16)
+    k = torch.randn(hkv, n, d, device="cuda").to(torch.bfloat16)
+    v = torch.randn(hkv, n, d, device="cuda").to(torch.bfloat16)
+    # pi: a random permutation inside every segment (build_key_permutation's shape); sigma random too
+    def seg_perm():
+        p = torch.arange(n, device="cuda")
+        for s0 in range(0, n - n % seg, seg):
+            p[s0:s0 + seg] = s0 + torch.randperm(seg, device="cuda")
+        return p
+    k_orig = torch.stack([seg_perm() for _ in range(hq)]).int()
+    q_orig = torch.stack([seg_perm() for _ in range(hq)]).int()
+    # lists: block 0 + the segment band (the forced policy) + a random admissible subset, ascending
+    kv_idx = torch.zeros(hq, t, t, dtype=torch.int32)
+    kv_cnt = torch.zeros(hq, t, dtype=torch.int32)
+    g = torch.Generator().manual_seed(1)
+    per = seg // b
+    for h in range(hq):
+        for i in range(t):
+            end = min((i // per + 1) * per, t)
+            keep = torch.rand(end, generator=g) < 0.4
+            keep[0] = True
+            keep[(i // per) * per:end] = True
+            sel = torch.nonzero(keep).flatten().int()
+            kv_idx[h, i, :sel.numel()] = sel
+            kv_cnt[h, i] = sel.numel()
+    kv_idx, kv_cnt = kv_idx.cuda(), kv_cnt.cuda()
+    out = ops.attention_block_sparse(q, k, v, b, kv_idx, kv_cnt, q_orig=q_orig, k_orig=k_orig, out_rows=q_orig)
+    ref = _torch_block_sparse_ref(q, k, v, b, kv_idx, kv_cnt, q_orig, k_orig, q_orig, d ** -0.5)
+    err = (out.float() - ref).abs()
+    assert err.max().item() <= BF16_MAX and err.mean().item() <= BF16_MEAN, (err.max().item(), err.mean().item())
+
+
+def test_dense_causal_many_items_per_slot(ops):
+    """The dense comparator over 32 heads x 129 query blocks (~14 items per slot)
+    against torch's own bf16 causal SDPA."""
+    torch.manual_seed(2)
+    hq, hkv, n, d = 32, 8, 16384 + 77, 128
+    q = torch.randn(hq, n, d, device="cuda").to(torch.bfloat16)
+    k = torch.randn(hkv, n, d, device="cuda").to(torch.bfloat16)
+    v = torch.randn(hkv, n, d, device="cuda").to(torch.bfloat16)
+    out = ops.dense_causal_attention(q, k, v)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        q[None], k.repeat_interleave(4, 0)[None], v.repeat_interleave(4, 0)[None], is_causal=True)[0]
+    err = (out.float() - ref.float()).abs()
+    assert err.max().item() <= BF16_MAX and err.mean().item() <= BF16_MEAN, (err.max().item(), err.mean().item())
