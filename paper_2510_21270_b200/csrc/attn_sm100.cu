@@ -84,7 +84,11 @@ struct __align__(8) Barriers {
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[2];
-  uint64_t p_full, pv_done, o_full, o_free;
+  // p_full[b]: P written over S[b] by all softmax threads.  One barrier per S
+  // buffer: softmax(e + 1) no longer waits for PV(e - 1), so a single barrier
+  // could complete twice before the MMA issuer waits on it.
+  uint64_t p_full[2];
+  uint64_t pv_done, o_full, o_free;
   uint32_t tmem_base;
 };
 
@@ -483,7 +487,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bar->s_full[0], 1);
     mbar_init(&bar->s_full[1], 1);
-    mbar_init(&bar->p_full, kSoftmaxThreads);
+    mbar_init(&bar->p_full[0], kSoftmaxThreads);
+    mbar_init(&bar->p_full[1], kSoftmaxThreads);
     mbar_init(&bar->pv_done, 1);
     mbar_init(&bar->o_full, 1);
     mbar_init(&bar->o_free, kSoftmaxThreads);
@@ -538,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
-    uint32_t q_it = 0, k_it = 0, v_it = 0, pv_it = 0, item_no = 0;
+    uint32_t q_it = 0, k_it = 0, v_it = 0, pv_it = 0, item_no = 0, p_cnt[2] = {0, 0};
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x, ++item_no) {
       const Item it = item_of(a, idx);
       const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
@@ -548,7 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_pv = [&](int pe) {
         const uint32_t stage = v_it % kVStages;
         mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
-        mbar_wait(&bar->p_full, pv_it & 1);
+        mbar_wait(&bar->p_full[pe & 1], p_cnt[pe & 1] & 1);
+        ++p_cnt[pe & 1];
         if (lane == 0) trace_event(a, 0, pv_it);
         if (pe == 0) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // previous item's epilogue read O
         tc_fence_after();
@@ -684,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         l = l * factor + rs;
         tc_fence_before();
-        mbar_arrive(&bar->p_full);
+        mbar_arrive(&bar->p_full[b]);
       }
       // ---- epilogue: merge the two half-row states, O / l -> out[out_rows[i]]
       if (vis.len > 0) {  // the item's last PV (o_full: one phase per non-empty item)
