@@ -66,18 +66,19 @@ constexpr int kD = 128;       // head dim
 constexpr int kKStages = 3;   // K ring depth (freed as soon as QK^T completes)
 constexpr int kVStages = 2;   // V ring depth (freed when PV completes)
 constexpr int kSplit = 2;                         // threads per query row
-// route every fourth exp2 of a block through the FMA-pipe polynomial; off:
-// with two threads per row the MUFU is ~1/3 busy and the polynomial's ~10
-// instructions per element cost more issue slots than they save
-constexpr bool kPolyExp2 = false;
+// keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the
+// MUFU (tests/micro/softmax_exp_bench.cu: 64 keys x 2 warps per SMSP, 1073 ->
+// ~900 cycles per pass at 4-6 of 16)
+constexpr int kPolyPer16 = 6;
 constexpr int kCols = kBN / kSplit;               // key columns per softmax thread
 constexpr int kSoftmaxThreads = 128 * kSplit;
 constexpr int kThreads = 128 + kSoftmaxThreads;
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
-constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O0 | O1
+constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | Q (+ 64 spare)
 __host__ __device__ constexpr uint32_t col_s(int b) { return b ? 128u : 0u; }
-__host__ __device__ constexpr uint32_t col_o(int h) { return h ? 384u : 256u; }
+constexpr uint32_t kColO = 256;   // O: 128 fp32 columns
+constexpr uint32_t kColQ = 384;   // Q: 128 x 128 bf16 = 64 columns, the A operand of S = Q K^T
 
 struct __align__(8) Barriers {
   uint64_t q_full, q_empty;
@@ -89,6 +90,7 @@ struct __align__(8) Barriers {
   // could complete twice before the MMA issuer waits on it.
   uint64_t p_full[2];
   uint64_t pv_done, o_full, o_free;
+  uint64_t drained;  // every tcgen05 operation of the MMA issuer complete (before dealloc)
   uint32_t tmem_base;
 };
 
@@ -98,8 +100,8 @@ struct SmemLayout {
   static constexpr int k = q + kTileBytes;
   static constexpr int v = k + kKStages * kTileBytes;
   static constexpr int korig = v + kVStages * kTileBytes;      // int[128]
-  static constexpr int xch = korig + 128 * 4;                  // float[2 (m, l)][2 half][128] epilogue exchange
-  static constexpr int bars = xch + 2 * 2 * 128 * 4;
+  static constexpr int xch = korig + 128 * 4;  // float [2 buf][2 half][128] row maxima + [2 half][128] sums
+  static constexpr int bars = xch + (2 * 2 + 2) * 128 * 4;
   static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
 };
 static_assert(SmemLayout::total <= 232448, "shared memory budget");
@@ -197,6 +199,19 @@ __device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
       "elect.sync _|e, 0xffffffff;\n"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
       "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMEM[128 lanes x 8 columns] <- 128 rows x 256 bits of a shared-memory matrix
+// (same descriptor format as the MMA operands; executes in order with tcgen05.mma)
+__device__ __forceinline__ void tc_cp_w(uint32_t d_tmem, uint64_t sdesc_) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(sdesc_)
       : "memory");
 }
 
@@ -428,42 +443,105 @@ __device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, V
   cls = (int)(x >> 30);
 }
 
-// Pass 1 (per visited block): this thread's kCols scores, masked, and their max.
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a pair on the FMA/ALU pipes (packed f32x2): the Cody-Waite split and
+// degree-3 minimax of exp2_poly.  Offloads the MUFU, whose 16 ex2/clk/SM take
+// as long as the block's two MMAs.
+__device__ __forceinline__ void exp2_poly2(float y0, float y1, float& p0, float& p1) {
+  const uint64_t x = pk2(fmaxf(y0, -126.5f), fmaxf(y1, -126.5f));
+  const uint64_t t = fadd2(x, pk2(12582912.0f, 12582912.0f));
+  const uint64_t jf = fadd2(t, pk2(-12582912.0f, -12582912.0f));
+  const uint64_t f = fadd2(x, jf ^ 0x8000000080000000ull);
+  uint64_t p = ffma2(pk2(0.055219680070877075f, 0.055219680070877075f), f,
+                     pk2(0.2426094114780426f, 0.2426094114780426f));
+  p = ffma2(p, f, pk2(0.6932516694068909f, 0.6932516694068909f));
+  p = ffma2(p, f, pk2(0.9999279975891113f, 0.9999279975891113f));
+  float q0, q1, t0, t1;
+  upk2(p, q0, q1);
+  upk2(t, t0, t1);
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
+}
+
+// Pass 1 (per visited block): this thread's kCols scores, masked, and their max
+// (3-input FMNMX, eight independent chains).
 template <bool kPartial>
 __device__ __forceinline__ float load_scores(uint32_t tS, const int* ko, int qo, uint32_t (&r)[kCols]) {
 #pragma unroll
   for (int c = 0; c < kCols / 32; ++c) TMEM_LD32(tS + c * 32, (r + c * 32));
   tmem_wait_ld();
-  float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  if (kPartial) {
 #pragma unroll
-  for (int j = 0; j < kCols; ++j) {
-    if (kPartial && ko[j] > qo) r[j] = 0xff800000u;  // -inf: inadmissible (attention.hpp:298-300)
-    mx4[j & 3] = fmaxf(mx4[j & 3], __uint_as_float(r[j]));
+    for (int j = 0; j < kCols; ++j)
+      if (ko[j] > qo) r[j] = 0xff800000u;  // -inf: inadmissible (attention.hpp:298-300)
   }
-  return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+  float mx[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) mx[u] = __uint_as_float(r[u]);
+#pragma unroll
+  for (int j = 8; j + 16 <= kCols; j += 16) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mx[u] = max3(mx[u], __uint_as_float(r[j + u]), __uint_as_float(r[j + 8 + u]));
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[kCols - 8 + u]));
+  return max3(max3(mx[0], mx[1], mx[2]), max3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
 }
 
-// Pass 2: p = exp2(s * scale_log2 - m) -> bf16, written into TMEM as the A
-// operand of the PV MMA (two keys per 32-bit column); returns sum p.
-template <bool kPoly>
+// Pass 2: p = 2^(s * scale_log2 - m) -> bf16 pairs written into TMEM as the A
+// operand of the PV MMA (two keys per 32-bit column); returns sum p.  Packed
+// f32x2 FMA/add; kPolyPer16 of every 16 keys take the FMA-pipe polynomial.
+template <int kPolyPer16>
 __device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, float neg_m, uint32_t tP) {
-  float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const uint64_t sc2 = pk2(sc, sc), nm2 = pk2(neg_m, neg_m);
+  uint64_t sum2[2] = {0ull, 0ull};
 #pragma unroll
   for (int c = 0; c < kCols / 32; ++c) {
     uint32_t pk[16];
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) {
-      const float p0 = ex2(fmaf(__uint_as_float(r[c * 32 + j]), sc, neg_m));
-      const float y1 = fmaf(__uint_as_float(r[c * 32 + j + 1]), sc, neg_m);
-      const float p1 = (kPoly && (j & 2)) ? exp2_poly(y1) : ex2(y1);
-      sum4[j & 3] += p0;
-      sum4[(j + 1) & 3] += p1;
+    for (int jp = 0; jp < 16; ++jp) {
+      const int j = c * 32 + 2 * jp;
+      float y0, y1, p0, p1;
+      upk2(ffma2(pk2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sc2, nm2), y0, y1);
+      if ((j & 15) >= 16 - kPolyPer16) {
+        exp2_poly2(y0, y1, p0, p1);
+      } else {
+        p0 = ex2(y0);
+        p1 = ex2(y1);
+      }
+      sum2[jp & 1] = fadd2(sum2[jp & 1], pk2(p0, p1));
       __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-      pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+      pk[jp] = *reinterpret_cast<uint32_t*>(&b2);
     }
     TMEM_ST16(tP + c * 16, pk);
   }
-  return (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+  float s0, s1, s2, s3;
+  upk2(sum2[0], s0, s1);
+  upk2(sum2[1], s2, s3);
+  return (s0 + s1) + (s2 + s3);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -491,6 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bar->p_full[1], kSoftmaxThreads);
     mbar_init(&bar->pv_done, 1);
     mbar_init(&bar->o_full, 1);
+    mbar_init(&bar->drained, 1);
     mbar_init(&bar->o_free, kSoftmaxThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -543,20 +622,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
-    uint32_t q_it = 0, k_it = 0, v_it = 0, pv_it = 0, item_no = 0, p_cnt[2] = {0, 0};
-    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x, ++item_no) {
+    // o_no: non-empty items so far.  o_free has one phase per non-empty item
+    // (an item without visited blocks has no epilogue reading O, and the
+    // softmax does not arrive for it: an arrival the issuer did not wait for
+    // could complete a phase early)
+    uint32_t q_it = 0, k_it = 0, v_it = 0, pv_it = 0, o_no = 0, p_cnt[2] = {0, 0};
+    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
       const Item it = item_of(a, idx);
       const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
       mbar_wait(&bar->q_full, q_it & 1);
       ++q_it;
+      // Q -> TMEM once per item: S = Q K^T then reads Q from TMEM (TS form), so
+      // the per-block shared-memory traffic of QK^T is K alone.  tcgen05.cp runs
+      // in issue order with the MMAs, after the previous item's last QK^T.
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k)
+        tc_cp_w(tmem + kColQ + k * 8, sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024));
+      tc_commit_w(&bar->q_empty);  // the Q tile in shared memory is free once copied
       // PV of visited block `pe` (its P lives in S[pe & 1])
       auto issue_pv = [&](int pe) {
         const uint32_t stage = v_it % kVStages;
         mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
+        if (lane == 0) trace_event(a, 5, pv_it);  // V tile present
         mbar_wait(&bar->p_full[pe & 1], p_cnt[pe & 1] & 1);
         ++p_cnt[pe & 1];
         if (lane == 0) trace_event(a, 0, pv_it);
-        if (pe == 0) mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // previous item's epilogue read O
+        if (pe == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // previous item's epilogue read O
         tc_fence_after();
         const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
 #pragma unroll
@@ -566,8 +658,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           // A = P [128 q x 16 kv] in TMEM: 16 keys = 8 columns
           // B = V [16 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
           const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-          tc_mma_ts_w(tmem + col_o(k >> 2), tmem + col_s(pe & 1) + (k >> 2) * kCols + (k & 3) * 8, bd, idesc_pv,
-                      (pe == 0 && (k & 3) == 0) ? 0u : 1u);
+          tc_mma_ts_w(tmem + kColO, tmem + col_s(pe & 1) + (k >> 2) * kCols + (k & 3) * 8, bd, idesc_pv,
+                      (pe == 0 && k == 0) ? 0u : 1u);
         }
         if (lane == 0) trace_event(a, 2, pv_it);
         tc_commit_w(&bar->pv_done);
@@ -578,16 +670,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (int e = 0; e < len; ++e) {
         const uint32_t stage = k_it % kKStages;
+        if (lane == 0) trace_event(a, 7, k_it);  // MMA ready to issue QK
         mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
+        if (lane == 0) trace_event(a, 1, k_it);  // K tile present
         // S[e & 1] held P_{e-2}; its PV was issued before this point and
         // tcgen05.mma executes in issue order
         tc_fence_after();
         const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
-          const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
           const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-          tc_mma_w(tmem + col_s(e & 1), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
+          tc_mma_ts_w(tmem + col_s(e & 1), tmem + kColQ + k * 8, bd, idesc_qk, k > 0 ? 1u : 0u);
         }
         if (lane == 0) trace_event(a, 4, k_it);
         tc_commit_w(&bar->s_full[e & 1]);
@@ -595,21 +688,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++k_it;
         if (e > 0) issue_pv(e - 1);
       }
-      // Q is free once every S of this item has completed
-      tc_commit_w(&bar->q_empty);
-      if (len > 0) issue_pv(len - 1);
-      else mbar_wait(&bar->o_free, (item_no & 1) ^ 1);  // keep the o_free phases in step
+      if (len > 0) {
+        issue_pv(len - 1);
+        ++o_no;
+      }
+    }
+    // nothing may still write TMEM when it is released (e.g. the Q copy of a
+    // trailing item without visited blocks)
+    tc_commit_w(&bar->drained);
+    mbar_wait(&bar->drained, 0);
+  } else if (warp == 3) {
+    // debug timeline only (PBS_ATTN_TRACE, CTA 0): completion time of every PV
+    if (a.trace && blockIdx.x == 0) {
+      uint32_t g = 0;
+      for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
+        const Item it = item_of(a, idx);
+        const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
+        for (int e = 0; e < len; ++e, ++g) {
+          mbar_wait(&bar->pv_done, g & 1);
+          if (lane == 0) trace_event(a, 3, g);
+        }
+      }
     }
   } else if (warp >= 4) {
     // ===================== softmax: kSplit threads per row =====================
+    // warps 4..7 own keys [0, 64) of every block, warps 8..11 keys [64, 128); each
+    // group of four covers the four TMEM lane quadrants (warp % 4).  The two
+    // threads of a row share one running max (their block maxima are exchanged
+    // through shared memory once per block) and therefore the one O; each keeps
+    // its own partial sum and rescales / writes its own 64 output columns.
     const int part = (warp - 4) >> 2;    // key columns [kCols part, kCols part + kCols)
     const int quad = warp & 3;           // TMEM lane quadrant of this warp
     const int row = quad * 32 + lane;    // query row within the tile
     const int st = threadIdx.x - 128;    // 0..255
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t tO = tmem + lane_off + kColO + part * (kD / kSplit);
     int* ko_all = reinterpret_cast<int*>(smem + SmemLayout::korig);
     const int* ko = ko_all + part * kCols;
-    float* xch = reinterpret_cast<float*>(smem + SmemLayout::xch);
+    float* xmax = reinterpret_cast<float*>(smem + SmemLayout::xch);  // [2][kSplit][128]
+    float* xsum = xmax + 2 * kSplit * 128;                           // [kSplit][128]
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
     uint32_t s_cnt[2] = {0, 0};
@@ -620,8 +737,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t i = it.qb * kBM + row;
       const bool valid = i < a.n;
       const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
-      float m = -INFINITY;  // this half-row's running max (log2 domain)
-      float l = 0.0f;       // this half-row's running sum
+      float m = -INFINITY;  // the row's running max (log2 domain), identical in both threads
+      float l = 0.0f;       // this thread's partial running sum
       for (int e = 0; e < vis.len; ++e, ++blk) {
         int64_t kb;
         int cls;
@@ -638,21 +755,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int b = e & 1;
         mbar_wait(&bar->s_full[b], s_cnt[b] & 1);
-        if (st == 0) trace_event(a, 6, blk);
         ++s_cnt[b];
+        if (st == 0) trace_event(a, 6, blk);
         tc_fence_after();
         const uint32_t tS = tmem + lane_off + col_s(b) + part * kCols;
         uint32_t r[kCols];
         const float hmax = (cls == 1) ? load_scores<true>(tS, ko, qo, r) : load_scores<false>(tS, ko, qo, r);
+        // the row's block max from both halves (double-buffered by block parity:
+        // a buffer is rewritten only after the next block's barrier)
+        float* xb = xmax + (blk & 1) * kSplit * 128;
+        xb[part * 128 + row] = hmax;
+        named_bar_sync(3, kSoftmaxThreads);
+        const float bmax = fmaxf(xb[row], xb[128 + row]) * sc;
         if (st == 0) trace_event(a, 10, blk);
-        // this half-row's own online softmax (log2 domain, lazy rescale by 2^8)
-        const float bmax = hmax * sc;
+        // online softmax (absorb, attention.hpp:96-126) in the log2 domain with
+        // lazy rescaling: O is rescaled only when the max grows by more than 8
         const float m_new = fmaxf(m, bmax);
         bool need_rescale = false;
         float factor = 1.0f;
         if (m_new != -INFINITY) {
           if (m == -INFINITY) {
-            m = m_new;  // this half's O rows are still exactly 0 here
+            m = m_new;  // nothing accumulated for this row yet (O is exactly 0)
           } else if (m_new > m + 8.0f) {
             factor = ex2(m - m_new);
             need_rescale = true;
@@ -664,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // columns [kCols part, +kCols/2).  (Packing both halves into columns
         // [0, kCols) would let part 1 overwrite scores part 0 has not read yet.)
         const uint32_t tP = tmem + lane_off + col_s(b) + part * kCols;
-        const float rs = emit_p<kPolyExp2>(r, sc, neg_m, tP);
+        const float rs = emit_p<kPolyPer16>(r, sc, neg_m, tP);
         tmem_wait_st();
         if (st == 0) trace_event(a, 8, blk);
         if (cls == 1) named_bar_sync(1, kSoftmaxThreads);  // ko[] may be refilled after this
@@ -676,9 +799,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (__any_sync(0xffffffffu, need_rescale)) {
           mbar_wait(&bar->pv_done, (blk - 1) & 1);
           tc_fence_after();
-          const uint32_t tO = tmem + lane_off + col_o(part);
-#pragma unroll
-          for (int c = 0; c < kD / 32; ++c) {
+#pragma unroll 1
+          for (int c = 0; c < kD / kSplit / 32; ++c) {
             uint32_t o[32];
             TMEM_LD32(tO + c * 32, o);
             tmem_wait_ld();
@@ -692,57 +814,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&bar->p_full[b]);
       }
-      // ---- epilogue: merge the two half-row states, O / l -> out[out_rows[i]]
-      if (vis.len > 0) {  // the item's last PV (o_full: one phase per non-empty item)
-        mbar_wait(&bar->o_full, o_cnt & 1);
+      // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138):
+      // O / l -> out[out_rows[i]] (the fused un-permute, pipeline.hpp:178)
+      if (vis.len > 0) {
+        xsum[part * 128 + row] = l;
+        named_bar_sync(2, kSoftmaxThreads);
+        l += xsum[(part ^ 1) * 128 + row];
+        mbar_wait(&bar->o_full, o_cnt & 1);  // the item's last PV
         ++o_cnt;
       }
-      xch[part * 128 + row] = m;
-      xch[256 + part * 128 + row] = l;
-      named_bar_sync(2, kSoftmaxThreads);
-      const float m0 = xch[row], m1 = xch[128 + row], l0 = xch[256 + row], l1 = xch[384 + row];
-      named_bar_sync(2, kSoftmaxThreads);  // xch is rewritten by the next item
-      const float mt = fmaxf(m0, m1);
-      const float f0 = (m0 == -INFINITY) ? 0.0f : ex2(m0 - mt);
-      const float f1 = (m1 == -INFINITY) ? 0.0f : ex2(m1 - mt);
-      const float lt = l0 * f0 + l1 * f1;
       tc_fence_after();
-      if (valid && !(lt > 0.0f) && a.status && part == 0) {
+      if (valid && !(l > 0.0f) && a.status && part == 0) {
         a.status[0] = 1;
         atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
       }
-      const float inv = (lt > 0.0f) ? 1.0f / lt : 0.0f;
-      const float g0 = f0 * inv, g1 = f1 * inv;
-      const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
-      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + part * kCols;
+      if (vis.len > 0) {
+        const float inv = (l > 0.0f) ? 1.0f / l : 0.0f;
+        const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
+        __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + part * (kD / kSplit);
+#pragma unroll 1
+        for (int c = 0; c < kD / kSplit / 32; ++c) {
+          uint32_t o[32];
+          TMEM_LD32(tO + c * 32, o);
+          tmem_wait_ld();
+          if (valid && l > 0.0f) {
 #pragma unroll
-      for (int c = 0; c < kCols / 32; ++c) {  // this thread writes output columns [kCols part, +kCols)
-        uint32_t o0[32], o1[32];
-        TMEM_LD32(tmem + lane_off + col_o(0) + part * kCols + c * 32, o0);
-        TMEM_LD32(tmem + lane_off + col_o(1) + part * kCols + c * 32, o1);
-        tmem_wait_ld();
-        if (valid && lt > 0.0f) {
+            for (int u = 0; u < 4; ++u) {
+              uint32_t pk[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int w2 = 0; w2 < 4; ++w2) {
-              const int j = u * 8 + 2 * w2;
-              float v0 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j]) * g0;
-              float v1 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j + 1]) * g0;
-              if (m1 != -INFINITY) {
-                v0 = fmaf(__uint_as_float(o1[j]), g1, v0);
-                v1 = fmaf(__uint_as_float(o1[j + 1]), g1, v1);
+              for (int w2 = 0; w2 < 4; ++w2) {
+                const int j = u * 8 + 2 * w2;
+                __nv_bfloat162 b2 =
+                    __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
+                pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
               }
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
-              pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
+              *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
-            *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&bar->o_free);
+      if (vis.len > 0) {
+        tc_fence_before();
+        mbar_arrive(&bar->o_free);
+      }
     }
   }
   tc_fence_before();

@@ -28,17 +28,24 @@ names = ["mma_sees_p0", "mma_sees_p1", "pv_issue0", "pv_issue1", "qk_issue0", "q
          "p_done0", "p_done1", "max_done0", "max_done1"]
 t0 = t[t > 0].min()
 lo, hi = 100, 1500
-sr, pd, md, qk, pv, ms = (t[6], t[8], t[10], t[4], t[2], t[0])
+sr, pd, md, qk, pv, ms, pvd = (t[6], t[8], t[10], t[4], t[2], t[0], t[3])
 b = np.arange(lo, hi)
-ok = (sr[b] > 0) & (pd[b] > 0) & (qk[b] > 0) & (pv[b] > 0) & (ms[b] > 0) & (sr[b + 1] > 0)
+ok = (sr[b] > 0) & (pd[b] > 0) & (qk[b] > 0) & (pv[b] > 0) & (ms[b] > 0) & (sr[b + 2] > 0) & (pvd[b] > 0)
 b = b[ok]
-print(f"CTA 0: blocks {len(b)}")
-print("  softmax: S ready -> max done  ", np.median(md[b] - sr[b]))
-print("  softmax: max done -> P written", np.median(pd[b] - md[b]))
-print("  P written -> MMA sees P       ", np.median(ms[b] - pd[b]))
-print("  (old design) S(b+1) ready - P(b) written", np.median(sr[b + 1] - pd[b]))
-print("  QK(b+1) issued -> S(b+1) ready (old: b+1)", np.median(sr[b + 1] - qk[b + 1]))
-print("  MMA sees P -> PV issued       ", np.median(pv[b] - ms[b]))
-print("  PV(b) issued -> QK(b+1) issued", np.median(qk[b + 1] - pv[b]))
-print("  QK(b+1) issued -> S(b+1) ready", np.median(sr[b + 1] - qk[b + 1]))
-print("  period S(b) -> S(b+1)         ", np.median(sr[b + 1] - sr[b]))
+med = lambda x: float(np.median(x))
+print(f"CTA 0: blocks {len(b)}   (order per block b: QK(b+1) issued, PV(b-1)... see below)")
+print("  softmax: S(b) ready -> max done      ", med(md[b] - sr[b]))
+print("  softmax: max done -> P(b) written    ", med(pd[b] - md[b]))
+print("  P(b) written -> MMA sees P(b)        ", med(ms[b] - pd[b]))
+print("  MMA sees P(b) -> PV(b) issued        ", med(pv[b] - ms[b]))
+print("  PV(b) issued -> PV(b) complete       ", med(pvd[b] - pv[b]))
+print("  PV(b) issued -> QK(b+2) issued       ", med(qk[b + 2] - pv[b]))
+print("  QK(b+2) issued -> S(b+2) ready       ", med(sr[b + 2] - qk[b + 2]))
+print("  PV(b) complete -> S(b+2) ready       ", med(sr[b + 2] - pvd[b]))
+print("  P(b) written -> S(b+1) ready         ", med(sr[b + 1] - pd[b]))
+print("  period S(b) -> S(b+1)                ", med(sr[b + 1] - sr[b]))
+kf, vf, top = t[1], t[5], t[7]
+print("  PV(b) issued -> MMA at QK(b+2)       ", med(top[b + 2] - pv[b]))
+print("  MMA at QK(b+2) -> K(b+2) present     ", med(kf[b + 2] - top[b + 2]))
+print("  K(b+2) present -> QK(b+2) issued     ", med(qk[b + 2] - kf[b + 2]))
+print("  MMA sees P(b) -> V(b) present        ", med(vf[b] - ms[b]))
