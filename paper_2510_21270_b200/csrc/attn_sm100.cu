@@ -75,20 +75,19 @@ constexpr int kSoftmaxThreads = 128 * kSplit;
 constexpr int kThreads = 128 + kSoftmaxThreads;
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
-constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | Q (+ 64 spare)
+constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | Q | P
 __host__ __device__ constexpr uint32_t col_s(int b) { return b ? 128u : 0u; }
 constexpr uint32_t kColO = 256;   // O: 128 fp32 columns
 constexpr uint32_t kColQ = 384;   // Q: 128 x 128 bf16 = 64 columns, the A operand of S = Q K^T
+constexpr uint32_t kColP = 448;   // P: 128 x 128 bf16 = 64 columns, the A operand of O += P V
 
 struct __align__(8) Barriers {
   uint64_t q_full, q_empty;
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
-  uint64_t s_full[2];
-  // p_full[b]: P written over S[b] by all softmax threads.  One barrier per S
-  // buffer: softmax(e + 1) no longer waits for PV(e - 1), so a single barrier
-  // could complete twice before the MMA issuer waits on it.
-  uint64_t p_full[2];
+  uint64_t s_full[2];  // S[b] = Q K^T complete
+  uint64_t s_free[2];  // S[b] read into registers by every softmax thread
+  uint64_t p_full;     // P written into TMEM by every softmax thread
   uint64_t pv_done, o_full, o_free;
   uint64_t drained;  // every tcgen05 operation of the MMA issuer complete (before dealloc)
   uint32_t tmem_base;
@@ -100,8 +99,8 @@ struct SmemLayout {
   static constexpr int k = q + kTileBytes;
   static constexpr int v = k + kKStages * kTileBytes;
   static constexpr int korig = v + kVStages * kTileBytes;      // int[128]
-  static constexpr int xch = korig + 128 * 4;  // float [2 buf][2 half][128] row maxima + [2 half][128] sums
-  static constexpr int bars = xch + (2 * 2 + 2) * 128 * 4;
+  static constexpr int xch = korig + 128 * 4;  // float [2 buf][kSplit][128] row maxima + [kSplit][128] sums
+  static constexpr int bars = xch + (2 * kSplit + kSplit) * 128 * 4;
   static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
 };
 static_assert(SmemLayout::total <= 232448, "shared memory budget");
@@ -126,16 +125,20 @@ __device__ __noinline__ void mbar_timeout_trap(uint32_t addr, uint32_t parity) {
          addr, parity);
   __trap();
 }
+// try_wait suspends the warp until the phase completes or this many ns pass, so
+// waiting warps (the producers and the MMA issuer share sub-partitions with the
+// softmax warps) do not spin on the issue slots
+constexpr uint32_t kWaitHintNs = 1000000;
 __device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
       "selp.u32 %0, 1, 0, P1;\n"
       "}\n"
       : "=r"(ok)
-      : "r"(addr), "r"(parity)
+      : "r"(addr), "r"(parity), "r"(kWaitHintNs)
       : "memory");
   return ok != 0;
 }
@@ -511,32 +514,28 @@ __device__ __forceinline__ float load_scores(uint32_t tS, const int* ko, int qo,
   return max3(max3(mx[0], mx[1], mx[2]), max3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
 }
 
-// Pass 2: p = 2^(s * scale_log2 - m) -> bf16 pairs written into TMEM as the A
-// operand of the PV MMA (two keys per 32-bit column); returns sum p.  Packed
-// f32x2 FMA/add; kPolyPer16 of every 16 keys take the FMA-pipe polynomial.
+// Pass 2: p = 2^(s * scale_log2 - m) -> bf16 pairs (two keys per 32-bit word,
+// the A-operand layout of the PV MMA in TMEM); returns sum p.  Packed f32x2
+// FMA/add; kPolyPer16 of every 16 keys take the FMA-pipe polynomial.
 template <int kPolyPer16>
-__device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, float neg_m, uint32_t tP) {
+__device__ __forceinline__ float compute_p(const uint32_t (&r)[kCols], float sc, float neg_m,
+                                           uint32_t (&pk)[kCols / 2]) {
   const uint64_t sc2 = pk2(sc, sc), nm2 = pk2(neg_m, neg_m);
   uint64_t sum2[2] = {0ull, 0ull};
 #pragma unroll
-  for (int c = 0; c < kCols / 32; ++c) {
-    uint32_t pk[16];
-#pragma unroll
-    for (int jp = 0; jp < 16; ++jp) {
-      const int j = c * 32 + 2 * jp;
-      float y0, y1, p0, p1;
-      upk2(ffma2(pk2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sc2, nm2), y0, y1);
-      if ((j & 15) >= 16 - kPolyPer16) {
-        exp2_poly2(y0, y1, p0, p1);
-      } else {
-        p0 = ex2(y0);
-        p1 = ex2(y1);
-      }
-      sum2[jp & 1] = fadd2(sum2[jp & 1], pk2(p0, p1));
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-      pk[jp] = *reinterpret_cast<uint32_t*>(&b2);
+  for (int jp = 0; jp < kCols / 2; ++jp) {
+    const int j = 2 * jp;
+    float y0, y1, p0, p1;
+    upk2(ffma2(pk2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sc2, nm2), y0, y1);
+    if ((j & 15) >= 16 - kPolyPer16) {
+      exp2_poly2(y0, y1, p0, p1);
+    } else {
+      p0 = ex2(y0);
+      p1 = ex2(y1);
     }
-    TMEM_ST16(tP + c * 16, pk);
+    sum2[jp & 1] = fadd2(sum2[jp & 1], pk2(p0, p1));
+    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+    pk[jp] = *reinterpret_cast<uint32_t*>(&b2);
   }
   float s0, s1, s2, s3;
   upk2(sum2[0], s0, s1);
@@ -565,8 +564,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bar->s_full[0], 1);
     mbar_init(&bar->s_full[1], 1);
-    mbar_init(&bar->p_full[0], kSoftmaxThreads);
-    mbar_init(&bar->p_full[1], kSoftmaxThreads);
+    mbar_init(&bar->s_free[0], kSoftmaxThreads);
+    mbar_init(&bar->s_free[1], kSoftmaxThreads);
+    mbar_init(&bar->p_full, kSoftmaxThreads);
     mbar_init(&bar->pv_done, 1);
     mbar_init(&bar->o_full, 1);
     mbar_init(&bar->drained, 1);
@@ -622,11 +622,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
+    // Blocks are numbered globally across this CTA's items; block g uses S[g & 1].
+    // QK^T runs two blocks ahead of PV: QK(g + 2) needs only that the softmax
+    // has read S(g) into registers (s_free), not that P(g) is done, so it is
+    // issued before PV(g) and overlaps the softmax of block g.
     // o_no: non-empty items so far.  o_free has one phase per non-empty item
     // (an item without visited blocks has no epilogue reading O, and the
     // softmax does not arrive for it: an arrival the issuer did not wait for
     // could complete a phase early)
-    uint32_t q_it = 0, k_it = 0, v_it = 0, pv_it = 0, o_no = 0, p_cnt[2] = {0, 0};
+    uint32_t q_it = 0, k_it = 0, v_it = 0, o_no = 0, gq = 0, gp = 0;
+    auto issue_qk = [&]() {
+      const int b = gq & 1;
+      mbar_wait(&bar->s_free[b], ((gq >> 1) & 1) ^ 1);  // the softmax has read S(gq - 2)
+      const uint32_t stage = k_it % kKStages;
+      if (lane == 0) trace_event(a, 7, gq);  // MMA ready to issue QK
+      mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
+      if (lane == 0) trace_event(a, 1, gq);  // K tile present
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
+        tc_mma_ts_w(tmem + col_s(b), tmem + kColQ + k * 8, bd, idesc_qk, k > 0 ? 1u : 0u);
+      }
+      if (lane == 0) trace_event(a, 4, gq);
+      tc_commit_w(&bar->s_full[b]);
+      tc_commit_w(&bar->k_empty[stage]);
+      ++k_it;
+      ++gq;
+    };
+    auto issue_pv = [&](int pe, int len) {
+      const uint32_t stage = v_it % kVStages;
+      mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
+      if (lane == 0) trace_event(a, 5, gp);  // V tile present
+      mbar_wait(&bar->p_full, gp & 1);
+      if (lane == 0) trace_event(a, 0, gp);
+      if (pe == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // previous item's epilogue read O
+      tc_fence_after();
+      const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
+#pragma unroll
+      for (int k = 0; k < kBN / 16; ++k) {
+        // A = P [128 q x 16 kv] in TMEM (8 columns); B = V [16 kv x 128 d] MN-major SW128
+        const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
+        tc_mma_ts_w(tmem + kColO, tmem + kColP + k * 8, bd, idesc_pv, (pe == 0 && k == 0) ? 0u : 1u);
+      }
+      if (lane == 0) trace_event(a, 2, gp);
+      tc_commit_w(&bar->pv_done);
+      tc_commit_w(&bar->v_empty[stage]);
+      if (pe == len - 1) tc_commit_w(&bar->o_full);
+      ++v_it;
+      ++gp;
+    };
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
       const Item it = item_of(a, idx);
       const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
@@ -640,58 +686,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < kD / 16; ++k)
         tc_cp_w(tmem + kColQ + k * 8, sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024));
       tc_commit_w(&bar->q_empty);  // the Q tile in shared memory is free once copied
-      // PV of visited block `pe` (its P lives in S[pe & 1])
-      auto issue_pv = [&](int pe) {
-        const uint32_t stage = v_it % kVStages;
-        mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
-        if (lane == 0) trace_event(a, 5, pv_it);  // V tile present
-        mbar_wait(&bar->p_full[pe & 1], p_cnt[pe & 1] & 1);
-        ++p_cnt[pe & 1];
-        if (lane == 0) trace_event(a, 0, pv_it);
-        if (pe == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // previous item's epilogue read O
-        tc_fence_after();
-        const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
-          // keys [0, 64) accumulate into O0, keys [64, 128) into O1: each half
-          // of the row runs its own online softmax (no per-block exchange)
-          // A = P [128 q x 16 kv] in TMEM: 16 keys = 8 columns
-          // B = V [16 kv x 128 d] MN-major SW128: 16 keys = 2 atoms of 8 rows
-          const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-          tc_mma_ts_w(tmem + kColO, tmem + col_s(pe & 1) + (k >> 2) * kCols + (k & 3) * 8, bd, idesc_pv,
-                      (pe == 0 && k == 0) ? 0u : 1u);
-        }
-        if (lane == 0) trace_event(a, 2, pv_it);
-        tc_commit_w(&bar->pv_done);
-        tc_commit_w(&bar->v_empty[stage]);
-        if (pe == len - 1) tc_commit_w(&bar->o_full);
-        ++pv_it;
-        ++v_it;
-      };
+      for (int e = 0; e < len && e < 2; ++e) issue_qk();
       for (int e = 0; e < len; ++e) {
-        const uint32_t stage = k_it % kKStages;
-        if (lane == 0) trace_event(a, 7, k_it);  // MMA ready to issue QK
-        mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
-        if (lane == 0) trace_event(a, 1, k_it);  // K tile present
-        // S[e & 1] held P_{e-2}; its PV was issued before this point and
-        // tcgen05.mma executes in issue order
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
-          const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-          tc_mma_ts_w(tmem + col_s(e & 1), tmem + kColQ + k * 8, bd, idesc_qk, k > 0 ? 1u : 0u);
-        }
-        if (lane == 0) trace_event(a, 4, k_it);
-        tc_commit_w(&bar->s_full[e & 1]);
-        tc_commit_w(&bar->k_empty[stage]);
-        ++k_it;
-        if (e > 0) issue_pv(e - 1);
+        if (e + 2 < len) issue_qk();
+        issue_pv(e, len);
       }
-      if (len > 0) {
-        issue_pv(len - 1);
-        ++o_no;
-      }
+      if (len > 0) ++o_no;
     }
     // nothing may still write TMEM when it is released (e.g. the Q copy of a
     // trailing item without visited blocks)
@@ -729,7 +729,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* xsum = xmax + 2 * kSplit * 128;                           // [kSplit][128]
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
-    uint32_t s_cnt[2] = {0, 0};
     uint32_t blk = 0, o_cnt = 0;
     for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
       const Item it = item_of(a, idx);
@@ -742,7 +741,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = 0; e < vis.len; ++e, ++blk) {
         int64_t kb;
         int cls;
+        if (st == 0) trace_event(a, 9, blk);  // softmax loop top
         visit_get(a, it, vis, e, lane, kb, cls);
+        if (st == 0) trace_event(a, 11, blk);  // visit entry known
         if (cls == 1) {
           if (st < 128) {
             const int64_t j = kb * kBN + st;
@@ -753,20 +754,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           named_bar_sync(1, kSoftmaxThreads);
         }
-        const int b = e & 1;
-        mbar_wait(&bar->s_full[b], s_cnt[b] & 1);
-        ++s_cnt[b];
+        const int b = blk & 1;
+        mbar_wait(&bar->s_full[b], (blk >> 1) & 1);
         if (st == 0) trace_event(a, 6, blk);
         tc_fence_after();
         const uint32_t tS = tmem + lane_off + col_s(b) + part * kCols;
         uint32_t r[kCols];
         const float hmax = (cls == 1) ? load_scores<true>(tS, ko, qo, r) : load_scores<false>(tS, ko, qo, r);
+        // S[b] is in registers: the MMA issuer may compute S(blk + 2) into it
+        tc_fence_before();
+        mbar_arrive(&bar->s_free[b]);
+        if (cls == 1) named_bar_sync(1, kSoftmaxThreads);  // ko[] may be refilled after this
         // the row's block max from both halves (double-buffered by block parity:
         // a buffer is rewritten only after the next block's barrier)
         float* xb = xmax + (blk & 1) * kSplit * 128;
         xb[part * 128 + row] = hmax;
         named_bar_sync(3, kSoftmaxThreads);
-        const float bmax = fmaxf(xb[row], xb[128 + row]) * sc;
+        float bmax = xb[row];
+#pragma unroll
+        for (int q = 1; q < kSplit; ++q) bmax = fmaxf(bmax, xb[q * 128 + row]);
+        bmax *= sc;
         if (st == 0) trace_event(a, 10, blk);
         // online softmax (absorb, attention.hpp:96-126) in the log2 domain with
         // lazy rescaling: O is rescaled only when the max grows by more than 8
@@ -783,22 +790,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         const float neg_m = (m == -INFINITY) ? 0.0f : -m;
-        // P over this thread's own consumed S columns: keys [kCols part, +kCols) ->
-        // columns [kCols part, +kCols/2).  (Packing both halves into columns
-        // [0, kCols) would let part 1 overwrite scores part 0 has not read yet.)
-        const uint32_t tP = tmem + lane_off + col_s(b) + part * kCols;
-        const float rs = emit_p<kPolyPer16>(r, sc, neg_m, tP);
-        tmem_wait_st();
-        if (st == 0) trace_event(a, 8, blk);
-        if (cls == 1) named_bar_sync(1, kSoftmaxThreads);  // ko[] may be refilled after this
-        // O may only be rescaled once the previous PV has completed.  Only then is
-        // pv_done waited on: S(blk) ready implies PV(blk - 2) complete (it was
-        // issued before QK(blk)) and PV(blk) cannot complete before this thread's
-        // P, so the barrier has completed blk - 1 or blk phases and the parity of
-        // PV(blk - 1) identifies it without waiting on every block.
+        uint32_t pk[kCols / 2];
+        const float rs = compute_p<kPolyPer16>(r, sc, neg_m, pk);
+        l = l * factor + rs;
+        // P is single-buffered in TMEM and O is rescaled in place: both need the
+        // previous PV complete (every PV is waited on, so the phases stay exact)
+        if (blk > 0) mbar_wait(&bar->pv_done, (blk - 1) & 1);
+        tc_fence_after();
         if (__any_sync(0xffffffffu, need_rescale)) {
-          mbar_wait(&bar->pv_done, (blk - 1) & 1);
-          tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < kD / kSplit / 32; ++c) {
             uint32_t o[32];
@@ -808,18 +807,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * factor);
             TMEM_ST32(tO + c * 32, o);
           }
-          tmem_wait_st();
         }
-        l = l * factor + rs;
+        // keys [kCols part, +kCols) -> P columns [kCols/2 part, +kCols/2)
+        const uint32_t tP = tmem + lane_off + kColP + part * (kCols / 2);
+#pragma unroll
+        for (int c = 0; c < kCols / 32; ++c) TMEM_ST16(tP + c * 16, (pk + c * 16));
+        tmem_wait_st();
+        if (st == 0) trace_event(a, 8, blk);
         tc_fence_before();
-        mbar_arrive(&bar->p_full[b]);
+        mbar_arrive(&bar->p_full);
       }
       // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138):
       // O / l -> out[out_rows[i]] (the fused un-permute, pipeline.hpp:178)
       if (vis.len > 0) {
         xsum[part * 128 + row] = l;
         named_bar_sync(2, kSoftmaxThreads);
-        l += xsum[(part ^ 1) * 128 + row];
+        l = 0.0f;
+#pragma unroll
+        for (int q = 0; q < kSplit; ++q) l += xsum[q * 128 + row];
         mbar_wait(&bar->o_full, o_cnt & 1);  // the item's last PV
         ++o_cnt;
       }

@@ -49,3 +49,8 @@ print("  PV(b) issued -> MMA at QK(b+2)       ", med(top[b + 2] - pv[b]))
 print("  MMA at QK(b+2) -> K(b+2) present     ", med(kf[b + 2] - top[b + 2]))
 print("  K(b+2) present -> QK(b+2) issued     ", med(qk[b + 2] - kf[b + 2]))
 print("  MMA sees P(b) -> V(b) present        ", med(vf[b] - ms[b]))
+lt, vg = t[9], t[11]
+print("  P(b) written -> loop top (b+1)       ", med(lt[b + 1] - pd[b]))
+print("  loop top -> visit entry (b+1)        ", med(vg[b + 1] - lt[b + 1]))
+print("  visit entry -> S(b+1) passed         ", med(sr[b + 1] - vg[b + 1]))
+print("  QK(b+1) issued -> PV(b) complete (>0: QK done before)", med(pvd[b] - qk[b + 1]))

@@ -13,7 +13,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)2 << 61;
   return d;
 }
-__host__ __device__ constexpr uint32_t idesc(uint32_t n) { return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24); }
+__host__ __device__ constexpr uint32_t idesc(uint32_t n, uint32_t bmn = 0) { return (1u << 4) | (1u << 7) | (1u << 10) | (bmn << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24); }
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc) : "memory");
 }
@@ -29,13 +29,13 @@ __device__ __forceinline__ void wait(uint64_t* bar, uint32_t ph) {
 
 // kLoad: 0 none; 1: warps 1.. stream tcgen05.ld over TMEM columns [256, 384);
 // 2: warps 1.. stream tcgen05.st; 3: warps 1.. stream st.shared into a 64 KB region
-template <int kMode, int kN, int kLoad>
+template <int kMode, int kN, int kLoad, bool kRandom = false, int kCommit = 0>
 __global__ void bench(long long* out, int iters, volatile int* stop) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* s = (unsigned char*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2[2];
   __shared__ uint32_t tbase;
-  if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar))); asm volatile("fence.mbarrier_init.release.cluster;"); }
+  if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar))); asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2[0]))); asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2[1]))); asm volatile("fence.mbarrier_init.release.cluster;"); }
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -45,6 +45,16 @@ __global__ void bench(long long* out, int iters, volatile int* stop) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = tbase;
   const uint32_t a = smem_u32(s), b = smem_u32(s + 32768);
+  if (kRandom) {  // random bf16 operands (switching power like real data)
+    uint32_t x = 12345u + threadIdx.x * 7919u + blockIdx.x * 104729u;
+    for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) {
+      x = x * 1664525u + 1013904223u;
+      const uint32_t lo = 0x3f80u ^ ((x >> 9) & 0x807fu), hi = 0x3f80u ^ ((x >> 20) & 0x807fu);
+      reinterpret_cast<uint32_t*>(s)[i] = lo | (hi << 16);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
   __shared__ int done;
   if (threadIdx.x == 0) done = 0;
   __syncthreads();
@@ -74,12 +84,18 @@ __global__ void bench(long long* out, int iters, volatile int* stop) {
   } else {
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
+    if (kCommit == 3) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (kCommit == 4) { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); __syncwarp(); asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+    if (kCommit == 5) { uint32_t ok; asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n" : "=r"(ok) : "r"(smem_u32(&bar2[1])), "r"(1u) : "memory"); asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const uint64_t bd = sdesc(b + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
       if (kMode == 0) mma_ss(tm, sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), bd, idesc(kN), k > 0);
-      else mma_ts(tm, tm + 256 + k * 8, bd, idesc(kN), k > 0);
+      else if (kMode == 1) mma_ts(tm, tm + 256 + k * 8, bd, idesc(kN), k > 0);
+      else mma_ts(tm, tm + 256 + k * 8, sdesc(b + k * 16 * 128, 16384, 1024), idesc(kN, 1), k > 0);  // B MN-major (V)
     }
+    if (kCommit == 1) commit(&bar2[it & 1]);  // a commit after every 8 MMAs (nobody waits)
+    if (kCommit == 2) { commit(&bar2[0]); wait(&bar2[0], it & 1); }  // and wait for it
   }
   commit(&bar);
   wait(&bar, 0);
@@ -92,23 +108,26 @@ __global__ void bench(long long* out, int iters, volatile int* stop) {
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
 }
 
-template <int kMode, int kN, int kLoad>
+template <int kMode, int kN, int kLoad, bool kRandom = false, int kCommit = 0>
 void run(int warps) {
   long long* d; cudaMalloc(&d, 148 * 8);
-  auto k = bench<kMode, kN, kLoad>;
+  auto k = bench<kMode, kN, kLoad, kRandom, kCommit>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-  const int iters = 4000;
+  const int iters = 20000;
   k<<<148, 32 * warps, 140 * 1024>>>(d, iters, nullptr);
   cudaDeviceSynchronize();
   k<<<148, 32 * warps, 140 * 1024>>>(d, iters, nullptr);
   long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   const double per = (double)h / (iters * 8.0);
-  printf("%s N=%d load %d warps %d: %.1f cycles per 128x%dx16 MMA (ideal %d) %s\n", kMode ? "TS" : "SS", kN, kLoad, warps, per, kN, kN / 2,
+  printf("commit %d %s%s N=%d load %d warps %d: %.1f cycles per 128x%dx16 MMA (ideal %d) %s\n", kCommit, kMode == 2 ? "TS-Bmn" : kMode ? "TS" : "SS", kRandom ? " random" : "", kN, kLoad, warps, per, kN, kN / 2,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 int main() {
-  run<0, 128, 0>(1); run<1, 128, 0>(1);
+  run<0, 128, 0>(1); run<1, 128, 0>(1); run<2, 128, 0>(1); run<2, 128, 0, false, 2>(1);
+  run<1, 128, 0, false, 3>(1); run<1, 128, 0, false, 4>(1); run<1, 128, 0, false, 5>(1);
+  run<0, 128, 0, true>(1); run<0, 256, 0, true>(1);
+  run<0, 128, 0, false, 1>(1); run<1, 128, 0, false, 1>(1); run<0, 128, 0, false, 2>(1); run<1, 128, 0, false, 2>(1);
   run<0, 128, 1>(9); run<1, 128, 1>(9); run<1, 128, 1>(5);
   run<0, 128, 2>(9); run<1, 128, 2>(9);
   run<0, 128, 3>(9); run<1, 128, 3>(9);
