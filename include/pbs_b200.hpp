@@ -129,4 +129,17 @@ inline PipelineReport pbs_attention_host(const float* q, const float* k, const f
   return rep;
 }
 
+/// attention_coverage (pipeline.hpp:198-243) on device buffers: per-head
+/// coverage into the device array `coverage` (double [Hq]).
+inline std::size_t coverage_workspace_size(const pbs_shape& s, std::size_t block) {
+  const std::size_t n = pbs_coverage_workspace_size(&s, (int64_t)block);
+  if (n == 0) throw Error(PBS_ERR_CONFIG, pbs_last_error());
+  return n;
+}
+inline void attention_coverage(const void* q, const void* k, const pbs_shape& s, std::size_t block,
+                               const uint8_t* mask, const int32_t* sigma, const int32_t* pi, double* coverage,
+                               void* ws, std::size_t ws_bytes, double scale = 0.0, void* stream = nullptr) {
+  check(pbs_attention_coverage(q, k, &s, (int64_t)block, mask, sigma, pi, scale, coverage, ws, ws_bytes, stream));
+}
+
 }  // namespace pbs_b200

@@ -208,6 +208,25 @@ PBS_API int pbs_attention_host(const void* q, const void* k, const void* v, cons
                        const pbs_pipeline_config* cfg, void* out, int32_t* sigma,
                        int32_t* pi, uint8_t* mask, pbs_report* report);
 
+/* ---- diagnostics (pipeline.hpp:195-295) --------------------------------- */
+
+/* Device scratch for pbs_attention_coverage. */
+PBS_API size_t pbs_coverage_workspace_size(const pbs_shape* shape, int64_t block_size);
+
+/* attention_coverage (pipeline.hpp:198-243): per query head, the fraction of
+ * the true causal attention probability mass (on the original, unpermuted
+ * q, k) that falls inside the selected blocks of the permuted grid: key j
+ * counts for query i iff mask[h][sigma^{-1}(i)/B][pi^{-1}(j)/B].  The
+ * reference streams rows in double and caps N^2 at 2^26; here each row's mass
+ * is exp(lse_selected - lse_causal) from two attention passes (block-sparse
+ * over the permuted grid, dense causal over the original order), so it runs at
+ * full length.  sigma / pi may be NULL (identity).  coverage: device double
+ * [Hq].  Tolerance vs the reference: 1e-5 on f32 inputs, 1e-3 on bf16 (the
+ * tensor-core pass uses approximate exp2). */
+PBS_API int pbs_attention_coverage(const void* q, const void* k, const pbs_shape* shape, int64_t block_size,
+                                   const uint8_t* mask, const int32_t* sigma, const int32_t* pi, double scale,
+                                   double* coverage, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- test hooks ---------------------------------------------------------- */
 /* y[i] = the device port of glibc expf (the reference's std::exp(float)). */
 PBS_API int pbs_debug_expf(const float* x, float* y, int64_t n, void* stream);

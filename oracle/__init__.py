@@ -234,6 +234,19 @@ class Oracle:
             _p(q_orig, C.c_int32), _p(k_orig, C.c_int32), _p(out, _F[dt])))
         return out
 
+    # ---- attention_coverage (pipeline.hpp:198-243)
+    def attention_coverage(self, q, k, mask, block_size, sigma=None, pi=None, scale=0.0):
+        dt = q.dtype.type
+        q, k = self._arr(q, dt), self._arr(k, dt)
+        mask = self._arr(mask, np.uint8)
+        sigma = None if sigma is None else self._arr(sigma, np.int32)
+        pi = None if pi is None else self._arr(pi, np.int32)
+        out = C.c_double(0.0)
+        self._check(self._fn("attention_coverage", dt)(
+            _p(q, _F[dt]), _p(k, _F[dt]), _SZ(q.shape[0]), _SZ(q.shape[1]), _p(mask, C.c_uint8),
+            _SZ(block_size), _p(sigma, C.c_int32), _p(pi, C.c_int32), C.c_double(scale), C.byref(out)))
+        return out.value
+
     # ---- a12 pbs_attention (pipeline.hpp:107-193)
     def pbs_attention(self, q, k, v, cfg: PipelineConfig) -> PipelineResult:
         dt = q.dtype.type

@@ -61,7 +61,10 @@ extern "C" {
                                   REAL* out);                                                  \
   int pbso_pbs_attention_##SFX(const REAL* q, const REAL* k, const REAL* v, size_t n,          \
                                size_t d, const pbs_pipeline_config* cfg, REAL* out,            \
-                               int32_t* sigma, int32_t* pi, uint8_t* mask, pbs_report* rep);
+                               int32_t* sigma, int32_t* pi, uint8_t* mask, pbs_report* rep);   \
+  int pbso_attention_coverage_##SFX(const REAL* q, const REAL* k, size_t n, size_t d,          \
+                                    const uint8_t* mask, size_t block, const int32_t* sigma,   \
+                                    const int32_t* pi, double scale, double* coverage);
 
 PBSO_DECL(float, f32)
 PBSO_DECL(double, f64)

@@ -182,6 +182,20 @@ int oracle_attn(const T* q, std::size_t n, const T* k, const T* v, std::size_t m
 }
 
 template <typename T>
+int coverage(const T* q, const T* k, std::size_t n, std::size_t d, const uint8_t* mask, std::size_t block,
+             const int32_t* sigma, const int32_t* pi, double scale, double* out) {
+  try {
+    const std::size_t t = (n + block - 1) / block;
+    pbs::BlockMask bm(t, t, block, 0);
+    for (std::size_t r = 0; r < t; ++r)
+      for (std::size_t c = 0; c < t; ++c) bm.set(r, c, mask[r * t + c] != 0);
+    *out = pbs::attention_coverage(to_mat(q, n, d), to_mat(k, n, d), bm, pbs::Permutation(idx_in(sigma, n)),
+                                   pbs::Permutation(idx_in(pi, n)), scale);
+    return 0;
+  } catch (const pbs::Error& e) { return fail(e); } catch (const std::exception& e) { return fail_other(e); }
+}
+
+template <typename T>
 void fill_report(const pbs::PipelineResult<T>& res, pbs_report* rep) {
   if (!rep) return;
   rep->block_density = res.report.block_density;
@@ -264,6 +278,11 @@ const char* pbsref_last_error(void) { return g_err.c_str(); }
                                  const pbs_pipeline_config* cfg, T* out, int32_t* sigma,           \
                                  int32_t* pi, uint8_t* mask, pbs_report* rep) {                    \
     return pipeline<T>(q, k, v, n, d, cfg, out, sigma, pi, mask, rep);                             \
+  }                                                                                                \
+  int pbsref_attention_coverage_##SFX(const T* q, const T* k, size_t n, size_t d,                  \
+                                      const uint8_t* mask, size_t block, const int32_t* sigma,     \
+                                      const int32_t* pi, double scale, double* cov) {              \
+    return coverage<T>(q, k, n, d, mask, block, sigma, pi, scale, cov);                            \
   }
 
 PBSREF_DEFS(float, f32)

@@ -30,7 +30,7 @@ EXPORTS = [
     "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_apply_rows",
     "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_block_sparse_attention_fwd",
     "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
-    "pbs_debug_expf",
+    "pbs_coverage_workspace_size", "pbs_attention_coverage", "pbs_debug_expf",
 ]
 
 
@@ -116,6 +116,8 @@ _SIGS = {
                                 C.POINTER(Report), VP]),
     "pbs_attention_host": (C.c_int, [VP, VP, VP, C.POINTER(Shape), C.POINTER(PipelineConfig), VP, VP, VP, VP,
                                      C.POINTER(Report)]),
+    "pbs_coverage_workspace_size": (SZ, [C.POINTER(Shape), I64]),
+    "pbs_attention_coverage": (C.c_int, [VP, VP, C.POINTER(Shape), I64, VP, VP, VP, DBL, VP, VP, SZ, VP]),
     "pbs_debug_expf": (C.c_int, [VP, VP, I64, VP]),
 }
 

@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(kRows* kLanes) attn_simt_kernel(AttnParams p, 
     }
   }
   if (!active) return;
+  const int64_t orow = p.out_rows ? (int64_t)p.out_rows[(int64_t)h * p.n + i] : i;
+  if (p.lse && lane == 0) p.lse[(int64_t)h * p.n + orow] = l > 0.0f ? m + logf(l) : -INFINITY;
   if (l == 0.0f) {
     if (p.status && lane == 0) {
       p.status[0] = 1;
@@ -106,7 +108,6 @@ __global__ void __launch_bounds__(kRows* kLanes) attn_simt_kernel(AttnParams p, 
     return;
   }
   const float inv = 1.0f / l;
-  const int64_t orow = p.out_rows ? (int64_t)p.out_rows[(int64_t)h * p.n + i] : i;
   T* out = static_cast<T*>(p.out) + ((int64_t)h * p.n + orow) * d;
   for (int c = 0; c < per; ++c) {
     const int col = lane * per + c;

@@ -333,6 +333,7 @@ struct KernelArgs {
   const int2* q_mm;  // [hq][t] min/max of q_orig per block (nullptr: identity)
   const int2* k_mm;  // [hq][t] min/max of k_orig per block
   int32_t* status;
+  float* lse;  // [hq][n] in output-row order, or nullptr
   __nv_bfloat16* out;
   int causal;   // identity element mask when q_orig/k_orig are null
   int dense;    // dense causal list (kb = 0..qb)
@@ -833,9 +834,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.status[0] = 1;
         atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
       }
+      const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
+      if (a.lse && valid && part == 0)  // natural-log LSE: l = sum 2^(s c - m), c = scale log2(e)
+        a.lse[(int64_t)it.h * a.n + orow] = (l > 0.0f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
       if (vis.len > 0) {
         const float inv = (l > 0.0f) ? 1.0f / l : 0.0f;
-        const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
         __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + part * (kD / kSplit);
 #pragma unroll 1
         for (int c = 0; c < kD / kSplit / 32; ++c) {
@@ -993,6 +996,7 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   a.k_orig = p.k_orig;
   a.out_rows = p.out_rows;
   a.status = p.status;
+  a.lse = p.lse;
   a.out = static_cast<__nv_bfloat16*>(p.out);
   a.causal = p.causal;
   a.dense = p.kv_idx == nullptr;

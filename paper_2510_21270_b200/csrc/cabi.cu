@@ -299,6 +299,109 @@ int pbs_dense_causal_attention_fwd(const void* q, const void* k, const void* v, 
   return run_attention(p, nullptr, as_stream(stream));
 }
 
+namespace {
+struct CoverageLayout {
+  size_t qp, kp, o, lse_s, lse_d, kv_idx, kv_cnt, total;
+};
+CoverageLayout coverage_plan(const pbs_shape* shape, int64_t block) {
+  const int64_t n = shape->seq_len, d = shape->head_dim, hq = shape->num_q_heads, t = ceil_div(n, block);
+  const size_t es = shape->dtype == PBS_DTYPE_BF16 ? 2 : 4;
+  CoverageLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return at;
+  };
+  L.qp = take((size_t)hq * n * d * es);
+  L.kp = take((size_t)hq * n * d * es);
+  L.o = take((size_t)hq * n * d * es);
+  L.lse_s = take((size_t)hq * n * 4);
+  L.lse_d = take((size_t)hq * n * 4);
+  L.kv_idx = take((size_t)hq * t * t * 4);
+  L.kv_cnt = take((size_t)hq * t * 4);
+  L.total = off + 256;
+  return L;
+}
+}  // namespace
+
+size_t pbs_coverage_workspace_size(const pbs_shape* shape, int64_t block_size) {
+  if (check_shape(shape) || block_size <= 0) return 0;
+  return coverage_plan(shape, block_size).total;
+}
+
+int pbs_attention_coverage(const void* q, const void* k, const pbs_shape* shape, int64_t block_size,
+                           const uint8_t* mask, const int32_t* sigma, const int32_t* pi, double scale,
+                           double* coverage, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_shape(shape)) return rc;
+  if (block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention_coverage: block size must be >= 1");
+  if (!mask || !coverage) return fail(PBS_ERR_CONFIG, "E_SHAPE", "attention_coverage: mask and coverage are required");
+  const CoverageLayout L = coverage_plan(shape, block_size);
+  if (workspace == nullptr || workspace_bytes < L.total)
+    return fail(PBS_ERR_RESOURCE, "E_RESOURCE",
+                "coverage workspace of " + std::to_string(workspace_bytes) + " bytes, need " + std::to_string(L.total));
+  cudaStream_t st = as_stream(stream);
+  char* ws = static_cast<char*>(workspace);
+  const int hq = shape->num_q_heads, hkv = shape->num_kv_heads, d = shape->head_dim;
+  const int64_t n = shape->seq_len, t = ceil_div(n, block_size);
+  const int es = shape->dtype == PBS_DTYPE_BF16 ? 2 : 4;
+  int32_t* kv_idx = reinterpret_cast<int32_t*>(ws + L.kv_idx);
+  int32_t* kv_cnt = reinterpret_cast<int32_t*>(ws + L.kv_cnt);
+  float* lse_s = reinterpret_cast<float*>(ws + L.lse_s);
+  float* lse_d = reinterpret_cast<float*>(ws + L.lse_d);
+  if (int rc = launch_mask_to_lists(mask, hq, t, kv_idx, kv_cnt, st)) return rc;
+  // the permuted grid: Q' = sigma Q, K' = pi K (V is irrelevant to the mass: K' stands in)
+  const void* qp = q;
+  const void* kp = k;
+  int kv_heads = hkv;
+  if (sigma) {
+    if (int rc = launch_apply_rows(sigma, q, hq, hq, n, d, es, ws + L.qp, st)) return rc;
+    qp = ws + L.qp;
+  }
+  if (pi) {
+    if (int rc = launch_apply_rows(pi, k, hkv, hq, n, d, es, ws + L.kp, st)) return rc;
+    kp = ws + L.kp;
+    kv_heads = hq;
+  }
+  AttnParams p{};
+  p.q = qp;
+  p.k = kp;
+  p.v = kp;
+  p.out = ws + L.o;
+  p.dtype = shape->dtype;
+  p.hq = hq;
+  p.kv_heads = kv_heads;
+  p.d = d;
+  p.n = n;
+  p.block = block_size;
+  p.scale = effective_scale(scale, d);
+  p.kv_idx = kv_idx;
+  p.kv_cnt = kv_cnt;
+  p.q_orig = sigma;
+  p.k_orig = pi;
+  p.out_rows = sigma;  // lse rows back in original order
+  p.causal = (sigma == nullptr && pi == nullptr) ? 1 : 0;
+  p.lse = lse_s;
+  if (int rc = run_attention(p, nullptr, st)) return rc;
+  // the true causal mass of every row (dense causal pass over the original order)
+  AttnParams dp{};
+  dp.q = q;
+  dp.k = k;
+  dp.v = k;
+  dp.out = ws + L.o;
+  dp.dtype = shape->dtype;
+  dp.hq = hq;
+  dp.kv_heads = hkv;
+  dp.d = d;
+  dp.n = n;
+  dp.block = 128;
+  dp.scale = effective_scale(scale, d);
+  dp.causal = 1;
+  dp.lse = lse_d;
+  if (int rc = run_attention(dp, nullptr, st)) return rc;
+  return launch_coverage_reduce(lse_s, lse_d, hq, n, coverage, st);
+}
+
 int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream) {
   int32_t h[2] = {0, 0};
   PBS_CUDA_CHECK(cudaMemcpyAsync(h, status, sizeof h, cudaMemcpyDeviceToHost, as_stream(stream)));

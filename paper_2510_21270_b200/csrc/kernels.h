@@ -40,6 +40,11 @@ int launch_score_select(const float* qbar, const float* kbar, float* logits_ws, 
                         int64_t block, int64_t segment, float scale, double tau, int forced_first, int forced_band,
                         int select, float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
                         double* row_cov, cudaStream_t st);
+// mask -> per-row ascending key-block lists (the attention's CSR)
+int launch_mask_to_lists(const uint8_t* mask, int hq, int64_t t, int32_t* kv_idx, int32_t* kv_cnt, cudaStream_t st);
+// coverage[h] = mean over rows of exp(lse_sparse - lse_dense) (attention_coverage)
+int launch_coverage_reduce(const float* lse_sparse, const float* lse_dense, int hq, int64_t n, double* coverage,
+                           cudaStream_t st);
 // selection from precomputed scores (pbs_select_blocks)
 int launch_select_from_scores(const float* scores, int hq, int64_t t, int64_t block,
                               int64_t segment, double tau, int forced_first, int forced_band,
@@ -61,6 +66,9 @@ struct AttnParams {
   const int32_t* k_orig;  // pi [Hq, N] or nullptr
   const int32_t* out_rows;  // sigma for the fused un-permute, or nullptr
   int32_t* status;          // device int32[2] or nullptr
+  // per-row log-sum-exp of the scaled, admissible scores (natural log; -inf for
+  // a row with no admissible key), f32 [Hq, N] in output-row order, or nullptr
+  float* lse;
   int causal;               // dense causal comparator mode
 };
 int launch_attention_simt(const AttnParams& p, cudaStream_t st);

@@ -309,3 +309,68 @@ int launch_select_from_scores(const float* scores, int hq, int64_t t, int64_t bl
 }
 
 }  // namespace pbs_b200
+
+// ---- mask -> attention lists, coverage reduction (attention_coverage) ------------
+namespace pbs_b200 {
+namespace {
+
+// one warp per (head, block row): ascending compaction of the row's selected blocks
+__global__ void mask_to_lists_kernel(const uint8_t* __restrict__ mask, int64_t rows, int64_t t,
+                                     int32_t* __restrict__ kv_idx, int32_t* __restrict__ kv_cnt) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= rows) return;
+  const uint8_t* m = mask + g * t;
+  int32_t* out = kv_idx + g * t;
+  int cnt = 0;
+  for (int64_t j0 = 0; j0 < t; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const bool sel = j < t && m[j] != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    if (sel) out[cnt + __popc(bal & ((1u << lane) - 1))] = (int32_t)j;
+    cnt += __popc(bal);
+  }
+  if (lane == 0) kv_cnt[g] = cnt;
+}
+
+// coverage[h] = (1/N) sum_i exp(lse_sparse[h][i] - lse_dense[h][i]): each row's
+// probabilities sum to 1 over its causal keys, so the reference's covered/total
+// (pipeline.hpp:216-242) is the mean per-row covered mass.  Double accumulation.
+__global__ void coverage_reduce_kernel(const float* __restrict__ ls, const float* __restrict__ ld, int64_t n,
+                                       double* __restrict__ coverage) {
+  const int h = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const float a = ls[(int64_t)h * n + i], b = ld[(int64_t)h * n + i];
+    if (a != -INFINITY && b != -INFINITY) acc += exp((double)a - (double)b);
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) coverage[h] = n > 0 ? acc / (double)n : 0.0;
+  }
+}
+
+}  // namespace
+
+int launch_mask_to_lists(const uint8_t* mask, int hq, int64_t t, int32_t* kv_idx, int32_t* kv_cnt, cudaStream_t st) {
+  const int64_t rows = (int64_t)hq * t;
+  if (rows == 0) return PBS_OK;
+  mask_to_lists_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(mask, rows, t, kv_idx, kv_cnt);
+  PBS_LAUNCH_CHECK("mask_to_lists_kernel");
+  return PBS_OK;
+}
+
+int launch_coverage_reduce(const float* lse_sparse, const float* lse_dense, int hq, int64_t n, double* coverage,
+                           cudaStream_t st) {
+  if (hq == 0) return PBS_OK;
+  coverage_reduce_kernel<<<(unsigned)hq, 1024, 0, st>>>(lse_sparse, lse_dense, n, coverage);
+  PBS_LAUNCH_CHECK("coverage_reduce_kernel");
+  return PBS_OK;
+}
+
+}  // namespace pbs_b200

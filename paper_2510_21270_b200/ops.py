@@ -16,6 +16,8 @@ and stream plumbing here.
     attention_block_sparse    attention.hpp:259-310
     dense_causal_attention    attention.hpp:314-321 (causal comparator)
     pbs_attention             pipeline.hpp:107-193
+    attention_coverage        pipeline.hpp:198-243
+    density_sweep             pipeline.hpp:245-295
 """
 from __future__ import annotations
 
@@ -245,6 +247,67 @@ def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=
     check(lib().pbs_attention_host(_ptr(q), _ptr(k), _ptr(v), C.byref(shape), C.byref(cfg), _ptr(out),
                                    _ptr(sigma), _ptr(pi), _ptr(mask), C.byref(rep)))
     return PipelineResult(out, sigma, pi, mask, rep.as_dict())
+
+
+def attention_coverage(q, k, mask, sigma=None, pi=None, block_size=128, scale=0.0):
+    """attention_coverage (pipeline.hpp:198-243) per query head: the fraction of
+    the true causal probability mass of the ORIGINAL q, k that falls inside the
+    selected blocks of the permuted grid.  Returns a float64 CPU tensor [Hq].
+    (No N^2 <= 2^26 cap: the mass is computed from two attention passes.)"""
+    _check_dev(q, k, mask, sigma, pi)
+    shape = make_shape(q, k)
+    need = lib().pbs_coverage_workspace_size(C.byref(shape), int(block_size))
+    if need == 0:
+        check(_lib.PBS_ERR_CONFIG)
+    ws = workspace(need, q.device)
+    cov = torch.empty(q.shape[0], dtype=torch.float64, device=q.device)
+    check(lib().pbs_attention_coverage(_ptr(q), _ptr(k), C.byref(shape), int(block_size), _ptr(mask), _ptr(sigma),
+                                       _ptr(pi), float(scale), _ptr(cov), _ptr(ws), ws.numel(), _stream()))
+    return cov.cpu()
+
+
+@dataclass
+class SweepRow:
+    """SweepRow (pipeline.hpp:234-243); density / coverage averaged over heads."""
+
+    tau: float
+    segment_size: int
+    strategy: str
+    density: float
+    coverage: float
+    max_err: float
+    mean_err: float
+    time_us: float
+
+
+_STRATEGY_NAMES = {0: "none", 1: "key_permute", 2: "query_permute", 3: "both"}
+
+
+def density_sweep(q, k, v, base: PipelineConfig, taus, segment_sizes):
+    """density_sweep (pipeline.hpp:245-295): one pipeline run per (tau, segment
+    size), against the dense causal attention of the same inputs; rows sorted by
+    (segment size, tau).  Errors compare with this library's dense causal
+    attention (the reference compares with its attention_oracle)."""
+    if not taus or not segment_sizes:
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_CONFIG: density_sweep needs at least one tau and one segment size")
+    oracle = dense_causal_attention(q, k, v, scale=base.scale).float()
+    rows = []
+    for s in sorted(segment_sizes):
+        for tau in sorted(taus):
+            cfg = make_config(block_size=int(base.block_size), segment_size=int(s), tau=float(tau),
+                              strategy=_STRATEGY_NAMES[int(base.strategy)], scale=float(base.scale),
+                              forced_first_block=bool(base.forced_first_block),
+                              forced_diagonal_band=bool(base.forced_diagonal_band))
+            res = pbs_attention(q, k, v, cfg)
+            cov = attention_coverage(q, k, res.mask, res.sigma, res.pi, int(cfg.block_size), float(cfg.scale))
+            err = (res.output.float() - oracle).abs()
+            r = res.report
+            rows.append(SweepRow(tau=float(tau), segment_size=int(s), strategy=_STRATEGY_NAMES[int(cfg.strategy)],
+                                 density=r["block_density"], coverage=float(cov.mean()),
+                                 max_err=float(err.max()), mean_err=float(err.mean()),
+                                 time_us=r["estimate_us"] + r["permute_us"] + r["select_us"] + r["attention_us"]
+                                 + r["unpermute_us"]))
+    return rows
 
 
 def debug_expf(x: torch.Tensor) -> torch.Tensor:

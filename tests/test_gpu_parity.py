@@ -329,3 +329,42 @@ def test_dense_causal_many_items_per_slot(ops):
         q[None], k.repeat_interleave(4, 0)[None], v.repeat_interleave(4, 0)[None], is_causal=True)[0]
     err = (out.float() - ref.float()).abs()
     assert err.max().item() <= BF16_MAX and err.mean().item() <= BF16_MEAN, (err.max().item(), err.mean().item())
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-5), ("bf16", 1e-3)])
+@pytest.mark.parametrize("strategy", ["key_permute", "query_permute", "none"])
+def test_attention_coverage_matches_reference(ops, strategy, dtype, tol):
+    """attention_coverage (pipeline.hpp:198-243) on the device (two attention
+    passes, exp(lse_selected - lse_causal) per row) against the compiled
+    reference on the same mask / sigma / pi.  f32 runs the CUDA-core kernel,
+    bf16 the tcgen05 kernel (approximate exp2: 1e-3)."""
+    import oracle as orc
+
+    ref = orc.Oracle("ref") if orc.Oracle.available("ref") else orc.Oracle("oracle")
+    rng = np.random.default_rng(23)
+    hq, hkv, n, d, b, s = 2, 1, 1024 + 64, 128, 128, 256
+    tq, tk, tv, q, k, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0)
+    if dtype == "f32":
+        tq, tk, tv = tq.float(), tk.float(), tv.float()
+    cfg = ops.make_config(block_size=b, segment_size=0 if strategy == "none" else s, tau=0.8, strategy=strategy)
+    res = ops.pbs_attention(tq, tk, tv, cfg)
+    cov = ops.attention_coverage(tq, tk, res.mask, res.sigma, res.pi, b).numpy()
+    sigma, pi, mask = res.sigma.cpu().numpy(), res.pi.cpu().numpy(), res.mask.cpu().numpy()
+    for h in range(hq):
+        want = ref.attention_coverage(q[h], k[kv_of(h, hq, hkv)], mask[h], b, sigma[h], pi[h])
+        assert abs(cov[h] - want) <= tol, (h, cov[h], want)
+
+
+def test_density_sweep_rows(ops):
+    """density_sweep (pipeline.hpp:245-295): rows sorted by (segment, tau),
+    density and coverage monotone in tau, tau = 1 exact against dense causal."""
+    rng = np.random.default_rng(29)
+    tq, tk, tv, *_ = bf16_inputs(rng, 4, 2, 2048, 128, kind="vertical_lines", strength=20.0)
+    rows = ops.density_sweep(tq, tk, tv, ops.make_config(), [1.0, 0.5, 0.9], [512, 256])
+    assert [(r.segment_size, r.tau) for r in rows] == [(256, 0.5), (256, 0.9), (256, 1.0), (512, 0.5),
+                                                      (512, 0.9), (512, 1.0)]
+    for a, c in zip(rows[:2], rows[1:3]):
+        assert a.density <= c.density and a.coverage <= c.coverage + 1e-6
+    full = rows[2]
+    assert abs(full.coverage - 1.0) <= 1e-3 and full.max_err <= BF16_MAX
+    assert all(r.time_us > 0 for r in rows)

@@ -379,3 +379,37 @@ def test_inverse_roundtrip():
     inv = inverse(p)
     np.testing.assert_array_equal(p[inv], np.arange(100))
     np.testing.assert_array_equal(inv[p], np.arange(100))
+
+
+@pytest.mark.parametrize("strategy", ["none", "key_permute", "query_permute", "both"])
+@pytest.mark.parametrize("dtype", [F32, F64])
+def test_attention_coverage_matches_reference(oracle, ref, strategy, dtype):
+    """attention_coverage (pipeline.hpp:198-243): the C restatement equals the
+    compiled reference bit for bit on the pipeline's own mask / sigma / pi."""
+    rng = np.random.default_rng(17)
+    for n, d, b, s, tau in ((130, 8, 8, 16, 0.5), (256, 16, 16, 64, 0.9)):
+        q, k, v = (bf16_round(rng.standard_normal((n, d))).astype(dtype) for _ in range(3))
+        if strategy == "none":
+            s = 0
+        cfg = make_config(block_size=b, segment_size=s, tau=tau, strategy=strategy)
+        r = ref.pbs_attention(q, k, v, cfg)
+        a = oracle.attention_coverage(q, k, r.mask, b, r.sigma, r.pi)
+        want = ref.attention_coverage(q, k, r.mask, b, r.sigma, r.pi)
+        assert a == want
+        assert 0.0 < a <= 1.0
+
+
+def test_attention_coverage_properties(oracle):
+    """Full mask -> coverage 1; tau = 1 selects the whole causal grid (C4);
+    a stricter tau never raises coverage (monotone, block_selection_test.cpp:211-231)."""
+    rng = np.random.default_rng(3)
+    n, d, b, s = 256, 16, 16, 64
+    q, k, v = (rng.standard_normal((n, d)).astype(F64) for _ in range(3))
+    t = n // b
+    assert oracle.attention_coverage(q, k, np.ones((t, t), np.uint8), b) == pytest.approx(1.0, abs=1e-12)
+    cov = []
+    for tau in (0.3, 0.6, 0.9, 1.0):
+        r = oracle.pbs_attention(q, k, v, make_config(block_size=b, segment_size=s, tau=tau))
+        cov.append(oracle.attention_coverage(q, k, r.mask, b, r.sigma, r.pi))
+    assert cov[-1] == pytest.approx(1.0, abs=1e-12)
+    assert all(x <= y + 1e-12 for x, y in zip(cov, cov[1:]))
