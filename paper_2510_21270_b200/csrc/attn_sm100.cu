@@ -73,6 +73,8 @@ constexpr int kPolyPer16 = 6;
 constexpr int kCols = kBN / kSplit;               // key columns per softmax thread
 constexpr int kSoftmaxThreads = 128 * kSplit;
 constexpr int kThreads = 128 + kSoftmaxThreads;
+constexpr int kItemRing = 4;
+constexpr int kItemConsumers = 3 + kSoftmaxThreads / 32;  // warps 0, 1, 2 and the softmax warps
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
 constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | Q | P
@@ -90,6 +92,10 @@ struct __align__(8) Barriers {
   uint64_t p_full;     // P written into TMEM by every softmax thread
   uint64_t pv_done, o_full, o_free;
   uint64_t drained;  // every tcgen05 operation of the MMA issuer complete (before dealloc)
+  // dynamic work distribution: warp 3 claims items from a global counter and
+  // publishes them through this ring to the 11 consumer warps
+  uint64_t item_full[4], item_empty[4];
+  int32_t item_ring[4];
   uint32_t tmem_base;
 };
 
@@ -125,20 +131,16 @@ __device__ __noinline__ void mbar_timeout_trap(uint32_t addr, uint32_t parity) {
          addr, parity);
   __trap();
 }
-// try_wait suspends the warp until the phase completes or this many ns pass, so
-// waiting warps (the producers and the MMA issuer share sub-partitions with the
-// softmax warps) do not spin on the issue slots
-constexpr uint32_t kWaitHintNs = 1000000;
 __device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
       "selp.u32 %0, 1, 0, P1;\n"
       "}\n"
       : "=r"(ok)
-      : "r"(addr), "r"(parity), "r"(kWaitHintNs)
+      : "r"(addr), "r"(parity)
       : "memory");
   return ok != 0;
 }
@@ -340,6 +342,7 @@ struct KernelArgs {
   int64_t items;
   const int32_t* vis;   // [hq][t][t] visited blocks (kb | cls << 30), sparse mode
   const int32_t* nvis;  // [hq][t]
+  int32_t* item_counter;  // zeroed before the launch; items are claimed in order (heaviest first)
   unsigned long long* trace;  // debug timeline of CTA 0 (PBS_ATTN_TRACE), else nullptr
 };
 
@@ -544,6 +547,21 @@ __device__ __forceinline__ float compute_p(const uint32_t (&r)[kCols], float sc,
   return (s0 + s1) + (s2 + s3);
 }
 
+// The item sequence of this CTA, as published by the scheduler warp: every
+// consumer warp reads the same sequence in order; -1 ends it.
+struct ItemStream {
+  uint32_t n = 0;
+  __device__ __forceinline__ int64_t next(Barriers* bar, int lane) {
+    const int slot = (int)(n % kItemRing);
+    mbar_wait(&bar->item_full[slot], (n / kItemRing) & 1);
+    const int32_t idx = *reinterpret_cast<volatile int32_t*>(&bar->item_ring[slot]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar->item_empty[slot]);
+    ++n;
+    return idx;
+  }
+};
+
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const KernelArgs a) {
@@ -571,6 +589,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bar->pv_done, 1);
     mbar_init(&bar->o_full, 1);
     mbar_init(&bar->drained, 1);
+    for (int i = 0; i < kItemRing; ++i) {
+      mbar_init(&bar->item_full[i], 1);
+      mbar_init(&bar->item_empty[i], kItemConsumers);
+    }
     mbar_init(&bar->o_free, kSoftmaxThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -589,7 +611,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warp 0: Q + K ring; warp 2: V ring
     const bool kp = (warp == 0);
     uint32_t q_it = 0, it_k = 0;
-    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
+    ItemStream items;
+    for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
       const int kvh = it.h / a.group;
       Visit vis = visit_begin(a, it);
@@ -674,7 +697,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++v_it;
       ++gp;
     };
-    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
+    ItemStream items;
+    for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
       const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
       mbar_wait(&bar->q_full, q_it & 1);
@@ -699,16 +723,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_commit_w(&bar->drained);
     mbar_wait(&bar->drained, 0);
   } else if (warp == 3) {
-    // debug timeline only (PBS_ATTN_TRACE, CTA 0): completion time of every PV
-    if (a.trace && blockIdx.x == 0) {
-      uint32_t g = 0;
-      for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
-        const Item it = item_of(a, idx);
-        const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
-        for (int e = 0; e < len; ++e, ++g) {
-          mbar_wait(&bar->pv_done, g & 1);
-          if (lane == 0) trace_event(a, 3, g);
-        }
+    // ===================== scheduler: claim items in order, publish them =========
+    if (lane == 0) {
+      for (uint32_t n = 0;; ++n) {
+        const int slot = (int)(n % kItemRing);
+        mbar_wait(&bar->item_empty[slot], ((n / kItemRing) & 1) ^ 1);
+        int32_t idx = atomicAdd(a.item_counter, 1);
+        if ((int64_t)idx >= a.items) idx = -1;
+        *reinterpret_cast<volatile int32_t*>(&bar->item_ring[slot]) = idx;
+        mbar_arrive(&bar->item_full[slot]);  // release: the consumers' wait orders the read after the write
+        if (idx < 0) break;
       }
     }
   } else if (warp >= 4) {
@@ -731,7 +755,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
     uint32_t blk = 0, o_cnt = 0;
-    for (int64_t idx = blockIdx.x; idx < a.items; idx += gridDim.x) {
+    ItemStream items;
+    for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
       Visit vis = visit_begin(a, it);
       const int64_t i = it.qb * kBM + row;
@@ -957,6 +982,31 @@ int make_map(CUtensorMap* map, const void* base, int heads, int64_t n) {
 
 int g_num_sms = 0;
 
+// Library-owned scratch for calls that pass none (the block-sparse / dense C-ABI
+// entries): one grow-only device buffer per stream, so back-to-back calls never
+// go through the allocator (a stream-ordered malloc/free per call showed up as
+// occasional 10-30 ms stalls when the pool returned memory to the driver).
+// Work on one stream is ordered, so the buffer is reused safely by that stream.
+void* stream_scratch(cudaStream_t st, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<cudaStream_t, std::pair<void*, size_t>>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cache) {
+    if (e.first != st) continue;
+    if (e.second.second >= bytes) return e.second.first;
+    cudaStreamSynchronize(st);  // the old buffer may still be in use by this stream
+    cudaFree(e.second.first);
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    e.second = {p, bytes};
+    return p;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  cache.push_back({st, {p, bytes}});
+  return p;
+}
+
 }  // namespace
 
 bool attention_sm100_supported(const AttnParams& p) {
@@ -972,8 +1022,8 @@ bool attention_sm100_supported(const AttnParams& p) {
 
 size_t attention_sm100_workspace_bytes(int hq, int64_t n, int64_t block) {
   const int64_t t = ceil_div(n, block);
-  // block min/max of sigma and pi, then the visit lists and counts
-  return (size_t)2 * hq * t * sizeof(int2) + ((size_t)hq * t * t + (size_t)hq * t) * 4 + 256;
+  // the item counter, block min/max of sigma and pi, then the visit lists and counts
+  return 256 + (size_t)2 * hq * t * sizeof(int2) + ((size_t)hq * t * t + (size_t)hq * t) * 4 + 256;
 }
 
 int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st) {
@@ -1003,11 +1053,13 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   if (a.dense && !p.causal) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention without a block list must be causal");
   a.items = (int64_t)p.hq * t;
   // scratch: block min/max of the original positions + visit lists
-  void* own = nullptr;
-  if (!sched_ws && !a.dense) {
-    PBS_CUDA_CHECK(cudaMallocAsync(&own, attention_sm100_workspace_bytes(p.hq, p.n, p.block), st));
-    sched_ws = own;
+  if (!sched_ws) {
+    sched_ws = stream_scratch(st, a.dense ? 256 : attention_sm100_workspace_bytes(p.hq, p.n, p.block));
+    if (!sched_ws) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "attention scratch allocation failed");
   }
+  a.item_counter = static_cast<int32_t*>(sched_ws);
+  PBS_CUDA_CHECK(cudaMemsetAsync(a.item_counter, 0, sizeof(int32_t), st));
+  sched_ws = static_cast<char*>(sched_ws) + 256;
   if (p.q_orig || p.k_orig) {
     int2* mm = static_cast<int2*>(sched_ws);
     const int64_t rows = (int64_t)p.hq * t;
@@ -1058,7 +1110,6 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
       fclose(f);
     }
   }
-  if (own) PBS_CUDA_CHECK(cudaFreeAsync(own, st));
   return PBS_OK;
 }
 

@@ -158,12 +158,17 @@ def select_blocks(scores, block_size, segment_size, tau, forced_first_block=True
 
 
 def attention_block_sparse(qp, kp, vp, block_size, kv_idx, kv_cnt, q_orig=None, k_orig=None, out_rows=None,
-                           scale=0.0, check_status=True):
-    """Permuted block-sparse attention; raises DegenerateRowError like finalize_into."""
+                           scale=0.0, check_status=True, out=None, status=None):
+    """Permuted block-sparse attention; raises DegenerateRowError like finalize_into.
+    `out` / `status` (int32 [2]) may be preallocated: the call then allocates
+    nothing and never synchronises (check_status=False)."""
     _check_dev(qp, kp, vp, kv_idx, kv_cnt, q_orig, k_orig, out_rows)
     shape = make_shape(qp, kp)
-    out = torch.empty_like(qp)
-    status = torch.tensor([0, 0x7FFFFFFF], dtype=torch.int32, device=qp.device)
+    out = torch.empty_like(qp) if out is None else out
+    if status is None:
+        status = torch.empty(2, dtype=torch.int32, device=qp.device)
+    status[0] = 0
+    status[1] = 0x7FFFFFFF
     check(lib().pbs_block_sparse_attention_fwd(_ptr(qp), _ptr(kp), _ptr(vp), kp.shape[0], C.byref(shape),
                                                block_size, scale, _ptr(kv_idx), _ptr(kv_cnt), _ptr(q_orig),
                                                _ptr(k_orig), _ptr(out_rows), _ptr(out), _ptr(status), _stream()))

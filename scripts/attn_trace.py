@@ -30,7 +30,7 @@ t0 = t[t > 0].min()
 lo, hi = 100, 1500
 sr, pd, md, qk, pv, ms, pvd = (t[6], t[8], t[10], t[4], t[2], t[0], t[3])
 b = np.arange(lo, hi)
-ok = (sr[b] > 0) & (pd[b] > 0) & (qk[b] > 0) & (pv[b] > 0) & (ms[b] > 0) & (sr[b + 2] > 0) & (pvd[b] > 0)
+ok = (sr[b] > 0) & (pd[b] > 0) & (qk[b] > 0) & (pv[b] > 0) & (ms[b] > 0) & (sr[b + 2] > 0)
 b = b[ok]
 med = lambda x: float(np.median(x))
 print(f"CTA 0: blocks {len(b)}   (order per block b: QK(b+1) issued, PV(b-1)... see below)")
