@@ -136,7 +136,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
       "selp.u32 %0, 1, 0, P1;\n"
       "}\n"
       : "=r"(ok)
