@@ -440,8 +440,9 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
   int32_t* kv_idx = static_cast<int32_t*>(at(L.kv_idx));
   int32_t* kv_cnt = static_cast<int32_t*>(at(L.kv_cnt));
   double* row_cov = static_cast<double*>(at(L.row_cov));
-  const int32_t init_status[2] = {0, 0x7fffffff};
-  PBS_CUDA_CHECK(cudaMemcpyAsync(status, init_status, sizeof init_status, cudaMemcpyHostToDevice, st));
+  // status = {0, 0x7f7f7f7f}: memsets (not a host copy) keep the call capturable in a CUDA graph
+  PBS_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
+  PBS_CUDA_CHECK(cudaMemsetAsync(status + 1, 0x7f, sizeof(int32_t), st));
 
   Timer tm(report != nullptr, st);
   tm.mark();

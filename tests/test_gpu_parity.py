@@ -368,3 +368,34 @@ def test_density_sweep_rows(ops):
     full = rows[2]
     assert abs(full.coverage - 1.0) <= 1e-3 and full.max_err <= BF16_MAX
     assert all(r.time_us > 0 for r in rows)
+
+
+def test_pipeline_cuda_graph_replay(ops):
+    """The device pipeline (report=False, caller workspace) is stream-ordered and
+    allocation-free, so the whole of Algorithm 1 (~20 launches) captures into
+    one CUDA graph; replays reproduce the eager output bit for bit, also after
+    the inputs are overwritten in place (the serving pattern)."""
+    rng = np.random.default_rng(31)
+    tq, tk, tv, *_ = bf16_inputs(rng, 8, 2, 4096, 128, kind="vertical_lines", strength=20.0)
+    cfg = ops.make_config()
+    ws = torch.empty(ops.workspace_size(tq, tk, cfg), dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(tq)
+    eager = ops.pbs_attention(tq, tk, tv, cfg, report=False, out=out, return_perms=False, ws=ws).output.clone()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm-up on the capture stream (one-time attribute setup)
+        ops.pbs_attention(tq, tk, tv, cfg, report=False, out=out, return_perms=False, ws=ws)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ops.pbs_attention(tq, tk, tv, cfg, report=False, out=out, return_perms=False, ws=ws)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    tq2, tk2, tv2, *_ = bf16_inputs(np.random.default_rng(32), 8, 2, 4096, 128, kind="vertical_lines")
+    want = ops.pbs_attention(tq2, tk2, tv2, cfg).output
+    tq.copy_(tq2), tk.copy_(tk2), tv.copy_(tv2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
