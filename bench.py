@@ -42,7 +42,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PBS-Attn prefill attention ms at 128K ctx; speedup vs dense FA; TFLOP/s"
-HQ, HKV, N, D = 32, 8, 131072, 128
+# attention shapes of BASELINE.json's configs: (q heads, kv heads, default N, workload prefix)
+MODELS = {"llama": (32, 8, 131072, "llama31_8b_attn"),   # configs[1], configs[2] (the headline)
+          "qwen": (28, 4, 262144, "qwen25_7b_attn")}     # configs[3]
+HQ, HKV, N, D = 32, 8, 131072, 128   # the selected model (set from --model)
+PREFIX = "llama31_8b_attn"
 BLOCK, SEGMENT, TAU = 128, 256, 0.9
 LINE_PERIOD, LINE_SEGS, LINES, STRENGTH = 3, 2, 16, 30.0
 
@@ -53,37 +57,55 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--seq", type=int, default=N)
+    ap.add_argument("--model", choices=sorted(MODELS), default="llama")
+    ap.add_argument("--seq", type=int, default=None, help="sequence length (default: the model's config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seq", type=int, default=8192, help="sequence length of the CPU reference sample")
-    return ap.parse_args()
+    args = ap.parse_args()
+    global HQ, HKV, N, PREFIX
+    HQ, HKV, N, PREFIX = MODELS[args.model]
+    if args.seq is None:
+        args.seq = N
+    return args
 
 
 # ------------------------------------------------------------------ sharding
 def shard_of(rank, world):
-    """Query heads split along KV groups: rank r owns KV heads
-    [r*HKV/world, (r+1)*HKV/world) and their HQ/HKV query heads each.
-    Returns (kv_head0, kv_heads, q_head0, q_heads)."""
-    if HKV % world:
-        raise ValueError(f"{HKV} KV groups do not split over {world} ranks")
-    kv_local = HKV // world
+    """Head-parallel shard: rank r owns query heads
+    [r HQ / world, (r + 1) HQ / world).  Llama's 8 groups of 4 split whole
+    groups over 1/2/4/8 ranks; Qwen's 4 groups of 7 split 3 + 4 on 8 ranks, both
+    halves holding the group's KV head.  Returns (q0, q1, kv_list, g_local):
+    the local K/V are the global KV heads kv_list, local query head j reads
+    local KV head j // g_local (when the local heads do not split evenly over
+    their KV heads, each query head gets its own copy: g_local = 1)."""
+    q0, q1 = rank * HQ // world, (rank + 1) * HQ // world
+    if q1 <= q0:
+        raise ValueError(f"{HQ} query heads do not split over {world} ranks")
     g = HQ // HKV
-    return rank * kv_local, kv_local, rank * kv_local * g, kv_local * g
+    kvs = [h // g for h in range(q0, q1)]
+    uniq = sorted(set(kvs))
+    counts = {kvs.count(x) for x in uniq}
+    if len(counts) == 1:
+        return q0, q1, uniq, counts.pop()
+    return q0, q1, kvs, 1
 
 
 # ------------------------------------------------------------------ workload
-def make_inputs(torch, n, heads_q, heads_kv, kv_head0, device, seed=1234):
-    """Synthetic vertical-lines Q/K/V for KV heads [kv_head0, kv_head0 + heads_kv).
-    Every KV head (and its query group) is generated from its own seed, so any
-    head split reproduces the N=1 problem exactly."""
+def make_inputs(torch, n, q0, q1, kv_list, device, seed=1234):
+    """Synthetic vertical-lines Q/K/V for query heads [q0, q1) and the KV heads
+    kv_list.  Every KV head and its query group come from one generator seeded
+    by the KV head, drawn in a fixed order, so any head split reproduces the
+    N = 1 problem exactly."""
     g = HQ // HKV
-    q = torch.empty(heads_q, n, D, dtype=torch.bfloat16, device=device)
-    k = torch.empty(heads_kv, n, D, dtype=torch.bfloat16, device=device)
-    v = torch.empty(heads_kv, n, D, dtype=torch.bfloat16, device=device)
+    q = torch.empty(q1 - q0, n, D, dtype=torch.bfloat16, device=device)
+    k = torch.empty(len(kv_list), n, D, dtype=torch.bfloat16, device=device)
+    v = torch.empty(len(kv_list), n, D, dtype=torch.bfloat16, device=device)
     nseg = n // SEGMENT
-    for j in range(heads_kv):
-        kvh = kv_head0 + j
+    done = {}
+    for kvh in kv_list:
+        if kvh in done:
+            continue
         gen = torch.Generator(device=device)
         gen.manual_seed(seed * 1000 + kvh)
         u = torch.randn(D, generator=gen, device=device)
@@ -94,11 +116,14 @@ def make_inputs(torch, n, heads_q, heads_kv, kv_head0, device, seed=1234):
         offs = torch.randint(0, SEGMENT, (segs.numel(), LINES), generator=gen, device=device)
         pos = (segs[:, None] * SEGMENT + offs).reshape(-1)
         kk[pos] += STRENGTH * u
-        k[j] = kk.to(torch.bfloat16)
-        v[j] = torch.randn(n, D, generator=gen, device=device).to(torch.bfloat16)
+        done[kvh] = (kk.to(torch.bfloat16), torch.randn(n, D, generator=gen, device=device).to(torch.bfloat16))
         for r in range(g):
             qq = torch.randn(n, D, generator=gen, device=device) + (D ** 0.5) * u
-            q[j * g + r] = qq.to(torch.bfloat16)
+            h = kvh * g + r
+            if q0 <= h < q1:
+                q[h - q0] = qq.to(torch.bfloat16)
+    for j, kvh in enumerate(kv_list):
+        k[j], v[j] = done[kvh]
     return q, k, v
 
 
@@ -163,8 +188,8 @@ def cpu_reference_sample(n_s, threads, seed=99):
     if ref is None:  # reference never built on this machine: time the C restatement instead
         ref = oracle.Oracle("oracle")
         kind = "port"
-    hkv = max(1, threads // (HQ // HKV))
-    q, k, v = make_inputs(torch, n_s, hkv * (HQ // HKV), hkv, 0, "cpu", seed)
+    hkv = max(1, min(HKV, -(-threads // (HQ // HKV))))
+    q, k, v = make_inputs(torch, n_s, 0, min(HQ, hkv * (HQ // HKV)), list(range(hkv)), "cpu", seed)
     q = q[:threads].float().numpy()
     k = k.float().numpy()
     v = v.float().numpy()
@@ -180,10 +205,12 @@ def cpu_reference_sample(n_s, threads, seed=99):
     return wall, rep, kind, q.shape[0]
 
 
-def extrapolate_cpu_ms(wall_s, heads_s, n_s, n_full=N, heads_full=HQ):
+def extrapolate_cpu_ms(wall_s, heads_s, n_s, n_full=None, heads_full=None):
     """Scale a sampled CPU run to the full workload.  The sampled run is
     dominated (>85%) by block-sparse attention, whose work grows as N^2 at a
     fixed selected fraction; heads scale linearly (one head per thread)."""
+    n_full = N if n_full is None else n_full
+    heads_full = HQ if heads_full is None else heads_full
     return wall_s * 1e3 * (n_full / n_s) ** 2 * (heads_full / heads_s)
 
 
@@ -202,14 +229,14 @@ def run_reference(args):
         if i >= args.warmup:
             ms.append(extrapolate_cpu_ms(wall, heads, args.cpu_seq, args.seq))
     value = float(np.median(ms))
-    sample = (f"{heads} query heads x {args.cpu_seq} tokens (Llama GQA shapes, same synthetic workload), full "
+    sample = (f"{heads} query heads x {args.cpu_seq} tokens ({args.model} GQA shapes, same synthetic workload), full "
               f"reference pbs_attention per head on {threads} std::threads; wall time scaled by "
               f"(N/{args.cpu_seq})^2 x ({HQ}/{heads}) to {HQ} heads x {args.seq} tokens (extrapolated)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"llama31_8b_attn_{args.seq // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
+        "config": {"workload": f"{PREFIX}_{args.seq // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
                    "seq_len": args.seq, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
                    "strategy": "key_permute", "parallelism": "cpu threads"},
         "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": kind, "sample": sample},
@@ -238,19 +265,22 @@ def main():
 
     lib = ops.lib()
     n = args.seq
-    kv0, kv_local, _, hq_local = shard_of(rank, world)
-    q, k, v = make_inputs(torch, n, hq_local, kv_local, kv0, "cuda")
+    q0, q1, kv_list, _ = shard_of(rank, world)
+    q, k, v = make_inputs(torch, n, q0, q1, kv_list, "cuda")
+    max_local = max(shard_of(r, world)[1] - shard_of(r, world)[0] for r in range(world))
     torch.cuda.synchronize()
     cfg = ops.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy="key_permute")
     ws = ops.workspace(ops.workspace_size(q, k, cfg))
-    out = torch.empty_like(q)
-    full = torch.empty(HQ, n, D, dtype=torch.bfloat16, device="cuda") if world > 1 else out
+    # ranks with fewer heads pad their share of the gather (Qwen on 8 GPUs: 3 or 4)
+    out_pad = torch.zeros(max_local, n, D, dtype=torch.bfloat16, device="cuda")
+    out = out_pad[:q1 - q0]
+    full = torch.empty(world * max_local, n, D, dtype=torch.bfloat16, device="cuda") if world > 1 else out
     stream = torch.cuda.current_stream()
 
     def step():
         ops.pbs_attention(q, k, v, cfg, report=False, out=out, return_perms=False, ws=ws)
         if world > 1:
-            dist.all_gather_into_tensor(full, out)
+            dist.all_gather_into_tensor(full, out_pad)
 
     def barrier():
         if world > 1:
@@ -364,7 +394,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (vertical-lines Q/K/V, seeded; selection by the real tau=0.9 algorithm)",
-            "config": {"workload": f"llama31_8b_attn_{n // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
+            "config": {"workload": f"{PREFIX}_{n // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
                        "seq_len": n, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
                        "strategy": "key_permute", "parallelism": f"heads{world}",
                        "l2": "inputs (1.5 GiB) > L2 (126 MB); no flush"},

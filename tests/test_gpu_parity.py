@@ -399,3 +399,25 @@ def test_pipeline_cuda_graph_replay(ops):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, want)
+
+
+def test_pipeline_qwen_gqa_group_of_seven(ops, oracle):
+    """Qwen2.5-7B's GQA (28 q / 4 kv heads: groups of 7, BASELINE configs[3]) on
+    one group plus a 3 + 4 split of it (the 8-GPU shard shape): permutations and
+    masks bit-exact, outputs to the bf16 tolerance."""
+    from oracle import make_config as ocfg
+
+    rng = np.random.default_rng(37)
+    tq, tk, tv, q, k, v = bf16_inputs(rng, 7, 1, 2048 + 64, 128, kind="vertical_lines", strength=20.0)
+    cfg = ops.make_config(tau=0.9)
+    full = ops.pbs_attention(tq, tk, tv, cfg)
+    for lo, hi in ((0, 3), (3, 7)):
+        part = ops.pbs_attention(tq[lo:hi].contiguous(), tk, tv, cfg)
+        assert torch.equal(part.output, full.output[lo:hi])
+        assert torch.equal(part.mask, full.mask[lo:hi])
+    for h in range(7):
+        r = oracle.pbs_attention(q[h], k[0], v[0], ocfg(block_size=128, segment_size=256, tau=0.9))
+        np.testing.assert_array_equal(full.pi[h].cpu().numpy(), r.pi)
+        np.testing.assert_array_equal(full.mask[h].cpu().numpy(), r.mask)
+        err = np.abs(full.output[h].float().cpu().numpy() - r.output)
+        assert err.max() <= BF16_MAX and err.mean() <= BF16_MEAN
