@@ -13,7 +13,7 @@ from paper_2510_21270_b200 import ops  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 dense = len(sys.argv) > 2 and sys.argv[2] == "dense"
-q, k, v = bench.make_inputs(torch, n, 32, 8, 0, "cuda")
+q, k, v = bench.make_inputs(torch, n, 0, 32, list(range(8)), "cuda")
 cfg = ops.make_config(block_size=128, segment_size=256, tau=0.9, strategy="key_permute")
 path = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "attn_trace.bin")
 os.makedirs(os.path.dirname(path), exist_ok=True)
