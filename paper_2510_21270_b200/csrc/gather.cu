@@ -12,21 +12,46 @@
 namespace pbs_b200 {
 namespace {
 
+// kVecPerRow 16-byte vectors per row; a warp moves 32 / kVecPerRow rows per
+// pass (all lanes busy for 256-byte rows) and kUnroll passes' loads are issued
+// before any store, so each lane keeps kUnroll 16-byte loads in flight.
 template <int kVecPerRow>
 __global__ void __launch_bounds__(256) apply_rows_vec_kernel(const int32_t* __restrict__ perm,
                                                              const int4* __restrict__ src, int group,
                                                              int64_t rows, int64_t total_rows,
                                                              int4* __restrict__ dst) {
+  constexpr int kRowsPerPass = kVecPerRow >= 32 ? 1 : 32 / kVecPerRow;
+  constexpr int kVecPerLane = kVecPerRow >= 32 ? kVecPerRow / 32 : 1;
+  constexpr int kUnroll = 4;
   const int lane = threadIdx.x & 31;
+  const int sub = kVecPerRow >= 32 ? 0 : lane / kVecPerRow;  // row of the pass
+  const int col = kVecPerRow >= 32 ? lane : lane % kVecPerRow;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < total_rows; r += nwarps) {
-    const int64_t h = r / rows, i = r % rows;
-    const int64_t s = perm ? perm[r] : i;
-    const int4* sp = src + ((h / group) * rows + s) * kVecPerRow;
-    int4* dp = dst + r * kVecPerRow;
+  const int64_t step = nwarps * kRowsPerPass;
+  for (int64_t base = warp * kRowsPerPass * kUnroll; base < total_rows; base += step * kUnroll) {
+    int4 v[kUnroll][kVecPerLane];
+    int64_t rr[kUnroll];
 #pragma unroll
-    for (int v = lane; v < kVecPerRow; v += 32) dp[v] = __ldg(sp + v);
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t r = base + (int64_t)u * kRowsPerPass + sub;
+      rr[u] = r;
+      if (r < total_rows) {
+        const int64_t h = r / rows, i = r % rows;
+        const int64_t s = perm ? __ldg(perm + r) : i;
+        const int4* sp = src + ((h / group) * rows + s) * kVecPerRow;
+#pragma unroll
+        for (int w = 0; w < kVecPerLane; ++w) v[u][w] = __ldg(sp + col + w * 32);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (rr[u] < total_rows) {
+        int4* dp = dst + rr[u] * kVecPerRow;
+#pragma unroll
+        for (int w = 0; w < kVecPerLane; ++w) dp[col + w * 32] = v[u][w];
+      }
+    }
   }
 }
 
@@ -55,7 +80,7 @@ int launch_apply_rows(const int32_t* perm, const void* src, int src_heads, int d
   const int group = dst_heads / src_heads;
   const int64_t total = rows * dst_heads;
   const int64_t row_bytes = (int64_t)cols * esize;
-  const int blocks = (int)min64(ceil_div(total, 8), 148 * 16);
+  const int blocks = (int)min64(ceil_div(total, 8 * 8), 148 * 16);
   const bool aligned = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
   if (aligned && row_bytes == 256) {
     apply_rows_vec_kernel<16><<<blocks, 256, 0, st>>>(perm, static_cast<const int4*>(src), group, rows, total,

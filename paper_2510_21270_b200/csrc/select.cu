@@ -46,6 +46,59 @@ __global__ void pool_kernel(const T* __restrict__ x, int group, const int32_t* _
   }
 }
 
+// bf16, d % 8 == 0: a thread owns 8 columns (one 16-byte load per row) of one
+// block and sums its rows in order; 128 threads cover 128 / (d / 8) blocks, and
+// four rows' loads (row indices prefetched) are in flight ahead of the adds.
+__global__ void __launch_bounds__(128) pool_bf16x8_kernel(const __nv_bfloat16* __restrict__ x, int group,
+                                                          const int32_t* __restrict__ perm, int64_t n, int d,
+                                                          int64_t block, int64_t t, float* __restrict__ pooled) {
+  const int cg_per_row = d / 8;
+  const int blocks_per_cta = blockDim.x / cg_per_row;
+  const int64_t h = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blocks_per_cta + threadIdx.x / cg_per_row;
+  const int c0 = (threadIdx.x % cg_per_row) * 8;
+  if (b >= t || threadIdx.x >= blocks_per_cta * cg_per_row) return;
+  const int64_t r0 = b * block;
+  const int64_t rc = min(block, n - r0);
+  const __nv_bfloat16* xs = x + (h / group) * n * d + c0;
+  const int32_t* ph = perm ? perm + h * n : nullptr;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  constexpr int kU = 4;
+  int64_t r = r0;
+  for (; r + kU <= r0 + rc; r += kU) {
+    uint4 raw[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t src = ph ? __ldg(ph + r + u) : r + u;
+      raw[u] = __ldg(reinterpret_cast<const uint4*>(xs + src * d));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw[u]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p2[q]);
+        acc[2 * q] = __fadd_rn(acc[2 * q], f.x);
+        acc[2 * q + 1] = __fadd_rn(acc[2 * q + 1], f.y);
+      }
+    }
+  }
+  for (; r < r0 + rc; ++r) {
+    const int64_t src = ph ? ph[r] : r;
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(xs + src * d));
+    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(p2[q]);
+      acc[2 * q] = __fadd_rn(acc[2 * q], f.x);
+      acc[2 * q + 1] = __fadd_rn(acc[2 * q + 1], f.y);
+    }
+  }
+  float* dst = pooled + (h * t + b) * d + c0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) dst[q] = __fdiv_rn(acc[q], (float)rc);
+}
+
 constexpr int kSelThreads = 128;
 
 // block logits: Lb[h][i][j] = (qbar_i . kbar_j) * s for the admissible prefix
@@ -259,6 +312,13 @@ int launch_pool(const void* x, int dtype, int src_heads, int dst_heads, const in
   const int64_t t = ceil_div(n, block);
   if (t == 0) return PBS_OK;
   const int group = dst_heads / src_heads;
+  if (dtype == PBS_DTYPE_BF16 && d % 8 == 0 && d / 8 <= 128 && (uintptr_t)x % 16 == 0) {
+    const int per_cta = 128 / (d / 8);
+    pool_bf16x8_kernel<<<dim3((unsigned)ceil_div(t, per_cta), (unsigned)dst_heads), 128, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), group, perm, n, d, block, t, pooled);
+    PBS_LAUNCH_CHECK("pool_bf16x8_kernel");
+    return PBS_OK;
+  }
   const int threads = std::min(128, ((d + 31) / 32) * 32);
   dim3 grid((unsigned)t, (unsigned)dst_heads);
   if (dtype == PBS_DTYPE_BF16)
