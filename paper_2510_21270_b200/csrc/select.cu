@@ -221,8 +221,15 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
           keys[hi] = p;
         }
       }
-      __syncthreads();
+      // comparisons x in [32w, 32w + 32) (+ multiples of the block) touch only
+      // elements [64w, 64w + 64) while stride < 32: when the NEXT stage's
+      // stride is below 32 it reads only this warp's elements, and a warp
+      // barrier suffices
+      const int next_stride = stride > 1 ? stride >> 1 : size;
+      if (next_stride < 32) __syncwarp();
+      else __syncthreads();
     }
+  __syncthreads();
   if (warp == 0) {
     double cum = 0.0;
     int take = (int)a;  // fallback: every admissible block (line 188)
