@@ -317,23 +317,6 @@ def main():
         for key in stage:
             stage[key] += r[key] / reps
 
-    # dense causal FlashAttention comparator (same kernel family, full causal grid)
-    dout = torch.empty_like(q)
-    for _ in range(args.warmup):
-        ops.dense_causal_attention(q, k, v, out=dout)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        ops.dense_causal_attention(q, k, v, out=dout)
-    e1.record(stream)
-    barrier()
-    dense_ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([dense_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dense_ms = t.item()
-
     # e2e through the reference-facing host-buffer C-ABI call
     e2e = None
     if not args.no_e2e:
@@ -356,6 +339,23 @@ def main():
         bo = out.numel() * out.element_size()
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "timing": "host wall clock around the synchronous C-ABI call (pinned host buffers)"}
+
+    # dense causal FlashAttention comparator (same kernel family, full causal grid)
+    dout = torch.empty_like(q)
+    for _ in range(args.warmup):
+        ops.dense_causal_attention(q, k, v, out=dout)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ops.dense_causal_attention(q, k, v, out=dout)
+    e1.record(stream)
+    barrier()
+    dense_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([dense_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dense_ms = t.item()
 
     # FLOP accounting: executed = 4 B^2 d per selected block pair (band
     # tiles in full); dense-causal = 4 d N(N+1)/2 per head

@@ -135,6 +135,12 @@ struct Timer {
     if (on)
       for (auto& e : ev) cudaEventDestroy(e);
   }
+  Timer(const Timer&) = delete;
+  Timer& operator=(const Timer&) = delete;
+  void restart(cudaStream_t s) {
+    st = s;
+    k = 0;
+  }
   void mark() {
     if (on && k < 6) cudaEventRecord(ev[k++], st);
   }
@@ -416,9 +422,14 @@ int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream) {
   return PBS_OK;
 }
 
-int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* shape, const pbs_pipeline_config* cfg,
-                  void* out, int32_t* sigma_out, int32_t* pi_out, uint8_t* mask_out, void* workspace,
-                  size_t workspace_bytes, pbs_report* report, void* stream) {
+}  // extern "C"
+
+namespace pbs_b200 {
+namespace {
+// Algorithm 1 enqueued on `stream` (no synchronisation); stage events go to tm.
+int pipeline_enqueue(const void* q, const void* k, const void* v, const pbs_shape* shape,
+                     const pbs_pipeline_config* cfg, void* out, int32_t* sigma_out, int32_t* pi_out,
+                     uint8_t* mask_out, void* workspace, size_t workspace_bytes, Timer& tm, void* stream) {
   if (int rc = check_shape(shape)) return rc;
   if (int rc = check_cfg(cfg)) return rc;
   const Layout L = plan(shape, cfg);
@@ -444,7 +455,6 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
   PBS_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
   PBS_CUDA_CHECK(cudaMemsetAsync(status + 1, 0x7f, sizeof(int32_t), st));
 
-  Timer tm(report != nullptr, st);
   tm.mark();
   // ---- stage 1: estimate (pipeline.hpp:129-155)
   const void* kp = k;
@@ -527,16 +537,27 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
   if (int rc = run_attention(p, at(L.sched), st)) return rc;
   tm.mark();
   tm.mark();  // un-permute is fused into the attention epilogue
-  if (!report) return PBS_OK;
+  return PBS_OK;
+}
 
-  // ---- report (pipeline.hpp:182-191)
-  std::vector<int32_t> cnt((size_t)hq * t);
-  std::vector<double> cov((size_t)hq * t);
-  int32_t hs[2];
-  PBS_CUDA_CHECK(cudaMemcpyAsync(cnt.data(), kv_cnt, cnt.size() * 4, cudaMemcpyDeviceToHost, st));
-  PBS_CUDA_CHECK(cudaMemcpyAsync(cov.data(), row_cov, cov.size() * 8, cudaMemcpyDeviceToHost, st));
-  PBS_CUDA_CHECK(cudaMemcpyAsync(hs, status, sizeof hs, cudaMemcpyDeviceToHost, st));
-  PBS_CUDA_CHECK(cudaStreamSynchronize(st));
+// The per-row counters the report needs, copied to host memory on `st`
+// (asynchronous; complete once `st` reaches this point).
+int report_fetch(const pbs_shape* shape, const pbs_pipeline_config* cfg, const void* workspace, int32_t* cnt,
+                 double* cov, int32_t* hs, cudaStream_t st) {
+  const Layout L = plan(shape, cfg);
+  const char* ws = static_cast<const char*>(workspace);
+  const int64_t t = ceil_div(shape->seq_len, cfg->block_size), hq = shape->num_q_heads;
+  PBS_CUDA_CHECK(cudaMemcpyAsync(cnt, ws + L.kv_cnt, (size_t)hq * t * 4, cudaMemcpyDeviceToHost, st));
+  PBS_CUDA_CHECK(cudaMemcpyAsync(cov, ws + L.row_cov, (size_t)hq * t * 8, cudaMemcpyDeviceToHost, st));
+  PBS_CUDA_CHECK(cudaMemcpyAsync(hs, ws + L.status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  return PBS_OK;
+}
+
+// ---- report (pipeline.hpp:182-191) from the fetched counters
+int report_build(const pbs_shape* shape, const pbs_pipeline_config* cfg, const int32_t* cnt, const double* cov,
+                 const int32_t* hs, const Timer& tm, pbs_report* report) {
+  const int hq = shape->num_q_heads;
+  const int64_t b = cfg->block_size, s = cfg->segment_size, t = ceil_div(shape->seq_len, b);
   if (hs[0]) {
     return fail(PBS_ERR_DEGENERATE, "E_DEGENERATE",
                 "query block " + std::to_string(hs[1] % t) + " (head " + std::to_string(hs[1] / t) +
@@ -568,6 +589,28 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
   report->unpermute_us = tm.us(4);
   return PBS_OK;
 }
+}  // namespace
+}  // namespace pbs_b200
+
+extern "C" {
+
+int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* shape, const pbs_pipeline_config* cfg,
+                  void* out, int32_t* sigma_out, int32_t* pi_out, uint8_t* mask_out, void* workspace,
+                  size_t workspace_bytes, pbs_report* report, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  Timer tm(report != nullptr, st);
+  if (int rc = pipeline_enqueue(q, k, v, shape, cfg, out, sigma_out, pi_out, mask_out, workspace, workspace_bytes,
+                                tm, stream))
+    return rc;
+  if (!report) return PBS_OK;
+  const int64_t t = ceil_div(shape->seq_len, cfg->block_size), hq = shape->num_q_heads;
+  std::vector<int32_t> cnt((size_t)hq * t);
+  std::vector<double> cov((size_t)hq * t);
+  int32_t hs[2];
+  if (int rc = report_fetch(shape, cfg, workspace, cnt.data(), cov.data(), hs, st)) return rc;
+  PBS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return report_build(shape, cfg, cnt.data(), cov.data(), hs, tm, report);
+}
 
 // ---- host-buffer entry: library-owned device arena, pipelined by KV group ------
 //
@@ -583,6 +626,12 @@ struct Arena {
   int device = -1;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_rep[2] = {nullptr, nullptr};
+  // per slot: stage timers and pinned copies of the report counters, so a
+  // group's report is built while the next group computes
+  Timer* timer[2] = {nullptr, nullptr};
+  char* pinned = nullptr;
+  size_t pinned_bytes = 0;
 };
 Arena g_arena;
 
@@ -593,6 +642,8 @@ int arena_streams(Arena& A) {
     PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_in[i], cudaEventDisableTiming));
     PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_done[i], cudaEventDisableTiming));
     PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_out[i], cudaEventDisableTiming));
+    PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_rep[i], cudaEventDisableTiming));
+    A.timer[i] = new Timer(true, A.st[1]);
   }
   return PBS_OK;
 }
@@ -662,35 +713,33 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   char* ho_ = static_cast<char*>(out);
   pbs_report total{};
   double dens = 0.0, cov = 0.0;
-  auto copy_in = [&](int64_t c) -> int {
-    Slot& S = sl[c % nslots];
-    if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_in, A.ev_out[c % nslots], 0));  // slot drained
-    PBS_CUDA_CHECK(cudaMemcpyAsync(S.q, hq_ + (size_t)c * qb, qb, cudaMemcpyHostToDevice, s_in));
-    PBS_CUDA_CHECK(cudaMemcpyAsync(S.k, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
-    PBS_CUDA_CHECK(cudaMemcpyAsync(S.v, hv_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
-    PBS_CUDA_CHECK(cudaEventRecord(A.ev_in[c % nslots], s_in));
-    return PBS_OK;
+  // pinned report counters per slot: kv_cnt (int32), row_cov (double), status
+  const size_t rep_bytes = al((size_t)g * t * 4) + al((size_t)g * t * 8) + 256;
+  if (report && A.pinned_bytes < rep_bytes * 2) {
+    if (A.pinned) cudaFreeHost(A.pinned);
+    A.pinned = nullptr;
+    A.pinned_bytes = 0;
+    PBS_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&A.pinned), rep_bytes * 2, cudaHostAllocDefault));
+    A.pinned_bytes = rep_bytes * 2;
+  }
+  auto rep_cnt = [&](int i) { return reinterpret_cast<int32_t*>(A.pinned + i * rep_bytes); };
+  auto rep_cov = [&](int i) { return reinterpret_cast<double*>(A.pinned + i * rep_bytes + al((size_t)g * t * 4)); };
+  auto rep_hs = [&](int i) {
+    return reinterpret_cast<int32_t*>(A.pinned + i * rep_bytes + al((size_t)g * t * 4) + al((size_t)g * t * 8));
   };
-  if (int rc = copy_in(0)) return rc;
-  for (int64_t c = 0; c < hkv; ++c) {
-    Slot& S = sl[c % nslots];
-    if (c + 1 < hkv && nslots > 1)
-      if (int rc = copy_in(c + 1)) return rc;
-    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_in[c % nslots], 0));
+  // fold the report of group c (its counters were fetched on s_run) into the total
+  auto fold = [&](int64_t c) -> int {
+    const int i = (int)(c % nslots);
+    PBS_CUDA_CHECK(cudaEventSynchronize(A.ev_rep[i]));
     pbs_report r{};
-    if (int rc = pbs_attention(S.q, S.k, S.v, &cs, cfg, S.out, sigma ? S.sig : nullptr, pi ? S.pi : nullptr,
-                               mask ? S.mask : nullptr, S.ws, ws, &r, s_run))
-      return rc;  // (the report path synchronises s_run)
-    PBS_CUDA_CHECK(cudaEventRecord(A.ev_done[c % nslots], s_run));
-    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_out, A.ev_done[c % nslots], 0));
-    PBS_CUDA_CHECK(cudaMemcpyAsync(ho_ + (size_t)c * qb, S.out, qb, cudaMemcpyDeviceToHost, s_out));
-    if (sigma) PBS_CUDA_CHECK(cudaMemcpyAsync(sigma + (size_t)c * g * n, S.sig, pb, cudaMemcpyDeviceToHost, s_out));
-    if (pi) PBS_CUDA_CHECK(cudaMemcpyAsync(pi + (size_t)c * g * n, S.pi, pb, cudaMemcpyDeviceToHost, s_out));
-    if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask + (size_t)c * mb, S.mask, mb, cudaMemcpyDeviceToHost, s_out));
-    PBS_CUDA_CHECK(cudaEventRecord(A.ev_out[c % nslots], s_out));
-    if (nslots == 1 && c + 1 < hkv) {
-      PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
-      if (int rc = copy_in(c + 1)) return rc;
+    if (int rc = report_build(&cs, cfg, rep_cnt(i), rep_cov(i), rep_hs(i), *A.timer[i], &r)) {
+      if (rc == PBS_ERR_DEGENERATE) {  // name the head in the whole problem
+        const int32_t hfull = (int32_t)(c * g + rep_hs(i)[1] / t);
+        return fail(PBS_ERR_DEGENERATE, "E_DEGENERATE",
+                    "query block " + std::to_string(rep_hs(i)[1] % t) + " (head " + std::to_string(hfull) +
+                        ") has an empty softmax denominator (all keys masked)");
+      }
+      return rc;
     }
     total.selected_blocks += r.selected_blocks;
     total.total_admissible_blocks += r.total_admissible_blocks;
@@ -702,7 +751,52 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     total.select_us += r.select_us;
     total.attention_us += r.attention_us;
     total.unpermute_us += r.unpermute_us;
+    return PBS_OK;
+  };
+  auto copy_in = [&](int64_t c) -> int {
+    Slot& S = sl[c % nslots];
+    if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_in, A.ev_out[c % nslots], 0));  // slot drained
+    PBS_CUDA_CHECK(cudaMemcpyAsync(S.q, hq_ + (size_t)c * qb, qb, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaMemcpyAsync(S.k, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaMemcpyAsync(S.v, hv_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_in[c % nslots], s_in));
+    return PBS_OK;
+  };
+  if (int rc = copy_in(0)) return rc;
+  for (int64_t c = 0; c < hkv; ++c) {
+    const int i = (int)(c % nslots);
+    Slot& S = sl[i];
+    if (c + 1 < hkv && nslots > 1)
+      if (int rc = copy_in(c + 1)) return rc;
+    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_in[i], 0));
+    Timer& tm = *A.timer[i];
+    tm.restart(s_run);
+    tm.on = report != nullptr;
+    if (int rc = pipeline_enqueue(S.q, S.k, S.v, &cs, cfg, S.out, sigma ? S.sig : nullptr, pi ? S.pi : nullptr,
+                                  mask ? S.mask : nullptr, S.ws, ws, tm, s_run))
+      return rc;
+    if (report) {
+      if (int rc = report_fetch(&cs, cfg, S.ws, rep_cnt(i), rep_cov(i), rep_hs(i), s_run)) return rc;
+      PBS_CUDA_CHECK(cudaEventRecord(A.ev_rep[i], s_run));
+    }
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_done[i], s_run));
+    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_out, A.ev_done[i], 0));
+    PBS_CUDA_CHECK(cudaMemcpyAsync(ho_ + (size_t)c * qb, S.out, qb, cudaMemcpyDeviceToHost, s_out));
+    if (sigma) PBS_CUDA_CHECK(cudaMemcpyAsync(sigma + (size_t)c * g * n, S.sig, pb, cudaMemcpyDeviceToHost, s_out));
+    if (pi) PBS_CUDA_CHECK(cudaMemcpyAsync(pi + (size_t)c * g * n, S.pi, pb, cudaMemcpyDeviceToHost, s_out));
+    if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask + (size_t)c * mb, S.mask, mb, cudaMemcpyDeviceToHost, s_out));
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_out[i], s_out));
+    // the previous group's report, while this one computes (its slot's
+    // counters are overwritten only two groups later, after this fold)
+    if (report && c > 0)
+      if (int rc = fold(c - 1)) return rc;
+    if (nslots == 1 && c + 1 < hkv) {
+      PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
+      if (int rc = copy_in(c + 1)) return rc;
+    }
   }
+  if (report && hkv > 0)
+    if (int rc = fold(hkv - 1)) return rc;
   PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
   total.block_density = dens / (double)hkv;
   total.pooled_score_coverage = cov / (double)hkv;

@@ -232,7 +232,7 @@ def pbs_attention(q, k, v, cfg: PipelineConfig | None = None, report=True, out=N
     return PipelineResult(out, sigma, pi, mask, rep.as_dict() if rep else None)
 
 
-def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=False, out=None):
+def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=False, out=None, report=True):
     """The reference-facing call on HOST (CPU) tensors: copies in, runs, copies out.
     Pass pinned host tensors (and a pinned `out`) for full PCIe bandwidth."""
     cfg = cfg or make_config()
@@ -248,10 +248,10 @@ def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=
         sigma = torch.empty(hq, n, dtype=torch.int32)
         pi = torch.empty(hq, n, dtype=torch.int32)
         mask = torch.empty(hq, t, t, dtype=torch.uint8)
-    rep = Report()
+    rep = Report() if report else None
     check(lib().pbs_attention_host(_ptr(q), _ptr(k), _ptr(v), C.byref(shape), C.byref(cfg), _ptr(out),
-                                   _ptr(sigma), _ptr(pi), _ptr(mask), C.byref(rep)))
-    return PipelineResult(out, sigma, pi, mask, rep.as_dict())
+                                   _ptr(sigma), _ptr(pi), _ptr(mask), C.byref(rep) if rep else None))
+    return PipelineResult(out, sigma, pi, mask, rep.as_dict() if rep else None)
 
 
 def attention_coverage(q, k, mask, sigma=None, pi=None, block_size=128, scale=0.0):
