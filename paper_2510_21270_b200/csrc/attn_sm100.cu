@@ -65,32 +65,34 @@ constexpr int kBN = 128;      // keys per tile (= block size B)
 constexpr int kD = 128;       // head dim
 constexpr int kKStages = 3;   // K ring depth (freed as soon as QK^T completes)
 constexpr int kVStages = 2;   // V ring depth (freed when PV completes)
-constexpr int kSplit = 2;                         // threads per query row
-// keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the
-// MUFU (tests/micro/softmax_exp_bench.cu: 64 keys x 2 warps per SMSP, 1073 ->
-// ~900 cycles per pass at 4-6 of 16)
-constexpr int kPolyPer16 = 6;
-constexpr int kCols = kBN / kSplit;               // key columns per softmax thread
-constexpr int kSoftmaxThreads = 128 * kSplit;
+// Two softmax warpgroups take alternate visited blocks of an item (split-KV
+// inside the CTA): each thread owns one query row (one TMEM lane) and all 128
+// keys of its warpgroup's blocks, with its own running max, sum and O
+// accumulator; the two states merge once per item in the epilogue.
+constexpr int kGroups = 2;
+constexpr int kCols = kBN;                        // key columns per softmax thread
+constexpr int kSoftmaxThreads = 128 * kGroups;
 constexpr int kThreads = 128 + kSoftmaxThreads;
+constexpr int kRegsControl = 72;                  // setmaxnreg: producers / MMA issuer / scheduler
+constexpr int kRegsSoftmax = 208;                 //             softmax warpgroups
+static_assert((168 - kRegsControl) * 128 >= (kRegsSoftmax - 168) * kSoftmaxThreads, "register file split");
+// keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the MUFU
+constexpr int kPolyPer16 = 2;
 constexpr int kItemRing = 4;
 constexpr int kItemConsumers = 3 + kSoftmaxThreads / 32;  // warps 0, 1, 2 and the softmax warps
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
-constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O | Q | P
-__host__ __device__ constexpr uint32_t col_s(int b) { return b ? 128u : 0u; }
-constexpr uint32_t kColO = 256;   // O: 128 fp32 columns
-constexpr uint32_t kColQ = 384;   // Q: 128 x 128 bf16 = 64 columns, the A operand of S = Q K^T
-constexpr uint32_t kColP = 448;   // P: 128 x 128 bf16 = 64 columns, the A operand of O += P V
+constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O0 | O1
+__host__ __device__ constexpr uint32_t col_s(int w) { return (uint32_t)w * 128u; }
+__host__ __device__ constexpr uint32_t col_o(int w) { return 256u + (uint32_t)w * 128u; }
 
 struct __align__(8) Barriers {
   uint64_t q_full, q_empty;
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
-  uint64_t s_full[2];  // S[b] = Q K^T complete
-  uint64_t s_free[2];  // S[b] read into registers by every softmax thread
-  uint64_t p_full;     // P written into TMEM by every softmax thread
-  uint64_t pv_done, o_full, o_free;
+  uint64_t s_full[kGroups];  // S_w = Q K^T complete (and every earlier MMA: the group's previous PV)
+  uint64_t p_full[kGroups];  // P_w written into TMEM over S_w by the group's 128 threads
+  uint64_t o_full, o_free;   // the item's last PV complete / both groups' epilogue read O
   uint64_t drained;  // every tcgen05 operation of the MMA issuer complete (before dealloc)
   // dynamic work distribution: warp 3 claims items from a global counter and
   // publishes them through this ring to the 11 consumer warps
@@ -104,9 +106,9 @@ struct SmemLayout {
   static constexpr int q = 0;
   static constexpr int k = q + kTileBytes;
   static constexpr int v = k + kKStages * kTileBytes;
-  static constexpr int korig = v + kVStages * kTileBytes;      // int[128]
-  static constexpr int xch = korig + 128 * 4;  // float [2 buf][kSplit][128] row maxima + [kSplit][128] sums
-  static constexpr int bars = xch + (2 * kSplit + kSplit) * 128 * 4;
+  static constexpr int korig = v + kVStages * kTileBytes;  // int [kGroups][128]
+  static constexpr int xch = korig + kGroups * 128 * 4;    // float [2 items][kGroups][2 (m, l)][128]
+  static constexpr int bars = xch + 2 * kGroups * 2 * 128 * 4;
   static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
 };
 static_assert(SmemLayout::total <= 232448, "shared memory budget");
@@ -124,13 +126,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Bounded wait: a deadlock becomes a diagnosable trap (~10 s at 2 GHz)
-// instead of a hung GPU.  The clock is only read after the first failed probe.
-__device__ __noinline__ void mbar_timeout_trap(uint32_t addr, uint32_t parity) {
-  printf("pbs_b200: mbarrier wait timed out (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x, threadIdx.x,
-         addr, parity);
-  __trap();
-}
+// Bounded wait: a deadlock becomes a trap (~10 s at 2 GHz; the launch then fails
+// with an illegal-instruction error) instead of a hung GPU.  The trap is inline:
+// a call (e.g. to printf) would make every wait site an ABI call boundary and
+// force the softmax's 128 live scores into local memory.
 __device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -149,7 +148,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try(addr, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try(addr, parity))
-    if (clock64() - t0 > 20000000000ll) mbar_timeout_trap(addr, parity);
+    if (clock64() - t0 > 20000000000ll) asm volatile("trap;");
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
@@ -518,28 +517,33 @@ __device__ __forceinline__ float load_scores(uint32_t tS, const int* ko, int qo,
   return max3(max3(mx[0], mx[1], mx[2]), max3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
 }
 
-// Pass 2: p = 2^(s * scale_log2 - m) -> bf16 pairs (two keys per 32-bit word,
-// the A-operand layout of the PV MMA in TMEM); returns sum p.  Packed f32x2
-// FMA/add; kPolyPer16 of every 16 keys take the FMA-pipe polynomial.
+// Pass 2: p = 2^(s * scale_log2 - m) -> bf16 pairs written into TMEM over the
+// consumed S columns (two keys per 32-bit column: the A-operand layout of the
+// PV MMA), one 32-key chunk at a time; returns sum p.  Packed f32x2 FMA/add;
+// kPolyPer16 of every 16 keys take the FMA-pipe polynomial.
 template <int kPolyPer16>
-__device__ __forceinline__ float compute_p(const uint32_t (&r)[kCols], float sc, float neg_m,
-                                           uint32_t (&pk)[kCols / 2]) {
+__device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, float neg_m, uint32_t tP) {
   const uint64_t sc2 = pk2(sc, sc), nm2 = pk2(neg_m, neg_m);
   uint64_t sum2[2] = {0ull, 0ull};
 #pragma unroll
-  for (int jp = 0; jp < kCols / 2; ++jp) {
-    const int j = 2 * jp;
-    float y0, y1, p0, p1;
-    upk2(ffma2(pk2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sc2, nm2), y0, y1);
-    if ((j & 15) >= 16 - kPolyPer16) {
-      exp2_poly2(y0, y1, p0, p1);
-    } else {
-      p0 = ex2(y0);
-      p1 = ex2(y1);
+  for (int c = 0; c < kCols / 32; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int jp = 0; jp < 16; ++jp) {
+      const int j = c * 32 + 2 * jp;
+      float y0, y1, p0, p1;
+      upk2(ffma2(pk2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sc2, nm2), y0, y1);
+      if ((j & 15) >= 16 - kPolyPer16) {
+        exp2_poly2(y0, y1, p0, p1);
+      } else {
+        p0 = ex2(y0);
+        p1 = ex2(y1);
+      }
+      sum2[jp & 1] = fadd2(sum2[jp & 1], pk2(p0, p1));
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+      pk[jp] = *reinterpret_cast<uint32_t*>(&b2);
     }
-    sum2[jp & 1] = fadd2(sum2[jp & 1], pk2(p0, p1));
-    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-    pk[jp] = *reinterpret_cast<uint32_t*>(&b2);
+    TMEM_ST16(tP + c * 16, pk);
   }
   float s0, s1, s2, s3;
   upk2(sum2[0], s0, s1);
@@ -581,19 +585,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar->v_full[s], 1);
       mbar_init(&bar->v_empty[s], 1);
     }
-    mbar_init(&bar->s_full[0], 1);
-    mbar_init(&bar->s_full[1], 1);
-    mbar_init(&bar->s_free[0], kSoftmaxThreads);
-    mbar_init(&bar->s_free[1], kSoftmaxThreads);
-    mbar_init(&bar->p_full, kSoftmaxThreads);
-    mbar_init(&bar->pv_done, 1);
+    for (int w = 0; w < kGroups; ++w) {
+      mbar_init(&bar->s_full[w], 1);
+      mbar_init(&bar->p_full[w], 128);
+    }
     mbar_init(&bar->o_full, 1);
+    mbar_init(&bar->o_free, kSoftmaxThreads);
     mbar_init(&bar->drained, 1);
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(&bar->item_full[i], 1);
       mbar_init(&bar->item_empty[i], kItemConsumers);
     }
-    mbar_init(&bar->o_free, kSoftmaxThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -606,7 +608,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
 
-  if (warp == 0 || warp == 2) {
+  if (warp < 4) {
+   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
+   if (warp == 0 || warp == 2) {
     // ===================== TMA producers (lane 0 issues) =====================
     // warp 0: Q + K ring; warp 2: V ring
     const bool kp = (warp == 0);
@@ -641,61 +645,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++it_k;
       }
     }
-  } else if (warp == 1) {
+   } else if (warp == 1) {
     // ===================== MMA issuer (warp-collective, one elected lane) ========
+    // Per item: S_0 = Q K_0^T, S_1 = Q K_1^T, then for e = 0, 1, ...:
+    //   O_w (+)= P_e V_e (w = e & 1, once the group's softmax wrote P_e over S_w)
+    //   S_w = Q K_{e+2}^T (after that PV in issue order: it overwrites P_e)
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
-    // Blocks are numbered globally across this CTA's items; block g uses S[g & 1].
-    // QK^T runs two blocks ahead of PV: QK(g + 2) needs only that the softmax
-    // has read S(g) into registers (s_free), not that P(g) is done, so it is
-    // issued before PV(g) and overlaps the softmax of block g.
-    // o_no: non-empty items so far.  o_free has one phase per non-empty item
-    // (an item without visited blocks has no epilogue reading O, and the
-    // softmax does not arrive for it: an arrival the issuer did not wait for
-    // could complete a phase early)
-    uint32_t q_it = 0, k_it = 0, v_it = 0, o_no = 0, gq = 0, gp = 0;
-    auto issue_qk = [&]() {
-      const int b = gq & 1;
-      mbar_wait(&bar->s_free[b], ((gq >> 1) & 1) ^ 1);  // the softmax has read S(gq - 2)
+    uint32_t q_it = 0, k_it = 0, v_it = 0, o_no = 0, p_cnt[kGroups] = {0, 0};
+    auto issue_qk = [&](int e, int len) {
+      const int w = e & 1;
       const uint32_t stage = k_it % kKStages;
-      if (lane == 0) trace_event(a, 7, gq);  // MMA ready to issue QK
       mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
-      if (lane == 0) trace_event(a, 1, gq);  // K tile present
       tc_fence_after();
       const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
 #pragma unroll
       for (int k = 0; k < kD / 16; ++k) {
+        const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
         const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-        tc_mma_ts_w(tmem + col_s(b), tmem + kColQ + k * 8, bd, idesc_qk, k > 0 ? 1u : 0u);
+        tc_mma_w(tmem + col_s(w), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
       }
-      if (lane == 0) trace_event(a, 4, gq);
-      tc_commit_w(&bar->s_full[b]);
+      tc_commit_w(&bar->s_full[w]);
       tc_commit_w(&bar->k_empty[stage]);
+      if (e + 1 == len) tc_commit_w(&bar->q_empty);  // every QK of the item issued: Q is free once they complete
       ++k_it;
-      ++gq;
-    };
-    auto issue_pv = [&](int pe, int len) {
-      const uint32_t stage = v_it % kVStages;
-      mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
-      if (lane == 0) trace_event(a, 5, gp);  // V tile present
-      mbar_wait(&bar->p_full, gp & 1);
-      if (lane == 0) trace_event(a, 0, gp);
-      if (pe == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // previous item's epilogue read O
-      tc_fence_after();
-      const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
-#pragma unroll
-      for (int k = 0; k < kBN / 16; ++k) {
-        // A = P [128 q x 16 kv] in TMEM (8 columns); B = V [16 kv x 128 d] MN-major SW128
-        const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-        tc_mma_ts_w(tmem + kColO, tmem + kColP + k * 8, bd, idesc_pv, (pe == 0 && k == 0) ? 0u : 1u);
-      }
-      if (lane == 0) trace_event(a, 2, gp);
-      tc_commit_w(&bar->pv_done);
-      tc_commit_w(&bar->v_empty[stage]);
-      if (pe == len - 1) tc_commit_w(&bar->o_full);
-      ++v_it;
-      ++gp;
     };
     ItemStream items;
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
@@ -703,26 +677,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
       mbar_wait(&bar->q_full, q_it & 1);
       ++q_it;
-      // Q -> TMEM once per item: S = Q K^T then reads Q from TMEM (TS form), so
-      // the per-block shared-memory traffic of QK^T is K alone.  tcgen05.cp runs
-      // in issue order with the MMAs, after the previous item's last QK^T.
-      tc_fence_after();
-#pragma unroll
-      for (int k = 0; k < kD / 16; ++k)
-        tc_cp_w(tmem + kColQ + k * 8, sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024));
-      tc_commit_w(&bar->q_empty);  // the Q tile in shared memory is free once copied
-      for (int e = 0; e < len && e < 2; ++e) issue_qk();
-      for (int e = 0; e < len; ++e) {
-        if (e + 2 < len) issue_qk();
-        issue_pv(e, len);
+      if (len == 0) {
+        tc_commit_w(&bar->q_empty);
+        continue;
       }
-      if (len > 0) ++o_no;
+      for (int e = 0; e < len && e < kGroups; ++e) issue_qk(e, len);
+      for (int e = 0; e < len; ++e) {
+        const int w = e & 1;
+        const uint32_t stage = v_it % kVStages;
+        mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
+        mbar_wait(&bar->p_full[w], p_cnt[w] & 1);
+        ++p_cnt[w];
+        if (e == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // the previous epilogue read O_0 and O_1
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kBN / 16; ++k) {
+          // A = P [128 q x 16 kv] in TMEM (8 columns over S_w); B = V [16 kv x 128 d] MN-major SW128
+          const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
+          tc_mma_ts_w(tmem + col_o(w), tmem + col_s(w) + k * 8, bd, idesc_pv, (e < kGroups && k == 0) ? 0u : 1u);
+        }
+        tc_commit_w(&bar->v_empty[stage]);
+        if (e + 1 == len) tc_commit_w(&bar->o_full);
+        ++v_it;
+        if (e + kGroups < len) issue_qk(e + kGroups, len);
+      }
+      ++o_no;
     }
-    // nothing may still write TMEM when it is released (e.g. the Q copy of a
-    // trailing item without visited blocks)
+    // nothing may still write TMEM when it is released
     tc_commit_w(&bar->drained);
     mbar_wait(&bar->drained, 0);
-  } else if (warp == 3) {
+   } else {
     // ===================== scheduler: claim items in order, publish them =========
     if (lane == 0) {
       for (uint32_t n = 0;; ++n) {
@@ -735,26 +720,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (idx < 0) break;
       }
     }
-  } else if (warp >= 4) {
-    // ===================== softmax: kSplit threads per row =====================
-    // warps 4..7 own keys [0, 64) of every block, warps 8..11 keys [64, 128); each
-    // group of four covers the four TMEM lane quadrants (warp % 4).  The two
-    // threads of a row share one running max (their block maxima are exchanged
-    // through shared memory once per block) and therefore the one O; each keeps
-    // its own partial sum and rescales / writes its own 64 output columns.
-    const int part = (warp - 4) >> 2;    // key columns [kCols part, kCols part + kCols)
-    const int quad = warp & 3;           // TMEM lane quadrant of this warp
-    const int row = quad * 32 + lane;    // query row within the tile
-    const int st = threadIdx.x - 128;    // 0..255
+   }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    // ===================== softmax: group w takes the item's blocks e = w, w+2, ...
+    // One thread per query row (TMEM lane) and all 128 keys of the block, with the
+    // group's own running max m, sum l and accumulator O_w.  O_w is stable when
+    // S_w is ready: the group's previous PV was issued before that QK^T, whose
+    // commit covers it, so the lazy rescale needs no wait.
+    const int w = (warp - 4) >> 2;     // softmax group
+    const int quad = warp & 3;         // TMEM lane quadrant of this warp
+    const int row = quad * 32 + lane;  // query row within the tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tO = tmem + lane_off + kColO + part * (kD / kSplit);
-    int* ko_all = reinterpret_cast<int*>(smem + SmemLayout::korig);
-    const int* ko = ko_all + part * kCols;
-    float* xmax = reinterpret_cast<float*>(smem + SmemLayout::xch);  // [2][kSplit][128]
-    float* xsum = xmax + 2 * kSplit * 128;                           // [kSplit][128]
+    const uint32_t tS = tmem + lane_off + col_s(w);
+    const uint32_t tO = tmem + lane_off + col_o(w);
+    int* ko = reinterpret_cast<int*>(smem + SmemLayout::korig) + w * 128;
+    float* xch = reinterpret_cast<float*>(smem + SmemLayout::xch);  // [2 items][kGroups][2][128]
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
-    uint32_t blk = 0, o_cnt = 0;
+    uint32_t s_cnt = 0, o_cnt = 0;
     ItemStream items;
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
@@ -762,70 +746,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t i = it.qb * kBM + row;
       const bool valid = i < a.n;
       const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
-      float m = -INFINITY;  // the row's running max (log2 domain), identical in both threads
-      float l = 0.0f;       // this thread's partial running sum
-      for (int e = 0; e < vis.len; ++e, ++blk) {
+      float m = -INFINITY;  // this group's running max (log2 domain)
+      float l = 0.0f;       // this group's running sum
+      for (int e = w; e < vis.len; e += kGroups) {
         int64_t kb;
         int cls;
-        if (st == 0) trace_event(a, 9, blk);  // softmax loop top
         visit_get(a, it, vis, e, lane, kb, cls);
-        if (st == 0) trace_event(a, 11, blk);  // visit entry known
-        if (cls == 1) {
-          if (st < 128) {
-            const int64_t j = kb * kBN + st;
-            int v = 0x7fffffff;
-            if (j < a.n) v = a.k_orig ? a.k_orig[(int64_t)it.h * a.n + j] : (int)j;
-            if (!any_mask && j < a.n) v = -1;  // unmasked: only the ragged tail
-            ko_all[st] = v;
-          }
-          named_bar_sync(1, kSoftmaxThreads);
+        if (cls == 1) {  // original positions of the block's keys, for this group
+          const int64_t j = kb * kBN + row;
+          int v = 0x7fffffff;
+          if (j < a.n) v = a.k_orig ? a.k_orig[(int64_t)it.h * a.n + j] : (int)j;
+          if (!any_mask && j < a.n) v = -1;  // unmasked: only the ragged tail
+          ko[row] = v;
+          named_bar_sync(1 + w, 128);
         }
-        const int b = blk & 1;
-        mbar_wait(&bar->s_full[b], (blk >> 1) & 1);
-        if (st == 0) trace_event(a, 6, blk);
+        mbar_wait(&bar->s_full[w], s_cnt & 1);
+        ++s_cnt;
         tc_fence_after();
-        const uint32_t tS = tmem + lane_off + col_s(b) + part * kCols;
         uint32_t r[kCols];
-        const float hmax = (cls == 1) ? load_scores<true>(tS, ko, qo, r) : load_scores<false>(tS, ko, qo, r);
-        // S[b] is in registers: the MMA issuer may compute S(blk + 2) into it
-        tc_fence_before();
-        mbar_arrive(&bar->s_free[b]);
-        if (cls == 1) named_bar_sync(1, kSoftmaxThreads);  // ko[] may be refilled after this
-        // the row's block max from both halves (double-buffered by block parity:
-        // a buffer is rewritten only after the next block's barrier)
-        float* xb = xmax + (blk & 1) * kSplit * 128;
-        xb[part * 128 + row] = hmax;
-        named_bar_sync(3, kSoftmaxThreads);
-        float bmax = xb[row];
+        if (cls == 1) {
+          // ElementMask (attention.hpp:41-73) applied in TMEM, 32 columns at a
+          // time, so the 128 scores below are loaded already masked
+#pragma unroll 1
+          for (int c = 0; c < kCols / 32; ++c) {
+            uint32_t t32[32];
+            TMEM_LD32(tS + c * 32, t32);
+            tmem_wait_ld();
 #pragma unroll
-        for (int q = 1; q < kSplit; ++q) bmax = fmaxf(bmax, xb[q * 128 + row]);
-        bmax *= sc;
-        if (st == 0) trace_event(a, 10, blk);
+            for (int j = 0; j < 32; ++j)
+              if (ko[c * 32 + j] > qo) t32[j] = 0xff800000u;  // -inf: inadmissible (attention.hpp:298-300)
+            TMEM_ST32(tS + c * 32, t32);
+          }
+          tmem_wait_st();
+          named_bar_sync(1 + w, 128);  // ko may be refilled after this
+        }
+        const float hmax = load_scores<false>(tS, ko, qo, r);
         // online softmax (absorb, attention.hpp:96-126) in the log2 domain with
-        // lazy rescaling: O is rescaled only when the max grows by more than 8
-        const float m_new = fmaxf(m, bmax);
-        bool need_rescale = false;
+        // lazy rescaling: O_w is rescaled only when the max grows by more than 8
+        const float m_new = fmaxf(m, hmax * sc);
         float factor = 1.0f;
+        bool rescale = false;
         if (m_new != -INFINITY) {
           if (m == -INFINITY) {
-            m = m_new;  // nothing accumulated for this row yet (O is exactly 0)
+            m = m_new;  // nothing accumulated for this row in O_w yet (exactly 0)
           } else if (m_new > m + 8.0f) {
             factor = ex2(m - m_new);
-            need_rescale = true;
+            rescale = true;
             m = m_new;
           }
         }
         const float neg_m = (m == -INFINITY) ? 0.0f : -m;
-        uint32_t pk[kCols / 2];
-        const float rs = compute_p<kPolyPer16>(r, sc, neg_m, pk);
-        l = l * factor + rs;
-        // P is single-buffered in TMEM and O is rescaled in place: both need the
-        // previous PV complete (every PV is waited on, so the phases stay exact)
-        if (blk > 0) mbar_wait(&bar->pv_done, (blk - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, need_rescale)) {
+        if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll 1
-          for (int c = 0; c < kD / kSplit / 32; ++c) {
+          for (int c = 0; c < kD / 32; ++c) {
             uint32_t o[32];
             TMEM_LD32(tO + c * 32, o);
             tmem_wait_ld();
@@ -834,62 +807,74 @@ __global__ void __launch_bounds__(kThreads, 1)
             TMEM_ST32(tO + c * 32, o);
           }
         }
-        // keys [kCols part, +kCols) -> P columns [kCols/2 part, +kCols/2)
-        const uint32_t tP = tmem + lane_off + kColP + part * (kCols / 2);
-#pragma unroll
-        for (int c = 0; c < kCols / 32; ++c) TMEM_ST16(tP + c * 16, (pk + c * 16));
+        const float rs = emit_p<kPolyPer16>(r, sc, neg_m, tS);
+        l = l * factor + rs;
         tmem_wait_st();
-        if (st == 0) trace_event(a, 8, blk);
         tc_fence_before();
-        mbar_arrive(&bar->p_full);
+        mbar_arrive(&bar->p_full[w]);
       }
-      // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138):
-      // O / l -> out[out_rows[i]] (the fused un-permute, pipeline.hpp:178)
-      if (vis.len > 0) {
-        xsum[part * 128 + row] = l;
-        named_bar_sync(2, kSoftmaxThreads);
-        l = 0.0f;
-#pragma unroll
-        for (int q = 0; q < kSplit; ++q) l += xsum[q * 128 + row];
-        mbar_wait(&bar->o_full, o_cnt & 1);  // the item's last PV
-        ++o_cnt;
+      // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138): merge
+      // the two groups' (m, l, O), O / l -> out[out_rows[i]] (the fused
+      // un-permute, pipeline.hpp:178); group w writes output columns [64 w, 64 w + 64)
+      if (vis.len == 0) {
+        if (valid && a.status && w == 0) {
+          a.status[0] = 1;
+          atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
+        }
+        continue;
       }
+      float* xb = xch + (o_cnt & 1) * kGroups * 2 * 128;  // by item parity: the next item's writes cannot race
+      xb[(w * 2 + 0) * 128 + row] = m;
+      xb[(w * 2 + 1) * 128 + row] = l;
+      named_bar_sync(3, kSoftmaxThreads);
+      const float m0 = xb[row], l0 = xb[128 + row], m1 = xb[256 + row], l1 = xb[384 + row];
+      mbar_wait(&bar->o_full, o_cnt & 1);  // the item's last PV
+      ++o_cnt;
       tc_fence_after();
-      if (valid && !(l > 0.0f) && a.status && part == 0) {
+      const float mt = fmaxf(m0, m1);
+      const float f0 = (m0 == -INFINITY) ? 0.0f : ex2(m0 - mt);
+      const float f1 = (m1 == -INFINITY) ? 0.0f : ex2(m1 - mt);
+      const float lt = l0 * f0 + l1 * f1;
+      if (valid && !(lt > 0.0f) && a.status && w == 0) {
         a.status[0] = 1;
         atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
       }
       const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
-      if (a.lse && valid && part == 0)  // natural-log LSE: l = sum 2^(s c - m), c = scale log2(e)
-        a.lse[(int64_t)it.h * a.n + orow] = (l > 0.0f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
-      if (vis.len > 0) {
-        const float inv = (l > 0.0f) ? 1.0f / l : 0.0f;
-        __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + part * (kD / kSplit);
+      if (a.lse && valid && w == 0)  // natural-log LSE: l = sum 2^(s c - m), c = scale log2(e)
+        a.lse[(int64_t)it.h * a.n + orow] = (lt > 0.0f) ? (mt + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
+      const float inv = (lt > 0.0f) ? 1.0f / lt : 0.0f;
+      const float g0 = f0 * inv, g1 = f1 * inv;
+      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + w * (kD / kGroups);
 #pragma unroll 1
-        for (int c = 0; c < kD / kSplit / 32; ++c) {
-          uint32_t o[32];
-          TMEM_LD32(tO + c * 32, o);
-          tmem_wait_ld();
-          if (valid && l > 0.0f) {
+      for (int c = 0; c < kD / kGroups / 32; ++c) {
+        const uint32_t col = w * (kD / kGroups) + c * 32;
+        uint32_t o0[32], o1[32];
+        TMEM_LD32(tmem + lane_off + col_o(0) + col, o0);
+        TMEM_LD32(tmem + lane_off + col_o(1) + col, o1);
+        tmem_wait_ld();
+        if (valid && lt > 0.0f) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              uint32_t pk[4];
+          for (int u = 0; u < 4; ++u) {
+            uint32_t pk[4];
 #pragma unroll
-              for (int w2 = 0; w2 < 4; ++w2) {
-                const int j = u * 8 + 2 * w2;
-                __nv_bfloat162 b2 =
-                    __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
-                pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
+            for (int w2 = 0; w2 < 4; ++w2) {
+              const int j = u * 8 + 2 * w2;
+              // a group without blocks in this item has m = -inf and a stale O: select, never multiply
+              float v0 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j]) * g0;
+              float v1 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j + 1]) * g0;
+              if (m1 != -INFINITY) {
+                v0 = fmaf(__uint_as_float(o1[j]), g1, v0);
+                v1 = fmaf(__uint_as_float(o1[j + 1]), g1, v1);
               }
-              *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+              pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
             }
+            *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
       }
-      if (vis.len > 0) {
-        tc_fence_before();
-        mbar_arrive(&bar->o_free);
-      }
+      tc_fence_before();
+      mbar_arrive(&bar->o_free);
     }
   }
   tc_fence_before();
