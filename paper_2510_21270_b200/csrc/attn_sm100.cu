@@ -76,8 +76,10 @@ constexpr int kThreads = 128 + kSoftmaxThreads;
 constexpr int kRegsControl = 72;                  // setmaxnreg: producers / MMA issuer / scheduler
 constexpr int kRegsSoftmax = 208;                 //             softmax warpgroups
 static_assert((168 - kRegsControl) * 128 >= (kRegsSoftmax - 168) * kSoftmaxThreads, "register file split");
-// keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the MUFU
-constexpr int kPolyPer16 = 2;
+// keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the
+// MUFU; 0: with two groups on alternate blocks the MUFU keeps up (A/B on the box:
+// 0 / 2 / 4 of 16 -> 61 / 62 / 66 ms x GHz for the 128K attention)
+constexpr int kPolyPer16 = 0;
 constexpr int kItemRing = 4;
 constexpr int kItemConsumers = 3 + kSoftmaxThreads / 32;  // warps 0, 1, 2 and the softmax warps
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
