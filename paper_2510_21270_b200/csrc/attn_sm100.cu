@@ -7,38 +7,31 @@
 // in the list of key blocks a query block visits.
 //
 // Tile: B = 128 query rows x 128 keys, d = 128, bf16 in, fp32 accumulate.
-// Persistent CTAs (one per SM) walk (head, query-block) work items, one KV
-// source at a time for L2 locality, heaviest query blocks first.
-// Warp roles (640 threads):
-//   warp 0       TMA producer for Q (once per item) and K (3-stage ring, a
-//                stage is released as soon as its QK^T completes)
-//   warp 2       TMA producer for V (2-stage ring, released after PV)
+// Persistent CTAs (one per SM) take (head, query-block) work items from a
+// global counter (warp 3 publishes them through an mbarrier ring), ordered one
+// KV source at a time for L2 locality, heaviest query blocks first.
+// Warp roles (384 threads; setmaxnreg gives the softmax 208 registers):
+//   warp 0       TMA producer for Q (once per item) and K (3-stage ring)
+//   warp 2       TMA producer for V (2-stage ring)
 //                (cp.async.bulk.tensor through 3-D [H, N, d] maps, SW128)
-//   warp 1       TMEM owner + MMA issuer (one elected lane):
-//                  S[e & 1] = Q K_e^T               (SS: Q, K K-major in smem)
-//                  O0 += P_e[:, :64]  V_e[:64]      (TS: P in TMEM,
-//                  O1 += P_e[:, 64:]  V_e[64:]       V MN-major in smem)
-//                completion via tcgen05.commit onto mbarriers
-//   warp 3       idle
-//   warps 4..11  softmax: two threads per query row (TMEM lane), each owning
-//                64 of the 128 key columns of every block (warps 4..7 the low
-//                half, 8..11 the high half; each group of four covers the
-//                four TMEM lane quadrants, warp % 4).
-// TMEM holds S0 | S1 | O0 | O1: S is double-buffered across visited blocks, so
-// QK^T of block e+1 runs on the tensor core while block e is in softmax, and
-// P_e is written back into TMEM over S_e (bf16, the TS-MMA A layout) and
-// consumed by the PV MMA from there (no shared-memory round trip for P).
-// Each half-row thread runs its own online softmax over its 64 keys of every
-// block (its own running max m and sum l; the PV is split into the two key
-// halves accumulating into O0 / O1), so there is no per-block exchange between
-// threads; the epilogue merges the two states once (m = max, O and l scaled by
-// exp2(m_h - m)).  Per block a thread loads its 64 scores (2 x tcgen05.ld
-// 32x32b.x32), masks partial blocks by original positions, applies the online
-// softmax in the exp2 domain with lazy rescaling (O_h rescaled only when the
-// running max grows by more than 8), and stores P with tcgen05.st (exp2 on the
-// MUFU; an FMA-pipe polynomial path, kPolyExp2, is kept for MUFU-bound
-// configurations).  The epilogue writes O / l straight to row out_rows[i]
-// (the fused un-permute, pipeline.hpp:178).
+//   warp 3       item scheduler
+//   warp 1       TMEM owner + MMA issuer (warp-collective, one elected lane):
+//                  S_w = Q K_e^T        (SS: Q, K K-major in smem), w = e & 1
+//                  O_w (+)= P_e V_e     (TS: P over S_w in TMEM, V MN-major)
+//                per item S_0, S_1, then per block e: PV(e), QK(e + 2)
+//   warps 4..7   softmax group 0: the item's visited blocks e = 0, 2, 4, ...
+//   warps 8..11  softmax group 1: blocks e = 1, 3, 5, ...
+// TMEM holds S_0 | S_1 | O_0 | O_1.  A softmax thread owns one query row (one
+// TMEM lane) and all 128 keys of its group's blocks, with the group's own
+// running max, sum and accumulator (split-KV inside the CTA): no exchange
+// between threads per block, and the two warps of an SM sub-partition work on
+// different blocks, so one's exponentials overlap the other's loads.  Per
+// block: 4 x tcgen05.ld 32x32b.x32 (partial blocks masked in TMEM first), row
+// max (3-input FMNMX), online softmax in the exp2 domain with lazy rescaling
+// (O_w rescaled only when the max grows by more than 8), p = 2^(s c - m) on the
+// MUFU written back over S_w as bf16 (tcgen05.st), then p_full.  The epilogue
+// merges the two groups' (m, l, O) once per item and writes O / l straight to
+// row out_rows[i] (the fused un-permute, pipeline.hpp:178).
 // Block classes follow AdmissibilityIndex::classify (attention.hpp:167-174):
 // per-block [min, max] of original positions; `none` blocks are skipped by
 // every role (an exact no-op, attention.hpp:286), `full` blocks skip the
