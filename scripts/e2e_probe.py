@@ -17,3 +17,7 @@ for rep in (True, False, True):
         ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout, report=rep)
         ts.append((time.perf_counter() - t0) * 1e3)
     print("report", rep, [round(x, 1) for x in ts])
+r = ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout, report=True).report
+print("host-entry stage sums (ms):", {k: round(r[k] / 1e3, 2) for k in ("estimate_us", "permute_us", "select_us", "attention_us")})
+d = ops.pbs_attention(q, k, v, cfg).report
+print("device-entry stages (ms):  ", {k: round(d[k] / 1e3, 2) for k in ("estimate_us", "permute_us", "select_us", "attention_us")})
