@@ -427,9 +427,12 @@ int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream) {
 namespace pbs_b200 {
 namespace {
 // Algorithm 1 enqueued on `stream` (no synchronisation); stage events go to tm.
+// pi_given (key_permute only): pi of every head, computed beforehand (the host
+// entry estimates all heads at once from the keys and the last query rows).
 int pipeline_enqueue(const void* q, const void* k, const void* v, const pbs_shape* shape,
                      const pbs_pipeline_config* cfg, void* out, int32_t* sigma_out, int32_t* pi_out,
-                     uint8_t* mask_out, void* workspace, size_t workspace_bytes, Timer& tm, void* stream) {
+                     uint8_t* mask_out, void* workspace, size_t workspace_bytes, Timer& tm, void* stream,
+                     const int32_t* pi_given = nullptr) {
   if (int rc = check_shape(shape)) return rc;
   if (int rc = check_cfg(cfg)) return rc;
   const Layout L = plan(shape, cfg);
@@ -445,7 +448,7 @@ int pipeline_enqueue(const void* q, const void* k, const void* v, const pbs_shap
   const float scale = effective_scale(cfg->scale, d);
   const int strategy = cfg->strategy;
   int32_t* status = static_cast<int32_t*>(at(L.status));
-  int32_t* pi = pi_out ? pi_out : static_cast<int32_t*>(at(L.pi));
+  int32_t* pi = pi_given ? const_cast<int32_t*>(pi_given) : pi_out ? pi_out : static_cast<int32_t*>(at(L.pi));
   int32_t* sigma = sigma_out ? sigma_out : static_cast<int32_t*>(at(L.sigma));
   uint8_t* mask = mask_out ? mask_out : static_cast<uint8_t*>(at(L.mask));
   int32_t* kv_idx = static_cast<int32_t*>(at(L.kv_idx));
@@ -459,7 +462,11 @@ int pipeline_enqueue(const void* q, const void* k, const void* v, const pbs_shap
   // ---- stage 1: estimate (pipeline.hpp:129-155)
   const void* kp = k;
   int kv_heads = hkv;
-  if (uses_pi(strategy)) {
+  if (pi_given && strategy != PBS_STRATEGY_KEY_PERMUTE)
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "a precomputed pi is only taken under key_permute");
+  if (pi_given) {
+    // stage 1 already done by the caller
+  } else if (uses_pi(strategy)) {
     float* scores = static_cast<float*>(at(L.scores));
     if (int rc = launch_importance(q, k, dt, hq, hkv, n, d, b, scale, scores, at(L.imp),
                                    importance_workspace_bytes(hq, n, b), st))
@@ -666,6 +673,15 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   const size_t ws = pbs_workspace_size(&cs, cfg);
   const size_t slot = al(qb) * 2 + al(kvb) * 2 + al(pb) * 2 + al(mb) + al(ws);
   const int nslots = hkv > 1 ? 2 : 1;
+  // key_permute over several KV groups: estimate every head up front from K and
+  // the last `take` query rows (stage 1 reads nothing else), so the per-group
+  // pipelines skip it.  One all-heads estimate fills the GPU; per-group ones
+  // (4 heads) leave its sequential denominator chains on a few SMs.
+  const bool est_first = cfg->strategy == PBS_STRATEGY_KEY_PERMUTE && hkv > 1;
+  const int64_t take = std::min<int64_t>(cfg->block_size, n);
+  const size_t kall_b = (size_t)hkv * kvb, qtail_b = (size_t)hq * take * d * es;
+  const size_t imp_b = importance_workspace_bytes((int)hq, n, cfg->block_size);
+  const size_t est_bytes = est_first ? al(kall_b) + al(qtail_b) + al(imp_b) + 3 * al((size_t)hq * n * 4) : 0;
   std::lock_guard<std::mutex> lk(g_arena.mu);
   Arena& A = g_arena;
   int dev = 0;
@@ -677,12 +693,12 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     A.bytes = 0;
   }
   if (int rc = arena_streams(A)) return rc;
-  if (A.bytes < slot * nslots) {
+  if (A.bytes < slot * nslots + est_bytes) {
     if (A.ptr) cudaFree(A.ptr);
     A.ptr = nullptr;
     A.bytes = 0;
-    PBS_CUDA_CHECK(cudaMalloc(&A.ptr, slot * nslots));
-    A.bytes = slot * nslots;
+    PBS_CUDA_CHECK(cudaMalloc(&A.ptr, slot * nslots + est_bytes));
+    A.bytes = slot * nslots + est_bytes;
   }
   A.device = dev;
   struct Slot {
@@ -710,6 +726,36 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   const char* hq_ = static_cast<const char*>(q);
   const char* hk_ = static_cast<const char*>(k);
   const char* hv_ = static_cast<const char*>(v);
+  char* k_all = nullptr;
+  int32_t* pi_all = nullptr;
+  Timer est_tm(report != nullptr, s_run);
+  if (est_first) {
+    char* p = static_cast<char*>(A.ptr) + (size_t)nslots * slot;
+    auto take_b = [&](size_t bytes) {
+      char* r = p;
+      p += al(bytes);
+      return r;
+    };
+    k_all = take_b(kall_b);
+    char* q_tail = take_b(qtail_b);
+    char* imp = take_b(imp_b);
+    float* scores = reinterpret_cast<float*>(take_b((size_t)hq * n * 4));
+    pi_all = reinterpret_cast<int32_t*>(take_b((size_t)hq * n * 4));
+    int32_t* pi_inv = reinterpret_cast<int32_t*>(take_b((size_t)hq * n * 4));
+    // K of every KV head and the last `take` rows of every query head first
+    PBS_CUDA_CHECK(cudaMemcpyAsync(k_all, hk_, kall_b, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaMemcpy2DAsync(q_tail, (size_t)take * d * es, hq_ + (size_t)(n - take) * d * es,
+                                     (size_t)n * d * es, (size_t)take * d * es, (size_t)hq, cudaMemcpyHostToDevice,
+                                     s_in));
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_rep[1], s_in));  // (reused: nothing else records it yet)
+    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_rep[1], 0));
+    est_tm.mark();
+    if (int rc = launch_importance(q_tail, k_all, shape->dtype, (int)hq, (int)hkv, n, (int)d, cfg->block_size,
+                                   effective_scale(cfg->scale, (int)d), scores, imp, imp_b, s_run, take))
+      return rc;
+    if (int rc = launch_segmented_sort(scores, 0, (int)hq, n, cfg->segment_size, pi_all, pi_inv, s_run)) return rc;
+    est_tm.mark();
+  }
   char* ho_ = static_cast<char*>(out);
   pbs_report total{};
   double dens = 0.0, cov = 0.0;
@@ -757,7 +803,7 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     Slot& S = sl[c % nslots];
     if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_in, A.ev_out[c % nslots], 0));  // slot drained
     PBS_CUDA_CHECK(cudaMemcpyAsync(S.q, hq_ + (size_t)c * qb, qb, cudaMemcpyHostToDevice, s_in));
-    PBS_CUDA_CHECK(cudaMemcpyAsync(S.k, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
+    if (!est_first) PBS_CUDA_CHECK(cudaMemcpyAsync(S.k, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
     PBS_CUDA_CHECK(cudaMemcpyAsync(S.v, hv_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
     PBS_CUDA_CHECK(cudaEventRecord(A.ev_in[c % nslots], s_in));
     return PBS_OK;
@@ -772,8 +818,10 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     Timer& tm = *A.timer[i];
     tm.restart(s_run);
     tm.on = report != nullptr;
-    if (int rc = pipeline_enqueue(S.q, S.k, S.v, &cs, cfg, S.out, sigma ? S.sig : nullptr, pi ? S.pi : nullptr,
-                                  mask ? S.mask : nullptr, S.ws, ws, tm, s_run))
+    const int32_t* pi_c = est_first ? pi_all + (size_t)c * g * n : nullptr;
+    if (int rc = pipeline_enqueue(S.q, est_first ? k_all + (size_t)c * kvb : S.k, S.v, &cs, cfg, S.out,
+                                  sigma ? S.sig : nullptr, (pi && !est_first) ? S.pi : nullptr,
+                                  mask ? S.mask : nullptr, S.ws, ws, tm, s_run, pi_c))
       return rc;
     if (report) {
       if (int rc = report_fetch(&cs, cfg, S.ws, rep_cnt(i), rep_cov(i), rep_hs(i), s_run)) return rc;
@@ -783,7 +831,8 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     PBS_CUDA_CHECK(cudaStreamWaitEvent(s_out, A.ev_done[i], 0));
     PBS_CUDA_CHECK(cudaMemcpyAsync(ho_ + (size_t)c * qb, S.out, qb, cudaMemcpyDeviceToHost, s_out));
     if (sigma) PBS_CUDA_CHECK(cudaMemcpyAsync(sigma + (size_t)c * g * n, S.sig, pb, cudaMemcpyDeviceToHost, s_out));
-    if (pi) PBS_CUDA_CHECK(cudaMemcpyAsync(pi + (size_t)c * g * n, S.pi, pb, cudaMemcpyDeviceToHost, s_out));
+    if (pi)
+      PBS_CUDA_CHECK(cudaMemcpyAsync(pi + (size_t)c * g * n, est_first ? pi_c : S.pi, pb, cudaMemcpyDeviceToHost, s_out));
     if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask + (size_t)c * mb, S.mask, mb, cudaMemcpyDeviceToHost, s_out));
     PBS_CUDA_CHECK(cudaEventRecord(A.ev_out[i], s_out));
     // the previous group's report, while this one computes (its slot's
@@ -797,6 +846,7 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   }
   if (report && hkv > 0)
     if (int rc = fold(hkv - 1)) return rc;
+  if (report && est_first) total.estimate_us += est_tm.us(0);  // events complete: every fold synchronised later work
   PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
   total.block_density = dens / (double)hkv;
   total.pooled_score_coverage = cov / (double)hkv;

@@ -42,14 +42,16 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // per-row denominator chains (K1bc) read 128-byte lines per step.
 template <typename T, bool kExact, bool kVec>
 __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
-    const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int d, int take, float scale,
-    float* __restrict__ L, unsigned* __restrict__ rowmax) {
+    const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int64_t q_rows, int d, int take,
+    float scale, float* __restrict__ L, unsigned* __restrict__ rowmax) {
   __shared__ __align__(16) xgemm::Smem sm;
   const int h = blockIdx.z;
   const int64_t j0 = (int64_t)blockIdx.x * kTile;
   const int i0 = blockIdx.y * kTile;
-  const int64_t r0 = n - take;
-  const T* a_base = q + ((int64_t)h * n + r0 + i0) * d;
+  // q holds q_rows rows per head (N, or just the last `take` rows), the
+  // estimate reads its last `take`
+  const int64_t r0 = q_rows - take;
+  const T* a_base = q + ((int64_t)h * q_rows + r0 + i0) * d;
   const T* b_base = k + ((int64_t)(h / group) * n + j0) * d;
   const int a_rows = min(kTile, take - i0);
   const int b_rows = (int)min64(kTile, n - j0);
@@ -368,8 +370,10 @@ size_t importance_workspace_bytes(int hq, int64_t n, int64_t block) {
 
 int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, int64_t n, int d,
                       int64_t block, float scale, float* scores, void* ws, size_t ws_bytes,
-                      cudaStream_t st) {
+                      cudaStream_t st, int64_t q_rows) {
   const int take = (int)min64(block, n);
+  if (q_rows <= 0) q_rows = n;
+  if (q_rows < take) return fail(PBS_ERR_CONFIG, "E_SHAPE", "importance: q holds fewer rows than the estimate reads");
   if (ws_bytes < importance_workspace_bytes(hq, n, block))
     return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "importance workspace too small");
   float* L = static_cast<float*>(ws);
@@ -382,13 +386,13 @@ int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, 
   if (dtype == PBS_DTYPE_BF16) {
     auto qq = static_cast<const __nv_bfloat16*>(q);
     auto kk = static_cast<const __nv_bfloat16*>(k);
-    if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
-    else importance_logits_kernel<__nv_bfloat16, true, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
+    if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
+    else importance_logits_kernel<__nv_bfloat16, true, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
   } else {
     auto qq = static_cast<const float*>(q);
     auto kk = static_cast<const float*>(k);
-    if (vec) importance_logits_kernel<float, false, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
-    else importance_logits_kernel<float, false, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, d, take, scale, L, rowmax);
+    if (vec) importance_logits_kernel<float, false, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
+    else importance_logits_kernel<float, false, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
   }
   PBS_LAUNCH_CHECK("importance_logits_kernel");
   const size_t smem = sizeof(float) * kRing * kJT * 32 + 2 * kRing * sizeof(uint64_t);

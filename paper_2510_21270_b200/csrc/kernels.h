@@ -12,9 +12,10 @@ namespace pbs_b200 {
 // Workspace for the exact importance estimate: E [Hq, N, take] f32 (logits,
 // then exps, key-major), rowmax [Hq, take] u32, w [Hq, take] f32.
 size_t importance_workspace_bytes(int hq, int64_t n, int64_t block);
+// q_rows: rows per head in q (0 = n; `take` = only the last take rows were passed)
 int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, int64_t n, int d,
                       int64_t block, float scale, float* scores, void* ws, size_t ws_bytes,
-                      cudaStream_t st);
+                      cudaStream_t st, int64_t q_rows = 0);
 // per segment stable sort; primary_keys: 0 = descending f32 scores, 1 = ascending u32 groups
 int launch_segmented_sort(const void* keys, int key_kind, int heads, int64_t n, int64_t segment,
                           int32_t* perm, int32_t* inv, cudaStream_t st);
