@@ -43,7 +43,7 @@ def _compile(src, force, verbose):
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(srcp), _headers_mtime())):
         return obj, None
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", srcp, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("PBS_NVCC_EXTRA", "").split(), "-c", srcp, "-o", obj]
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

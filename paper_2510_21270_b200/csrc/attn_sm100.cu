@@ -201,6 +201,71 @@ __device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
       : "memory");
 }
 
+// QK^T of one tile, K = d = 128 as 8 MMAs from ONE elected lane, descriptors
+// advanced inside the asm block (start address field = byte address >> 4):
+// k-step k reads bytes (k & 3) * 32 + (k >> 2) * kPanelBytes past the bases.
+// One election and one register->uniform move per operand for the 8 MMAs
+// .
+__device__ __forceinline__ void tc_mma_qk8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, t, f;\n"
+      ".reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      "setp.ne.b32 t, 1, 0;\n"
+      "setp.ne.b32 f, 0, 0;\n"
+      "add.s64 a1, %1, 2;    add.s64 b1, %2, 2;\n"
+      "add.s64 a2, %1, 4;    add.s64 b2, %2, 4;\n"
+      "add.s64 a3, %1, 6;    add.s64 b3, %2, 6;\n"
+      "add.s64 a4, %1, 1024; add.s64 b4, %2, 1024;\n"
+      "add.s64 a5, %1, 1026; add.s64 b5, %2, 1026;\n"
+      "add.s64 a6, %1, 1028; add.s64 b6, %2, 1028;\n"
+      "add.s64 a7, %1, 1030; add.s64 b7, %2, 1030;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+
+// PV over 128 keys: 8 MMAs (K = 16 keys each) with A = P in TMEM (8 columns per
+// step) and B = V rows advancing 16 x 128 bytes (encoded +128) per step.
+__device__ __forceinline__ void tc_mma_pv8(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, t, p;\n"
+      ".reg .b32 a1, a2, a3, a4, a5, a6, a7;\n"
+      ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n"
+      "setp.ne.b32 t, 1, 0;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "add.s32 a1, %1, 8;   add.s64 b1, %2, 128;\n"
+      "add.s32 a2, %1, 16;  add.s64 b2, %2, 256;\n"
+      "add.s32 a3, %1, 24;  add.s64 b3, %2, 384;\n"
+      "add.s32 a4, %1, 32;  add.s64 b4, %2, 512;\n"
+      "add.s32 a5, %1, 40;  add.s64 b5, %2, 640;\n"
+      "add.s32 a6, %1, 48;  add.s64 b6, %2, 768;\n"
+      "add.s32 a7, %1, 56;  add.s64 b7, %2, 896;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // TMEM[128 lanes x 8 columns] <- 128 rows x 256 bits of a shared-memory matrix
 // (same descriptor format as the MMA operands; executes in order with tcgen05.mma)
 __device__ __forceinline__ void tc_cp_w(uint32_t d_tmem, uint64_t sdesc_) {
@@ -342,8 +407,14 @@ struct KernelArgs {
 
 // debug timeline (PBS_ATTN_TRACE=file): CTA 0 records clock64 at pipeline events
 constexpr int kTraceEvents = 4096;
+// Compiled in only with -DPBS_ATTN_TRACE_EVENTS (PBS_NVCC_EXTRA at build time):
+// the checks cost issue slots in the hot loops.
 __device__ __forceinline__ void trace_event(const KernelArgs& a, int kind, uint32_t n) {
+#ifdef PBS_ATTN_TRACE_EVENTS
   if (a.trace && blockIdx.x == 0 && n < kTraceEvents) a.trace[kind * kTraceEvents + n] = clock64();
+#else
+  (void)a, (void)kind, (void)n;
+#endif
 }
 
 struct Item {
@@ -655,12 +726,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
       tc_fence_after();
       const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
-#pragma unroll
-      for (int k = 0; k < kD / 16; ++k) {
-        const uint64_t ad = sdesc(q_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-        const uint64_t bd = sdesc(k_base + (k >> 2) * kPanelBytes + (k & 3) * 32, 16, 1024);
-        tc_mma_w(tmem + col_s(w), ad, bd, idesc_qk, k > 0 ? 1u : 0u);
-      }
+      static_assert(kD == 128 && kPanelBytes == 1024 * 16, "tc_mma_qk8 descriptor steps");
+      tc_mma_qk8(tmem + col_s(w), sdesc(q_base, 16, 1024), sdesc(k_base, 16, 1024), idesc_qk);
       tc_commit_w(&bar->s_full[w]);
       tc_commit_w(&bar->k_empty[stage]);
       if (e + 1 == len) tc_commit_w(&bar->q_empty);  // every QK of the item issued: Q is free once they complete
@@ -686,12 +753,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (e == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // the previous epilogue read O_0 and O_1
         tc_fence_after();
         const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
-          // A = P [128 q x 16 kv] in TMEM (8 columns over S_w); B = V [16 kv x 128 d] MN-major SW128
-          const uint64_t bd = sdesc(v_base + k * 16 * 128, kPanelBytes, 1024);
-          tc_mma_ts_w(tmem + col_o(w), tmem + col_s(w) + k * 8, bd, idesc_pv, (e < kGroups && k == 0) ? 0u : 1u);
-        }
+        // A = P [128 q x 128 kv] in TMEM (64 columns over S_w); B = V [128 kv x 128 d] MN-major SW128
+        static_assert(kBN == 128, "tc_mma_pv8 covers 128 keys");
+        tc_mma_pv8(tmem + col_o(w), tmem + col_s(w), sdesc(v_base, kPanelBytes, 1024), idesc_pv, e < kGroups ? 0u : 1u);
         tc_commit_w(&bar->v_empty[stage]);
         if (e + 1 == len) tc_commit_w(&bar->o_full);
         ++v_it;
