@@ -17,7 +17,10 @@
 //  * exp is the device port of glibc expf (expf_glibc.cuh).
 // None of this is tensor-core work: the estimate is CUDA-core fp32, and the
 // tensor cores are reserved for the attention kernel.
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstring>
 
 #include "common.cuh"
 #include "exact_gemm.cuh"
@@ -36,10 +39,15 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // K1a: L[h][j][i] = (q[r0+i] . k[j]) * scale and rowmax[h][i] = max_j L.
 // grid (ceil(N/128), ceil(take/128), Hq).  L is key-major ([j][i]) so that the
-// per-row denominator chains (K1bc) read 128-byte lines per step.
+// per-row denominator chains (K1c) read 128-byte lines per step.
 template <typename T, bool kExact, bool kVec>
 __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
     const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int64_t q_rows, int d, int take,
@@ -93,55 +101,110 @@ __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
   }
 }
 
-// K1bc: per row i, e_j = expf(L[j][i] - mx_i) (permutation.hpp:171) and
-// denom_i = sequential sum over j = 0..N-1 (line 172), then
-// w_i = 1 / (denom * take) (line 174).  One CTA per (head, 32 rows): warps
-// 1..kExpWarps compute the exps of 64-key tiles into a shared-memory ring;
-// warp 0 is the adder, one dependent chain of N fp32 adds per lane.
-constexpr int kExpWarps = 16;
-constexpr int kJT = 32;            // keys per ring tile
-constexpr int kRing = 2 * kExpWarps;
+// K1b: E[j][i] = expf(L[j][i] - mx_i) in place (permutation.hpp:171), every
+// element once, on the whole GPU (the sequential passes below only stream E).
+// CTA = kExpKeys keys of one head; the row maxima are decoded into smem.
+constexpr int kExpKeys = 128;
+__global__ void __launch_bounds__(256) importance_exp_kernel(float* __restrict__ L, const unsigned* __restrict__ rowmax,
+                                                             int take, int64_t n) {
+  __shared__ float mx[1024];
+  __shared__ uint64_t tab[32];
+  load_exp2f_table(tab);
+  const int h = blockIdx.y;
+  for (int i = threadIdx.x; i < take && i < 1024; i += blockDim.x) mx[i] = decode_order_key(rowmax[(int64_t)h * take + i]);
+  __syncthreads();
+  const int64_t j0 = (int64_t)blockIdx.x * kExpKeys;
+  const int64_t cnt = min64(kExpKeys, n - j0) * take;
+  float* base = L + ((int64_t)h * n + j0) * take;
+  if (take % 4 == 0 && take <= 1024) {
+    // four 16-byte loads in flight per thread before any exp
+    float4* b4 = reinterpret_cast<float4*>(base);
+    const int64_t n4 = cnt / 4;
+    for (int64_t e0 = threadIdx.x; e0 < n4; e0 += 4 * (int64_t)blockDim.x) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + (int64_t)u * blockDim.x;
+        if (e < n4) x[u] = b4[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + (int64_t)u * blockDim.x;
+        if (e >= n4) break;
+        const int i = (int)((e * 4) % take);
+        x[u].x = expf_glibc(__fsub_rn(x[u].x, mx[i]), tab);
+        x[u].y = expf_glibc(__fsub_rn(x[u].y, mx[i + 1]), tab);
+        x[u].z = expf_glibc(__fsub_rn(x[u].z, mx[i + 2]), tab);
+        x[u].w = expf_glibc(__fsub_rn(x[u].w, mx[i + 3]), tab);
+        b4[e] = x[u];
+      }
+    }
+  } else {
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int i = (int)(e % take);
+      const float m = i < 1024 ? mx[i] : decode_order_key(rowmax[(int64_t)h * take + i]);
+      base[e] = expf_glibc(__fsub_rn(base[e], m), tab);
+    }
+  }
+}
 
-__global__ void __launch_bounds__(32 * (1 + kExpWarps)) importance_expsum_kernel(
-    const float* __restrict__ L, const unsigned* __restrict__ rowmax, int take, int64_t n, float* __restrict__ w) {
-  extern __shared__ __align__(16) unsigned char dsm[];
+// K1c: denom_i = sequential fp32 sum of E[j][i] over j = 0..N-1 (line 172), then
+// w_i = 1 / (denom * take) (line 174).  One CTA per (head, 32 rows): warp 1
+// streams 128-key x 32-row tiles of E into a shared-memory ring, one 2-D TMA
+// copy per tile (the whole ring in flight), warp 0 is the adder, one dependent
+// chain of N adds per lane.  Shapes whose row groups are not whole 16-byte
+// pieces (take % 4 != 0 or a partial row group) take 4-byte cp.async copies.
+constexpr int kJT = 128;    // keys per ring tile (one barrier round trip per 128 adds)
+constexpr int kRing = 8;    // 8 tiles = 128 KB in flight
+
+__device__ __forceinline__ void tma_load_3d_f32(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(ptx::smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(64, 1) importance_denom_kernel(const __grid_constant__ CUtensorMap tm_e, bool tma,
+                                                              const float* __restrict__ E, int take, int64_t n,
+                                                              float* __restrict__ w) {
+  extern __shared__ __align__(128) unsigned char dsm[];
   float (*ring)[kJT][32] = reinterpret_cast<float (*)[kJT][32]>(dsm);
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm + sizeof(float) * kRing * kJT * 32);
   uint64_t* empty = full + kRing;
   const int h = blockIdx.y;
   const int i0 = blockIdx.x * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = i0 + lane;
-  const bool row_ok = i < take;
-  __shared__ uint64_t tab[32];
-  load_exp2f_table(tab);
+  const int rows = min(32, take - i0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], tma ? 1 : 32);
       ptx::mbar_init(&empty[s], 1);
     }
     ptx::fence_mbar_init();
   }
   __syncthreads();
   const int64_t ntiles = (n + kJT - 1) / kJT;
-  const float* Lh = L + (int64_t)h * n * take;
-  if (warp > 0) {
-    const float mx = row_ok ? decode_order_key(rowmax[(int64_t)h * take + i]) : 0.0f;
-    for (int64_t t = warp - 1; t < ntiles; t += kExpWarps) {
+  const float* Eh = E + (int64_t)h * n * take;
+  if (warp == 1) {
+    for (int64_t t = 0; t < ntiles; ++t) {
       const int slot = (int)(t % kRing);
       ptx::mbar_wait(&empty[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
       const int64_t jb = t * kJT;
       const int cnt = (int)min64(kJT, n - jb);
-      // the whole tile in flight (cp.async straight into the ring slot), then exps in place
-      for (int jj = 0; jj < cnt; ++jj) {
-        if (row_ok) cp_async4(&ring[slot][jj][lane], Lh + (jb + jj) * take + i);
-        else ring[slot][jj][lane] = 0.0f;
+      if (tma) {
+        // keys past N are zero-filled by the TMA unit; the box is always 4 KB
+        if (lane == 0) {
+          ptx::mbar_expect_tx(&full[slot], kJT * 32 * 4);
+          tma_load_3d_f32(&ring[slot][0][0], &tm_e, &full[slot], i0, (int)jb, h);
+        }
+      } else {
+        for (int jj = 0; jj < cnt; ++jj)
+          if (lane < rows) cp_async4(&ring[slot][jj][lane], Eh + (jb + jj) * take + i0 + lane);
+        cp_async_wait_all();
+        ptx::mbar_arrive(&full[slot]);
       }
-      cp_async_wait_all();
-#pragma unroll 8
-      for (int jj = 0; jj < cnt; ++jj) ring[slot][jj][lane] = expf_glibc(__fsub_rn(ring[slot][jj][lane], mx), tab);
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&full[slot]);
     }
   } else {
     float denom = 0.0f;
@@ -150,59 +213,83 @@ __global__ void __launch_bounds__(32 * (1 + kExpWarps)) importance_expsum_kernel
       ptx::mbar_wait(&full[slot], (uint32_t)((t / kRing) & 1));
       const int cnt = (int)min64(kJT, n - t * kJT);
       if (cnt == kJT) {
-#pragma unroll 16
-        for (int jj = 0; jj < kJT; ++jj) denom = __fadd_rn(denom, ring[slot][jj][lane]);
+        float v[kJT];
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) v[jj] = ring[slot][jj][lane];
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) denom = __fadd_rn(denom, v[jj]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[slot]);
       } else {
         for (int jj = 0; jj < cnt; ++jj) denom = __fadd_rn(denom, ring[slot][jj][lane]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[slot]);
       }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[slot]);
     }
-    if (row_ok) w[(int64_t)h * take + i] = __fdiv_rn(1.0f, __fmul_rn(denom, (float)take));
+    if (lane < rows) w[(int64_t)h * take + i0 + lane] = __fdiv_rn(1.0f, __fmul_rn(denom, (float)take));
   }
 }
 
-// K1d: s[j] = sum_i e_ij * w_i in order i = 0..take-1 (line 175), the product
-// rounded before the add; e_ij recomputed as expf(L - mx_i) (bit-identical to
-// K1bc's).  CTA = 128 keys; [128 x 32] tiles staged through smem.
-__global__ void __launch_bounds__(128) importance_scores_kernel(const float* __restrict__ L,
-                                                                const unsigned* __restrict__ rowmax,
+// K1d: s[j] = sum_i E[j][i] * w_i in order i = 0..take-1 (line 175), the product
+// rounded before the add.  CTA = 128 keys, one per thread; 32-row chunks of the
+// keys' E rows double-buffered through smem (16-byte cp.async, rows padded to 36
+// floats so each thread's 16-byte reads are bank-conflict free).
+constexpr int kSK = 128;
+constexpr int kSPad = 36;
+__global__ void __launch_bounds__(kSK) importance_scores_kernel(const float* __restrict__ E,
                                                                 const float* __restrict__ w, int take, int64_t n,
                                                                 float* __restrict__ scores) {
-  __shared__ float tile[128][33];
-  __shared__ float ws[32], ms[32];
-  __shared__ uint64_t tab[32];
-  load_exp2f_table(tab);
+  __shared__ __align__(16) float tile[2][kSK][kSPad];
+  __shared__ float ws[2][32];
   const int h = blockIdx.y;
-  const int64_t j0 = (int64_t)blockIdx.x * 128;
+  const int64_t j0 = (int64_t)blockIdx.x * kSK;
   const int tid = threadIdx.x;
-  const float* Lh = L + (int64_t)h * n * take;
-  float s = 0.0f;
-  for (int i0 = 0; i0 < take; i0 += 32) {
+  const int keys = (int)min64(kSK, n - j0);
+  const float* Eh = E + (int64_t)h * n * take;
+  const bool vec = (take % 4 == 0);
+  auto stage = [&](int buf, int i0) {
     const int ic = min(32, take - i0);
-    if (tid < 32) {
-      ws[tid] = tid < ic ? w[(int64_t)h * take + i0 + tid] : 0.0f;
-      ms[tid] = tid < ic ? decode_order_key(rowmax[(int64_t)h * take + i0 + tid]) : 0.0f;
-    }
-    __syncthreads();
-    {
-      const int c = tid & 31;
-      for (int u = 0; u < 32; ++u) {  // rows r = (tid >> 5) + 4u: the tile in flight, then the exps
-        const int r = (tid >> 5) + 4 * u;
-        if (c < ic && j0 + r < n) cp_async4(&tile[r][c], Lh + (j0 + r) * take + i0 + c);
+    if (tid < 32) ws[buf][tid] = tid < ic ? w[(int64_t)h * take + i0 + tid] : 0.0f;
+    if (vec) {
+      // ic is a multiple of 4 here: ic / 4 pieces per key
+      const int pk = ic >> 2;
+      for (int c = tid; c < keys * pk; c += kSK) {
+        const int r = c / pk, q = c - r * pk;
+        cp_async16(&tile[buf][r][4 * q], Eh + (j0 + r) * take + i0 + 4 * q);
       }
-      cp_async_wait_all();
-#pragma unroll 8
-      for (int u = 0; u < 32; ++u) {
-        const int r = (tid >> 5) + 4 * u;
-        tile[r][c] = (c < ic && j0 + r < n) ? expf_glibc(__fsub_rn(tile[r][c], ms[c]), tab) : 0.0f;
+    } else {
+      for (int c = tid; c < keys * ic; c += kSK) {
+        const int r = c / ic, q = c - r * ic;
+        cp_async4(&tile[buf][r][q], Eh + (j0 + r) * take + i0 + q);
       }
     }
+    cp_async_commit();
+  };
+  float s = 0.0f;
+  stage(0, 0);
+  int buf = 0;
+  for (int i0 = 0; i0 < take; i0 += 32, buf ^= 1) {
+    const bool more = i0 + 32 < take;
+    if (more) stage(buf ^ 1, i0 + 32);
+    if (more) cp_async_wait_group1();
+    else cp_async_wait_all();
     __syncthreads();
-    for (int c = 0; c < ic; ++c) s = __fadd_rn(s, __fmul_rn(tile[tid][c], ws[c]));
-    __syncthreads();
+    const int ic = min(32, take - i0);
+    if (ic == 32) {
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        const float4 e = *reinterpret_cast<const float4*>(&tile[buf][tid][c]);
+        s = __fadd_rn(s, __fmul_rn(e.x, ws[buf][c]));
+        s = __fadd_rn(s, __fmul_rn(e.y, ws[buf][c + 1]));
+        s = __fadd_rn(s, __fmul_rn(e.z, ws[buf][c + 2]));
+        s = __fadd_rn(s, __fmul_rn(e.w, ws[buf][c + 3]));
+      }
+    } else {
+      for (int c = 0; c < ic; ++c) s = __fadd_rn(s, __fmul_rn(tile[buf][tid][c], ws[buf][c]));
+    }
+    __syncthreads();  // buf is refilled two chunks later
   }
-  if (j0 + tid < n) scores[(int64_t)h * n + j0 + tid] = s;
+  if (tid < keys) scores[(int64_t)h * n + j0 + tid] = s;
 }
 
 // ---- K2: segmented sort ------------------------------------------------------
@@ -395,17 +482,25 @@ int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, 
     else importance_logits_kernel<float, false, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
   }
   PBS_LAUNCH_CHECK("importance_logits_kernel");
+  importance_exp_kernel<<<dim3((unsigned)ceil_div(n, kExpKeys), (unsigned)hq), 256, 0, st>>>(L, rowmax, take, n);
+  PBS_LAUNCH_CHECK("importance_exp_kernel");
   const size_t smem = sizeof(float) * kRing * kJT * 32 + 2 * kRing * sizeof(uint64_t);
   static bool attr = false;
   if (!attr) {
-    PBS_CUDA_CHECK(cudaFuncSetAttribute(importance_expsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PBS_CUDA_CHECK(cudaFuncSetAttribute(importance_denom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  importance_expsum_kernel<<<dim3((unsigned)ceil_div(take, 32), (unsigned)hq), 32 * (1 + kExpWarps), smem, st>>>(
-      L, rowmax, take, n, w);
-  PBS_LAUNCH_CHECK("importance_expsum_kernel");
-  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, 128), (unsigned)hq), 128, 0, st>>>(L, rowmax, w, take, n,
-                                                                                         scores);
+  alignas(64) CUtensorMap tm_e;
+  const bool tma = (take % 4 == 0) && (take % 32 == 0);  // every CTA's 32 rows are whole 16-byte pieces
+  if (tma) {
+    if (int rc = make_f32_map_3d(&tm_e, L, take, n, hq, 32, kJT)) return rc;
+  } else {
+    memset(&tm_e, 0, sizeof(tm_e));
+  }
+  importance_denom_kernel<<<dim3((unsigned)ceil_div(take, 32), (unsigned)hq), 64, smem, st>>>(tm_e, tma, L, take, n,
+                                                                                              w);
+  PBS_LAUNCH_CHECK("importance_denom_kernel");
+  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, kSK), (unsigned)hq), kSK, 0, st>>>(L, w, take, n, scores);
   PBS_LAUNCH_CHECK("importance_scores_kernel");
   return PBS_OK;
 }

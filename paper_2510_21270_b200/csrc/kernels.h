@@ -24,6 +24,8 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
                         int d, int64_t block, uint32_t* groups, void* ws, size_t ws_bytes,
                         cudaStream_t st);
 int launch_identity(int32_t* perm, int heads, int64_t n, cudaStream_t st);
+// TMA map (a CUtensorMap, 64 bytes) over fp32 [d2][d1][d0] with a [1][box1][box0] box (attn_sm100.cu)
+int make_f32_map_3d(void* map, const float* base, int64_t d0, int64_t d1, int64_t d2, int box0, int box1);
 
 // ---- stage 2 (gather.cu) ------------------------------------------------------
 int launch_apply_rows(const int32_t* perm, const void* src, int src_heads, int dst_heads,

@@ -79,6 +79,8 @@ def test_device_expf_matches_host_expf(ops):
     (2, 2, 300, 16, 16, "f32"),
     (1, 1, 50, 32, 64, "bf16"),   # N < B: all queries
     (1, 1, 4096, 128, 64, "f32"),  # config 1 (B=64)
+    (2, 1, 1000, 64, 40, "bf16"),  # take % 32 != 0: cp.async denominators, 8-row chunk
+    (1, 1, 700, 128, 96, "bf16"),  # three TMA row groups, ragged last key tile
 ])
 def test_importance_and_key_permutation_bitexact(ops, oracle, hq, hkv, n, d, b, dtype):
     rng = np.random.default_rng(n + d)
