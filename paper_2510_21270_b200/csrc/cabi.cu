@@ -634,6 +634,7 @@ struct Arena {
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   cudaEvent_t ev_rep[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_k;  // per KV head: its keys are on the device (estimate-first path)
   // per slot: stage timers and pinned copies of the report counters, so a
   // group's report is built while the next group computes
   Timer* timer[2] = {nullptr, nullptr};
@@ -742,17 +743,30 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     float* scores = reinterpret_cast<float*>(take_b((size_t)hq * n * 4));
     pi_all = reinterpret_cast<int32_t*>(take_b((size_t)hq * n * 4));
     int32_t* pi_inv = reinterpret_cast<int32_t*>(take_b((size_t)hq * n * 4));
-    // K of every KV head and the last `take` rows of every query head first
-    PBS_CUDA_CHECK(cudaMemcpyAsync(k_all, hk_, kall_b, cudaMemcpyHostToDevice, s_in));
+    // the last `take` rows of every query head, then K one KV head at a time:
+    // each head's logits start as soon as its keys have landed, so the copy of
+    // K overlaps the estimate's GEMM
+    while (A.ev_k.size() < (size_t)hkv) {
+      cudaEvent_t e;
+      PBS_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      A.ev_k.push_back(e);
+    }
     PBS_CUDA_CHECK(cudaMemcpy2DAsync(q_tail, (size_t)take * d * es, hq_ + (size_t)(n - take) * d * es,
                                      (size_t)n * d * es, (size_t)take * d * es, (size_t)hq, cudaMemcpyHostToDevice,
                                      s_in));
-    PBS_CUDA_CHECK(cudaEventRecord(A.ev_rep[1], s_in));  // (reused: nothing else records it yet)
-    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_rep[1], 0));
-    est_tm.mark();
-    if (int rc = launch_importance(q_tail, k_all, shape->dtype, (int)hq, (int)hkv, n, (int)d, cfg->block_size,
-                                   effective_scale(cfg->scale, (int)d), scores, imp, imp_b, s_run, take))
-      return rc;
+    for (int64_t c = 0; c < hkv; ++c) {
+      PBS_CUDA_CHECK(cudaMemcpyAsync(k_all + (size_t)c * kvb, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
+      PBS_CUDA_CHECK(cudaEventRecord(A.ev_k[c], s_in));
+    }
+    const float sc = effective_scale(cfg->scale, (int)d);
+    for (int64_t c = 0; c < hkv; ++c) {
+      PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_k[c], 0));
+      if (c == 0) est_tm.mark();
+      if (int rc = launch_importance_logits(q_tail, k_all, shape->dtype, (int)hq, (int)hkv, (int)(c * g), (int)g, n,
+                                            (int)d, cfg->block_size, sc, imp, imp_b, s_run, take))
+        return rc;
+    }
+    if (int rc = launch_importance_finish((int)hq, n, cfg->block_size, scores, imp, imp_b, s_run)) return rc;
     if (int rc = launch_segmented_sort(scores, 0, (int)hq, n, cfg->segment_size, pi_all, pi_inv, s_run)) return rc;
     est_tm.mark();
   }

@@ -51,9 +51,9 @@ __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.
 template <typename T, bool kExact, bool kVec>
 __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
     const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int64_t q_rows, int d, int take,
-    float scale, float* __restrict__ L, unsigned* __restrict__ rowmax) {
+    float scale, float* __restrict__ L, unsigned* __restrict__ rowmax, int h0) {
   __shared__ __align__(16) xgemm::Smem sm;
-  const int h = blockIdx.z;
+  const int h = h0 + blockIdx.z;
   const int64_t j0 = (int64_t)blockIdx.x * kTile;
   const int i0 = blockIdx.y * kTile;
   // q holds q_rows rows per head (N, or just the last `take` rows), the
@@ -455,34 +455,59 @@ size_t importance_workspace_bytes(int hq, int64_t n, int64_t block) {
   return (size_t)hq * n * take * 4 + (size_t)hq * take * 8 + 256;
 }
 
-int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, int64_t n, int d,
-                      int64_t block, float scale, float* scores, void* ws, size_t ws_bytes,
-                      cudaStream_t st, int64_t q_rows) {
+namespace {
+struct ImpWs {
+  float* L;
+  unsigned* rowmax;
+  float* w;
+};
+ImpWs imp_ws(void* ws, int hq, int64_t n, int take) {
+  ImpWs r;
+  r.L = static_cast<float*>(ws);
+  r.rowmax = reinterpret_cast<unsigned*>(r.L + (size_t)hq * n * take);
+  r.w = reinterpret_cast<float*>(r.rowmax + (size_t)hq * take);
+  return r;
+}
+}  // namespace
+
+int launch_importance_logits(const void* q, const void* k, int dtype, int hq, int hkv, int h0, int nh, int64_t n,
+                             int d, int64_t block, float scale, void* ws, size_t ws_bytes, cudaStream_t st,
+                             int64_t q_rows) {
   const int take = (int)min64(block, n);
   if (q_rows <= 0) q_rows = n;
   if (q_rows < take) return fail(PBS_ERR_CONFIG, "E_SHAPE", "importance: q holds fewer rows than the estimate reads");
   if (ws_bytes < importance_workspace_bytes(hq, n, block))
     return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "importance workspace too small");
-  float* L = static_cast<float*>(ws);
-  unsigned* rowmax = reinterpret_cast<unsigned*>(L + (size_t)hq * n * take);
-  float* w = reinterpret_cast<float*>(rowmax + (size_t)hq * take);
-  PBS_CUDA_CHECK(cudaMemsetAsync(rowmax, 0, sizeof(unsigned) * hq * take, st));
+  if (h0 < 0 || nh < 0 || h0 + nh > hq) return fail(PBS_ERR_CONFIG, "E_SHAPE", "importance: head range");
+  if (nh == 0) return PBS_OK;
+  const ImpWs W = imp_ws(ws, hq, n, take);
+  PBS_CUDA_CHECK(cudaMemsetAsync(W.rowmax + (size_t)h0 * take, 0, sizeof(unsigned) * nh * take, st));
   const int group = hq / hkv;
   const bool vec = (d % 16 == 0) && ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0);
-  dim3 grid((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(take, kTile), (unsigned)hq);
+  dim3 grid((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(take, kTile), (unsigned)nh);
   if (dtype == PBS_DTYPE_BF16) {
     auto qq = static_cast<const __nv_bfloat16*>(q);
     auto kk = static_cast<const __nv_bfloat16*>(k);
-    if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
-    else importance_logits_kernel<__nv_bfloat16, true, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
+    if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
+    else importance_logits_kernel<__nv_bfloat16, true, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
   } else {
     auto qq = static_cast<const float*>(q);
     auto kk = static_cast<const float*>(k);
-    if (vec) importance_logits_kernel<float, false, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
-    else importance_logits_kernel<float, false, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, L, rowmax);
+    if (vec) importance_logits_kernel<float, false, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
+    else importance_logits_kernel<float, false, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
   }
   PBS_LAUNCH_CHECK("importance_logits_kernel");
-  importance_exp_kernel<<<dim3((unsigned)ceil_div(n, kExpKeys), (unsigned)hq), 256, 0, st>>>(L, rowmax, take, n);
+  return PBS_OK;
+}
+
+int launch_importance_finish(int hq, int64_t n, int64_t block, float* scores, void* ws, size_t ws_bytes,
+                             cudaStream_t st) {
+  const int take = (int)min64(block, n);
+  if (ws_bytes < importance_workspace_bytes(hq, n, block))
+    return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "importance workspace too small");
+  const ImpWs W = imp_ws(ws, hq, n, take);
+  float* L = W.L;
+  importance_exp_kernel<<<dim3((unsigned)ceil_div(n, kExpKeys), (unsigned)hq), 256, 0, st>>>(L, W.rowmax, take, n);
   PBS_LAUNCH_CHECK("importance_exp_kernel");
   const size_t smem = sizeof(float) * kRing * kJT * 32 + 2 * kRing * sizeof(uint64_t);
   static bool attr = false;
@@ -498,11 +523,19 @@ int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, 
     memset(&tm_e, 0, sizeof(tm_e));
   }
   importance_denom_kernel<<<dim3((unsigned)ceil_div(take, 32), (unsigned)hq), 64, smem, st>>>(tm_e, tma, L, take, n,
-                                                                                              w);
+                                                                                              W.w);
   PBS_LAUNCH_CHECK("importance_denom_kernel");
-  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, kSK), (unsigned)hq), kSK, 0, st>>>(L, w, take, n, scores);
+  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, kSK), (unsigned)hq), kSK, 0, st>>>(L, W.w, take, n, scores);
   PBS_LAUNCH_CHECK("importance_scores_kernel");
   return PBS_OK;
+}
+
+int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, int64_t n, int d,
+                      int64_t block, float scale, float* scores, void* ws, size_t ws_bytes,
+                      cudaStream_t st, int64_t q_rows) {
+  if (int rc = launch_importance_logits(q, k, dtype, hq, hkv, 0, hq, n, d, block, scale, ws, ws_bytes, st, q_rows))
+    return rc;
+  return launch_importance_finish(hq, n, block, scores, ws, ws_bytes, st);
 }
 
 int launch_identity(int32_t* perm, int heads, int64_t n, cudaStream_t st) {
