@@ -184,14 +184,19 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     mx = block_max(mx, red);
     for (int64_t j = tid; j < a; j += blockDim.x) sv[j] = expf_glibc(__fsub_rn(sv[j], mx), tab);
     __syncthreads();
-    if (warp == 0) {
+    if (tid == 0) {
+      // one thread, values straight from smem (loads run ahead of the add chain)
       float denom = 0.0f;
-      for (int64_t j0 = 0; j0 < a; j0 += 32) {
-        const float val = (j0 + lane < a) ? sv[j0 + lane] : 0.0f;
-        const int cnt = (int)min64(32, a - j0);
-        for (int kk = 0; kk < cnt; ++kk) denom = __fadd_rn(denom, __shfl_sync(0xffffffffu, val, kk));
+      int64_t j = 0;
+      for (; j + 8 <= a; j += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = sv[j + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) denom = __fadd_rn(denom, v[u]);
       }
-      if (lane == 0) s_denom = denom;
+      for (; j < a; ++j) denom = __fadd_rn(denom, sv[j]);
+      s_denom = denom;
     }
     __syncthreads();
     const float denom = s_denom;
@@ -230,23 +235,28 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
       else __syncthreads();
     }
   __syncthreads();
-  if (warp == 0) {
+  if (tid == 0) {
+    // one thread: the sorted values are fetched 8 ahead of the double chain
     double cum = 0.0;
     int take = (int)a;  // fallback: every admissible block (line 188)
-    bool done = false;
-    for (int64_t k0 = 0; k0 < a && !done; k0 += 32) {
-      const double val = (k0 + lane < a) ? (double)sv[keys[k0 + lane] & 0xffffffffu] : 0.0;
-      const int cnt = (int)min64(32, a - k0);
-      for (int kk = 0; kk < cnt; ++kk) {
-        cum += __shfl_sync(0xffffffffu, val, kk);
+    for (int64_t k0 = 0; k0 < a; k0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = (k0 + u < a) ? sv[keys[k0 + u] & 0xffffffffu] : 0.0f;
+      bool done = false;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k0 + u >= a) break;
+        cum += (double)v[u];
         if (cum >= tau) {
-          take = (int)(k0 + kk + 1);
+          take = (int)(k0 + u + 1);
           done = true;
           break;
         }
       }
+      if (done) break;
     }
-    if (lane == 0) s_take = take;
+    s_take = take;
   }
   __syncthreads();
   const int take = s_take;
