@@ -140,5 +140,82 @@ __device__ __forceinline__ void tile(const TA* __restrict__ a_base, int a_rows, 
   }
 }
 
+// bf16 operands with d % 32 == 0: the same per-output order, d staged in
+// chunks of 32 (half the CTA barriers of tile()), the next chunk held in
+// registers as raw bf16 (8 x 32-bit per operand per thread) and widened to f32
+// on its way into shared memory.  Needs sizeof(SmemWide) of dynamic smem.
+constexpr int kChunkW = 32;
+struct SmemWide {
+  float a[2][kChunkW][kTile + kPad];
+  float b[2][kChunkW][kTile + kPad];
+};
+
+__device__ __forceinline__ void load16_bf16(const __nv_bfloat16* __restrict__ base, int rows, int d, int row, int c,
+                                            uint4 (&v)[2]) {
+  if (row >= rows) {
+    v[0] = make_uint4(0u, 0u, 0u, 0u);
+    v[1] = v[0];
+    return;
+  }
+  const uint4* p = reinterpret_cast<const uint4*>(base + (int64_t)row * d + c);
+  v[0] = __ldg(p);
+  v[1] = __ldg(p + 1);
+}
+
+__device__ __forceinline__ void store16_widened(float (*dst)[kTile + kPad], int col0, int row, const uint4 (&v)[2]) {
+  const uint32_t w[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    dst[col0 + 2 * u][row] = __uint_as_float(w[u] << 16);             // bf16 -> f32 is exact
+    dst[col0 + 2 * u + 1][row] = __uint_as_float(w[u] & 0xffff0000u);
+  }
+}
+
+__device__ __forceinline__ void tile_bf16_wide(const __nv_bfloat16* __restrict__ a_base, int a_rows,
+                                               const __nv_bfloat16* __restrict__ b_base, int b_rows, int d,
+                                               float (&acc)[8][8], SmemWide& sm) {
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int lrow = tid >> 1;
+  const int lcol = (tid & 1) * 16;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+  const int nchunks = d / kChunkW;
+  uint4 ra[2], rb[2];
+  load16_bf16(a_base, a_rows, d, lrow, lcol, ra);
+  load16_bf16(b_base, b_rows, d, lrow, lcol, rb);
+  store16_widened(sm.a[0], lcol, lrow, ra);
+  store16_widened(sm.b[0], lcol, lrow, rb);
+  __syncthreads();
+  for (int kc = 0; kc < nchunks; ++kc) {
+    const int buf = kc & 1;
+    const bool more = kc + 1 < nchunks;
+    if (more) {
+      load16_bf16(a_base, a_rows, d, lrow, (kc + 1) * kChunkW + lcol, ra);
+      load16_bf16(b_base, b_rows, d, lrow, (kc + 1) * kChunkW + lcol, rb);
+    }
+#pragma unroll 4
+    for (int cc = 0; cc < kChunkW; ++cc) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&sm.a[buf][cc][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&sm.a[buf][cc][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&sm.b[buf][cc][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&sm.b[buf][cc][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) acc2<true>(acc[i][j], acc[i][j + 1], a[i], b[j], b[j + 1]);
+    }
+    if (more) {
+      store16_widened(sm.a[buf ^ 1], lcol, lrow, ra);
+      store16_widened(sm.b[buf ^ 1], lcol, lrow, rb);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace xgemm
 }  // namespace pbs_b200

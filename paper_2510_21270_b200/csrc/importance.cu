@@ -48,11 +48,11 @@ __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.
 // K1a: L[h][j][i] = (q[r0+i] . k[j]) * scale and rowmax[h][i] = max_j L.
 // grid (ceil(N/128), ceil(take/128), Hq).  L is key-major ([j][i]) so that the
 // per-row denominator chains (K1c) read 128-byte lines per step.
-template <typename T, bool kExact, bool kVec>
+// kWide (bf16, d % 32 == 0): xgemm::tile_bf16_wide with dynamic shared memory.
+template <typename T, bool kExact, bool kVec, bool kWide = false>
 __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
     const T* __restrict__ q, const T* __restrict__ k, int group, int64_t n, int64_t q_rows, int d, int take,
     float scale, float* __restrict__ L, unsigned* __restrict__ rowmax, int h0) {
-  __shared__ __align__(16) xgemm::Smem sm;
   const int h = h0 + blockIdx.z;
   const int64_t j0 = (int64_t)blockIdx.x * kTile;
   const int i0 = blockIdx.y * kTile;
@@ -64,7 +64,13 @@ __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
   const int a_rows = min(kTile, take - i0);
   const int b_rows = (int)min64(kTile, n - j0);
   float acc[8][8];
-  xgemm::tile<T, T, kExact, kVec>(a_base, a_rows, b_base, b_rows, d, acc, sm);
+  if constexpr (kWide) {
+    extern __shared__ __align__(16) unsigned char sm_dyn[];
+    xgemm::tile_bf16_wide(a_base, a_rows, b_base, b_rows, d, acc, *reinterpret_cast<xgemm::SmemWide*>(sm_dyn));
+  } else {
+    __shared__ __align__(16) xgemm::Smem sm;
+    xgemm::tile<T, T, kExact, kVec>(a_base, a_rows, b_base, b_rows, d, acc, sm);
+  }
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   float* Lh = L + (int64_t)h * n * take;
   float rmax[8];
@@ -488,7 +494,17 @@ int launch_importance_logits(const void* q, const void* k, int dtype, int hq, in
   if (dtype == PBS_DTYPE_BF16) {
     auto qq = static_cast<const __nv_bfloat16*>(q);
     auto kk = static_cast<const __nv_bfloat16*>(k);
-    if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
+    if (vec && d % xgemm::kChunkW == 0) {
+      auto kern = importance_logits_kernel<__nv_bfloat16, true, true, true>;
+      static bool attr = false;
+      if (!attr) {
+        PBS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)sizeof(xgemm::SmemWide)));
+        attr = true;
+      }
+      kern<<<grid, xgemm::kThreads, sizeof(xgemm::SmemWide), st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L,
+                                                                   W.rowmax, h0);
+    } else if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
     else importance_logits_kernel<__nv_bfloat16, true, false><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
   } else {
     auto qq = static_cast<const float*>(q);
