@@ -188,9 +188,10 @@ def cpu_reference_sample(n_s, threads, seed=99):
     if ref is None:  # reference never built on this machine: time the C restatement instead
         ref = oracle.Oracle("oracle")
         kind = "port"
-    hkv = max(1, min(HKV, -(-threads // (HQ // HKV))))
-    q, k, v = make_inputs(torch, n_s, 0, min(HQ, hkv * (HQ // HKV)), list(range(hkv)), "cpu", seed)
-    q = q[:threads].float().numpy()
+    # whole GQA groups only (the reference maps query head h to KV head h / group)
+    hkv = max(1, min(HKV, threads // (HQ // HKV)))
+    q, k, v = make_inputs(torch, n_s, 0, hkv * (HQ // HKV), list(range(hkv)), "cpu", seed)
+    q = q.float().numpy()
     k = k.float().numpy()
     v = v.float().numpy()
     cfg = oracle.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy="key_permute")

@@ -294,6 +294,10 @@ PBSREF_DEFS(double, f64)
 int pbsref_pbs_attention_heads_f32(const float* q, const float* k, const float* v, int hq, int hkv,
                                    size_t n, size_t d, const pbs_pipeline_config* cfg, float* out,
                                    int threads, pbs_report* rep_sum) {
+  if (hkv <= 0 || hq <= 0 || hq % hkv != 0) {
+    g_err = "E_SHAPE: query heads must be a whole number of GQA groups";
+    return PBS_ERR_CONFIG;
+  }
   const int g = hq / hkv;
   std::vector<pbs_report> reps(hq);
   std::vector<int> rcs(hq, 0);
