@@ -112,7 +112,10 @@ def test_key_permutation_ties_kat(ops):
 
 
 @pytest.mark.parametrize("n,d,b,s,tau", [(2048, 128, 128, 256, 0.9), (1000, 64, 32, 64, 0.5),
-                                         (640, 32, 64, 0, 0.7)])
+                                         (640, 32, 64, 0, 0.7),
+                                         # register sorts: 2, 8 and 16 keys per thread (T = 256 / 1024 / 2048)
+                                         (4096, 32, 16, 64, 0.9), (8192, 16, 8, 32, 0.9),
+                                         (16384, 16, 8, 64, 0.95)])
 def test_block_scores_and_selection_bitexact(ops, oracle, n, d, b, s, tau):
     rng = np.random.default_rng(7)
     tq, tk, tv, q, k, v = bf16_inputs(rng, 2, 1, n, d, kind="vertical_lines")
