@@ -227,6 +227,29 @@ PBS_API int pbs_attention_coverage(const void* q, const void* k, const pbs_shape
                                    const uint8_t* mask, const int32_t* sigma, const int32_t* pi, double scale,
                                    double* coverage, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- PBST tensor files (tensor_io.hpp) ------------------------------------ */
+/* Header of a PBST file: read_tensor's checks (tensor_io.hpp:98-146), same
+ * E_IO / E_FORMAT texts and byte offsets. */
+typedef struct pbs_tensor_info {
+  int32_t file_dtype;     /* Dtype (tensor_io.hpp:31): 0 = f32, 1 = f64 */
+  int32_t ndim;           /* 2 (rows, cols) or 3 (heads, rows, cols) */
+  int64_t heads;          /* 1 for a 2-D file */
+  int64_t rows;
+  int64_t cols;
+  int64_t payload_offset; /* bytes */
+} pbs_tensor_info;
+PBS_API int pbs_tensor_info_read(const char* path, pbs_tensor_info* info);
+/* read_tensor (tensor_io.hpp:98-146) into device memory: dst holds
+ * heads x rows x cols elements of dst_dtype (f32, or bf16 rounded to nearest).
+ * A non-finite payload element fails with E_FORMAT at its byte offset
+ * (tensor_io.hpp:80-81).  Synchronous with respect to `stream`. */
+PBS_API int pbs_tensor_load(const char* path, void* dst, int32_t dst_dtype, void* stream);
+/* write_tensor / write_tensor_stack (tensor_io.hpp:155-193) from device
+ * memory: src [heads, rows, cols] of src_dtype, file_dtype 0 = f32 / 1 = f64,
+ * as_stack = 0 writes a 2-D file (heads must be 1). */
+PBS_API int pbs_tensor_save(const char* path, const void* src, int32_t src_dtype, int64_t heads, int64_t rows,
+                            int64_t cols, int32_t file_dtype, int32_t as_stack, void* stream);
+
 /* ---- test hooks ---------------------------------------------------------- */
 /* y[i] = the device port of glibc expf (the reference's std::exp(float)). */
 PBS_API int pbs_debug_expf(const float* x, float* y, int64_t n, void* stream);

@@ -265,6 +265,32 @@ class Oracle:
             C.byref(rep)))
         return PipelineResult(out, sigma, pi, mask, rep.as_dict())
 
+    # ---- PBST files through the reference's tensor_io.hpp (reference only)
+    def write_tensor(self, path, a, as_stack=None):
+        """write_tensor / write_tensor_stack (tensor_io.hpp:155-193)."""
+        assert self.kind == "ref"
+        a = np.ascontiguousarray(a)
+        heads, rows, cols = (a.shape if a.ndim == 3 else (1, *a.shape))
+        stack = (a.ndim == 3) if as_stack is None else bool(as_stack)
+        fn = self.lib[f"pbsref_write_tensor_{_SFX[a.dtype.type]}"]
+        fn.argtypes = [C.c_char_p, C.c_void_p, _SZ, _SZ, _SZ, C.c_int]
+        self._check(fn(str(path).encode(), a.ctypes.data, heads, rows, cols, int(stack)))
+
+    def read_tensor(self, path):
+        """read_tensor (tensor_io.hpp:98-146): (values as float64 [heads, rows, cols]
+        or [rows, cols], file dtype code, ndim); errors raise with the E_* text."""
+        assert self.kind == "ref"
+        fn = self.lib["pbsref_read_tensor"]
+        fn.argtypes = [C.c_char_p, C.c_void_p, _SZ, C.c_void_p, C.c_void_p, C.c_void_p]
+        dims = np.zeros(3, dtype=np.int64)
+        fdt, nd = C.c_int(0), C.c_int(0)
+        self._check(fn(str(path).encode(), None, 0, dims.ctypes.data, C.addressof(fdt), C.addressof(nd)))
+        out = np.zeros(int(np.prod(dims)), dtype=np.float64)
+        self._check(fn(str(path).encode(), out.ctypes.data, out.size, dims.ctypes.data, C.addressof(fdt),
+                       C.addressof(nd)))
+        shape = tuple(int(x) for x in dims) if nd.value == 3 else (int(dims[1]), int(dims[2]))
+        return out.reshape(shape), fdt.value, nd.value
+
     # ---- multi-head CPU run (reference only; pbs_main.cpp:99-122)
     def pbs_attention_heads(self, q, k, v, cfg: PipelineConfig, threads: int):
         assert self.kind == "ref"

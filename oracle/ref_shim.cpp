@@ -21,6 +21,7 @@
 #include "pbs/errors.hpp"
 #include "pbs/permutation.hpp"
 #include "pbs/pipeline.hpp"
+#include "pbs/tensor_io.hpp"
 #include "pbs/workload.hpp"
 
 namespace {
@@ -379,5 +380,47 @@ int pbsref_pbs_attention_heads_f32(const float* q, const float* k, const float* 
   }
 PBSREF_GEN(float, f32)
 PBSREF_GEN(double, f64)
+
+// PBST files through the reference's own tensor_io.hpp: write_tensor(_stack)
+// of `heads` row-major [rows, cols] matrices, and read_tensor into a caller
+// buffer (dims[3] = heads, rows, cols; *file_dtype 0 f32 / 1 f64; values
+// widened to double).  Errors return the reference's code and E_* text.
+#define PBSREF_TIO(T, SFX)                                                                         \
+  int pbsref_write_tensor_##SFX(const char* path, const T* data, size_t heads, size_t rows,        \
+                                size_t cols, int as_stack) {                                       \
+    try {                                                                                          \
+      std::vector<pbs::Matrix<T>> hs;                                                              \
+      for (size_t h = 0; h < heads; ++h) hs.push_back(to_mat(data + h * rows * cols, rows, cols)); \
+      pbs::write_tensor<T>(path, std::span<const pbs::Matrix<T>>(hs.data(), hs.size()),           \
+                           as_stack != 0);                                                         \
+      return 0;                                                                                    \
+    } catch (const pbs::Error& e) { return fail(e); } catch (const std::exception& e) {            \
+      return fail_other(e);                                                                        \
+    }                                                                                              \
+  }
+PBSREF_TIO(float, f32)
+PBSREF_TIO(double, f64)
+
+int pbsref_read_tensor(const char* path, double* out, size_t capacity, int64_t* dims, int* file_dtype,
+                       int* ndim) {
+  try {
+    const pbs::LoadedTensor t = pbs::read_tensor(path);
+    *file_dtype = static_cast<int>(t.dtype);
+    *ndim = t.is_stack ? 3 : 2;
+    auto emit = [&](const auto& heads) {
+      dims[0] = static_cast<int64_t>(heads.size());
+      dims[1] = heads.empty() ? 0 : static_cast<int64_t>(heads[0].rows());
+      dims[2] = heads.empty() ? 0 : static_cast<int64_t>(heads[0].cols());
+      size_t o = 0;
+      for (const auto& m : heads)
+        for (size_t i = 0; i < m.size() && o < capacity; ++i) out[o++] = static_cast<double>(m.data()[i]);
+    };
+    if (t.dtype == pbs::Dtype::f32) emit(t.as<float>());
+    else emit(t.as<double>());
+    return 0;
+  } catch (const pbs::Error& e) { return fail(e); } catch (const std::exception& e) {
+    return fail_other(e);
+  }
+}
 
 }  // extern "C"

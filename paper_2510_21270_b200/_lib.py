@@ -30,7 +30,8 @@ EXPORTS = [
     "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_apply_rows",
     "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_block_sparse_attention_fwd",
     "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
-    "pbs_coverage_workspace_size", "pbs_attention_coverage", "pbs_debug_expf",
+    "pbs_coverage_workspace_size", "pbs_attention_coverage", "pbs_tensor_info_read", "pbs_tensor_load",
+    "pbs_tensor_save", "pbs_debug_expf",
 ]
 
 
@@ -62,6 +63,16 @@ class Report(C.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class TensorInfo(C.Structure):
+    """pbs_tensor_info: a PBST header (tensor_io.hpp:23-29)."""
+
+    _fields_ = [("file_dtype", C.c_int32), ("ndim", C.c_int32), ("heads", C.c_int64), ("rows", C.c_int64),
+                ("cols", C.c_int64), ("payload_offset", C.c_int64)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 class PbsError(RuntimeError):
     """Raised for any non-zero status; `code` mirrors pbs::ErrorCode (errors.hpp:11-16)."""
 
@@ -82,11 +93,15 @@ class DegenerateRowError(PbsError):
     pass
 
 
+class IoError(PbsError):
+    """E_IO / E_FORMAT (errors.hpp:42-59)."""
+
+
 class CudaError(PbsError):
     pass
 
 
-_ERRORS = {PBS_ERR_CONFIG: ConfigError, PBS_ERR_RESOURCE: ResourceError,
+_ERRORS = {PBS_ERR_CONFIG: ConfigError, PBS_ERR_RESOURCE: ResourceError, PBS_ERR_IO: IoError,
            PBS_ERR_DEGENERATE: DegenerateRowError, PBS_ERR_CUDA: CudaError}
 
 _lib = None
@@ -118,6 +133,9 @@ _SIGS = {
                                      C.POINTER(Report)]),
     "pbs_coverage_workspace_size": (SZ, [C.POINTER(Shape), I64]),
     "pbs_attention_coverage": (C.c_int, [VP, VP, C.POINTER(Shape), I64, VP, VP, VP, DBL, VP, VP, SZ, VP]),
+    "pbs_tensor_info_read": (C.c_int, [C.c_char_p, C.POINTER(TensorInfo)]),
+    "pbs_tensor_load": (C.c_int, [C.c_char_p, VP, I32, VP]),
+    "pbs_tensor_save": (C.c_int, [C.c_char_p, VP, I32, I64, I64, I64, I32, I32, VP]),
     "pbs_debug_expf": (C.c_int, [VP, VP, I64, VP]),
 }
 

@@ -18,6 +18,7 @@ and stream plumbing here.
     pbs_attention             pipeline.hpp:107-193
     attention_coverage        pipeline.hpp:198-243
     density_sweep             pipeline.hpp:245-295
+    tensor_info / load_tensor / save_tensor   tensor_io.hpp (PBST files)
 """
 from __future__ import annotations
 
@@ -313,6 +314,40 @@ def density_sweep(q, k, v, base: PipelineConfig, taus, segment_sizes):
                                  time_us=r["estimate_us"] + r["permute_us"] + r["select_us"] + r["attention_us"]
                                  + r["unpermute_us"]))
     return rows
+
+
+def tensor_info(path) -> dict:
+    """The header of a PBST file (read_tensor's checks, tensor_io.hpp:98-146):
+    file_dtype (0 f32 / 1 f64), ndim, heads, rows, cols, payload_offset."""
+    info = _lib.TensorInfo()
+    check(lib().pbs_tensor_info_read(str(path).encode(), C.byref(info)))
+    return info.as_dict()
+
+
+def load_tensor(path, dtype=torch.bfloat16, device=None) -> torch.Tensor:
+    """read_tensor (tensor_io.hpp:98-146) straight into device memory: a 3-D
+    file gives [heads, rows, cols], a 2-D file [rows, cols], as bf16 (rounded
+    to nearest) or f32.  Non-finite payload elements raise E_FORMAT with their
+    byte offset (tensor_io.hpp:80-81)."""
+    info = tensor_info(path)
+    shape = (info["heads"], info["rows"], info["cols"]) if info["ndim"] == 3 else (info["rows"], info["cols"])
+    out = torch.empty(shape, dtype=dtype, device=device or torch.device("cuda", torch.cuda.current_device()))
+    check(lib().pbs_tensor_load(str(path).encode(), _ptr(out), _dtype_code(out), _stream()))
+    return out
+
+
+def save_tensor(path, t: torch.Tensor, file_dtype="f32", as_stack=None):
+    """write_tensor / write_tensor_stack (tensor_io.hpp:155-193) from a device
+    tensor ([heads, rows, cols] or [rows, cols], bf16 or f32).  as_stack
+    defaults to the tensor's rank (3-D -> stack)."""
+    _check_dev(t)
+    if t.dim() not in (2, 3):
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: write_tensor takes a 2-D matrix or a 3-D stack")
+    heads, rows, cols = (t.shape if t.dim() == 3 else (1, *t.shape))
+    stack = (t.dim() == 3) if as_stack is None else bool(as_stack)
+    code = {"f32": 0, "f64": 1}[file_dtype]
+    check(lib().pbs_tensor_save(str(path).encode(), _ptr(t), _dtype_code(t), heads, rows, cols, code, int(stack),
+                                _stream()))
 
 
 def debug_expf(x: torch.Tensor) -> torch.Tensor:
