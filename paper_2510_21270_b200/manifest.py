@@ -2,6 +2,7 @@
 pbs_main.cpp `run`) on the device path.
 
     python -m paper_2510_21270_b200.manifest run --manifest run.json
+    python -m paper_2510_21270_b200.manifest sweep --manifest run.json --tau-list 0.5,0.9 --out s.csv
 
 A manifest names PBST input stacks (q, k, v), the PipelineConfig and where
 the output tensor and the report go (manifest.hpp:17-39).  Keys, defaults and
@@ -201,15 +202,66 @@ def run_manifest(m: RunManifest, base_dir=".") -> dict:
     return doc
 
 
+def format_sweep_csv(rows) -> str:
+    """format_sweep_csv (pbs_main.cpp:236-247)."""
+    out = ["tau,S,strategy,density,coverage,max_err,mean_err,time_us\n"]
+    for r in rows:
+        out.append("%.6g,%d,%s,%.6f,%.6f,%.9g,%.9g,%.1f\n" % (r.tau, r.segment_size, r.strategy, r.density,
+                                                             r.coverage, r.max_err, r.mean_err, r.time_us))
+    return "".join(out)
+
+
+def sweep_manifest(m: RunManifest, base_dir=".", taus=(), segments=(), strategies=(), out_path="") -> str:
+    """The CLI's `sweep` (pbs_main.cpp:248-267): density_sweep of head 0 for every
+    strategy (sorted, unique), defaults from the manifest's pipeline."""
+    import torch
+
+    from . import ops
+
+    def resolve(p):
+        return p if os.path.isabs(p) else os.path.join(base_dir, p)
+
+    q, k, v = (ops.load_tensor(resolve(x), dtype=torch.bfloat16) for x in (m.q, m.k, m.v))
+    q, k, v = (x[:1] if x.dim() == 3 else x.unsqueeze(0) for x in (q, k, v))
+    taus = list(taus) or [m.tau]
+    segments = list(segments) or [m.segment_size]
+    rows = []
+    for name in sorted(set(strategies or [m.strategy])):
+        if name not in _STRATEGIES:
+            raise _config_error(f"unknown permutation strategy '{name}'")
+        cfg = m.config()
+        cfg.strategy = _lib.STRATEGIES[name]
+        rows += ops.density_sweep(q, k, v, cfg, taus, segments)
+    text = format_sweep_csv(rows)
+    if out_path:
+        with open(out_path, "w") as f:
+            f.write(text)
+    else:
+        sys.stdout.write(text)
+    return text
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2510_21270_b200.manifest")
     sub = ap.add_subparsers(dest="cmd", required=True)
     r = sub.add_parser("run", help="Run the pipeline per head and write reports")
     r.add_argument("--manifest", required=True)
+    sw = sub.add_parser("sweep", help="Density/coverage/error sweep as CSV")
+    sw.add_argument("--manifest", required=True)
+    sw.add_argument("--tau-list", default="")
+    sw.add_argument("--segment-list", default="")
+    sw.add_argument("--strategies", default="")
+    sw.add_argument("--out", default="")
     args = ap.parse_args(argv)
     try:
         m = load_manifest(args.manifest)
-        run_manifest(m, os.path.dirname(os.path.abspath(args.manifest)))
+        base = os.path.dirname(os.path.abspath(args.manifest))
+        if args.cmd == "run":
+            run_manifest(m, base)
+        else:
+            split = lambda s: [x for x in s.split(",") if x]  # noqa: E731
+            sweep_manifest(m, base, [float(x) for x in split(args.tau_list)],
+                           [int(x) for x in split(args.segment_list)], split(args.strategies), args.out)
     except _lib.PbsError as e:  # the CLI's stderr line and exit code (pbs_main.cpp:467-480)
         sys.stderr.write(str(e) + "\n")
         return e.code

@@ -245,3 +245,33 @@ def test_manifest_run_matches_reference(ops, ref, tmp_path):
     assert agg["selected_blocks"] == sel and agg["total_admissible_blocks"] == adm
     assert set(agg) == {"block_density", "causal_density_baseline", "attention_coverage", "selected_blocks",
                         "total_admissible_blocks", "timings_us"}
+
+
+@gpu
+def test_manifest_sweep_csv(ops, ref, tmp_path):
+    import torch
+
+    import oracle as orc
+    from paper_2510_21270_b200 import manifest
+    rng = np.random.default_rng(12)
+    n, d = 1024, 64
+    qkv = [torch.from_numpy(rng.standard_normal((1, n, d))).to(torch.bfloat16).double().numpy() for _ in range(3)]
+    qkv[1][:, ::61] += 5.0
+    for name, x in zip("qkv", qkv):
+        ref.write_tensor(tmp_path / f"{name}.pbst", x)
+    m = manifest.load_manifest(_manifest(tmp_path, GOOD))
+    text = manifest.sweep_manifest(m, str(tmp_path), taus=[0.9, 0.5], segments=[128],
+                                   strategies=["none", "key_permute", "none"], out_path=str(tmp_path / "s.csv"))
+    assert (tmp_path / "s.csv").read_text() == text
+    lines = text.splitlines()
+    assert lines[0] == "tau,S,strategy,density,coverage,max_err,mean_err,time_us"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert [(r[0], r[1], r[2]) for r in rows] == [("0.5", "128", "key_permute"), ("0.9", "128", "key_permute"),
+                                                  ("0.5", "128", "none"), ("0.9", "128", "none")]
+    o = Oracle("oracle")
+    for r in rows:
+        cfg = orc.make_config(block_size=64, segment_size=128, tau=float(r[0]), strategy=r[2])
+        want = o.pbs_attention(*(x[0].astype(np.float32) for x in qkv), cfg).report["block_density"]
+        assert r[3] == "%.6f" % want
+        # coverage in (0, 1]; errors against dense causal attention (large at low tau)
+        assert 0.0 < float(r[4]) <= 1.0 and float(r[5]) >= float(r[6]) >= 0.0
