@@ -232,15 +232,25 @@ def test_degenerate_row_raises(ops):
     assert "query block 1" in str(e.value)
 
 
-def test_host_entry_matches_device_entry(ops):
+# hkv = 1: one group; key_permute with hkv > 1: the estimate of every head runs
+# up front (K streamed per KV head) and the groups take pi; query_permute with
+# hkv > 1: per-group pipelines on two slots
+@pytest.mark.parametrize("hq,hkv,n,strategy", [(2, 1, 1024, "key_permute"), (8, 4, 2048 + 128, "key_permute"),
+                                               (6, 3, 1024, "query_permute")])
+def test_host_entry_matches_device_entry(ops, hq, hkv, n, strategy):
     rng = np.random.default_rng(9)
-    tq, tk, tv, *_ = bf16_inputs(rng, 2, 1, 1024, 128, kind="vertical_lines")
-    cfg = ops.make_config()
+    tq, tk, tv, *_ = bf16_inputs(rng, hq, hkv, n, 128, kind="vertical_lines")
+    cfg = ops.make_config(strategy=strategy)
     dev = ops.pbs_attention(tq, tk, tv, cfg)
     host = ops.pbs_attention_host(tq.cpu(), tk.cpu(), tv.cpu(), cfg, return_perms=True)
     assert torch.equal(host.output, dev.output.cpu())
     assert torch.equal(host.pi, dev.pi.cpu())
+    assert torch.equal(host.sigma, dev.sigma.cpu())
     assert torch.equal(host.mask, dev.mask.cpu())
+    for key in ("selected_blocks", "total_admissible_blocks"):
+        assert host.report[key] == dev.report[key]
+    for key in ("block_density", "causal_density_baseline", "pooled_score_coverage"):
+        assert abs(host.report[key] - dev.report[key]) < 1e-12
 
 
 def test_cpp_dropin_runs(ops, tmp_path):
