@@ -1,6 +1,6 @@
 """Quick standalone probe of the tcgen05 attention kernel (run under `timeout`).
 
-python tests/gpu_probe_sm100.py   -> prints max errors vs SDPA and vs the SIMT path
+python scripts/gpu_probe_sm100.py   -> prints max errors vs SDPA and vs the SIMT path
 """
 import os
 import sys
