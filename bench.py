@@ -48,6 +48,7 @@ MODELS = {"llama": (32, 8, 131072, "llama31_8b_attn"),   # configs[1], configs[2
 HQ, HKV, N, D = 32, 8, 131072, 128   # the selected model (set from --model)
 PREFIX = "llama31_8b_attn"
 BLOCK, SEGMENT, TAU = 128, 256, 0.9
+STRATEGY = "key_permute"
 LINE_PERIOD, LINE_SEGS, LINES, STRENGTH = 3, 2, 16, 30.0
 
 
@@ -62,9 +63,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seq", type=int, default=8192, help="sequence length of the CPU reference sample")
+    ap.add_argument("--strategy", choices=["key_permute", "query_permute", "both", "none"], default="key_permute",
+                    help="permutation strategy (the paper's operating point is key_permute)")
     args = ap.parse_args()
-    global HQ, HKV, N, PREFIX
+    global HQ, HKV, N, PREFIX, STRATEGY
     HQ, HKV, N, PREFIX = MODELS[args.model]
+    STRATEGY = args.strategy
     if args.seq is None:
         args.seq = N
     return args
@@ -194,7 +198,7 @@ def cpu_reference_sample(n_s, threads, seed=99):
     q = q.float().numpy()
     k = k.float().numpy()
     v = v.float().numpy()
-    cfg = oracle.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy="key_permute")
+    cfg = oracle.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy=STRATEGY)
     t0 = time.perf_counter()
     if kind == "reference":
         _, rep = ref.pbs_attention_heads(q, k, v, cfg, threads)
@@ -239,7 +243,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{PREFIX}_{args.seq // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
                    "seq_len": args.seq, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
-                   "strategy": "key_permute", "parallelism": "cpu threads"},
+                   "strategy": STRATEGY, "parallelism": "cpu threads"},
         "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "sample_density": rep["block_density"] if rep else None,
@@ -270,7 +274,7 @@ def main():
     q, k, v = make_inputs(torch, n, q0, q1, kv_list, "cuda")
     max_local = max(shard_of(r, world)[1] - shard_of(r, world)[0] for r in range(world))
     torch.cuda.synchronize()
-    cfg = ops.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy="key_permute")
+    cfg = ops.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy=STRATEGY)
     ws = ops.workspace(ops.workspace_size(q, k, cfg))
     # ranks with fewer heads pad their share of the gather (Qwen on 8 GPUs: 3 or 4)
     out_pad = torch.zeros(max_local, n, D, dtype=torch.bfloat16, device="cuda")
@@ -397,7 +401,7 @@ def main():
             "data": "synthetic (vertical-lines Q/K/V, seeded; selection by the real tau=0.9 algorithm)",
             "config": {"workload": f"{PREFIX}_{n // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
                        "seq_len": n, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
-                       "strategy": "key_permute", "parallelism": f"heads{world}",
+                       "strategy": STRATEGY, "parallelism": f"heads{world}",
                        "l2": "inputs (1.5 GiB) > L2 (126 MB); no flush"},
             "speedup_vs_dense_fa": dense_ms / ms,
             "dense_fa_ms": dense_ms,

@@ -8,8 +8,8 @@
 // result is bit-identical to the scalar loop:
 //   kExact = true  : fmaf (valid when every product is exact in fp32, e.g.
 //                    bf16 x bf16 with |product| >= 2^-126)
-//   kExact = false : __fmul_rn then __fadd_rn (the reference's un-contracted
-//                    x86-64 code for arbitrary fp32 operands)
+//   kExact = false : rounded product then add (the reference's un-contracted
+//                    x86-64 code for arbitrary fp32 operands), packed f32x2
 #pragma once
 
 #include "common.cuh"
@@ -40,19 +40,26 @@ __device__ __forceinline__ uint64_t pk2(float x, float y) {
 __device__ __forceinline__ void upk2(uint64_t r, float& x, float& y) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
 }
+// {-0.0f, -0.0f}.  Kept in constant memory so that ptxas cannot see the value:
+// ptxas contracts mul.rn.f32x2 + add.rn.f32x2 (and an fma with a literal -0
+// addend + add) into one FFMA2, which would skip the product's rounding.
+static __constant__ uint64_t kNegZero2 = 0x8000000080000000ull;
+
 template <bool kExact>
 __device__ __forceinline__ void acc2(float& c0, float& c1, float a, float b0, float b1) {
+  uint64_t rc = pk2(c0, c1);
+  const uint64_t ra = pk2(a, a), rb = pk2(b0, b1);
   if (kExact) {
-    uint64_t rc = pk2(c0, c1);
-    const uint64_t ra = pk2(a, a), rb = pk2(b0, b1);
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rc) : "l"(ra), "l"(rb));
-    upk2(rc, c0, c1);
   } else {
-    // scalar: ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2, which
-    // would change the rounding of non-exact products
-    c0 = __fadd_rn(c0, __fmul_rn(a, b0));
-    c1 = __fadd_rn(c1, __fmul_rn(a, b1));
+    // product rounded on its own (fma with a -0 addend == mul, bit for bit,
+    // signed zeros included), then the add: the reference's un-contracted
+    // mul-then-add, two outputs per instruction
+    uint64_t rp;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rp) : "l"(ra), "l"(rb), "l"(kNegZero2));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(rc) : "l"(rp));
   }
+  upk2(rc, c0, c1);
 }
 
 // load 8 consecutive elements [c, c+8) of row `row` (zero beyond rows/d)

@@ -380,15 +380,31 @@ __global__ void centroid_kernel(const T* __restrict__ k, int64_t n, int d, int64
   }
 }
 
+// |q_i| = sqrt(sum_c q_ic^2), sequential c (permutation.hpp:238-243).  One
+// thread per row; rows are read 16 bytes at a time when d and the base allow
+// (a row per lane: scalar 2-byte loads made every warp load touch 32 lines).
 template <typename T>
 __global__ void qnorm_kernel(const T* __restrict__ q, int64_t rows, int d, float* __restrict__ qn) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= rows) return;
   const T* p = q + g * d;
   float s = 0.0f;
-  for (int c = 0; c < d; ++c) {
-    const float x = to_f32(p[c]);
-    s = __fadd_rn(s, __fmul_rn(x, x));
+  constexpr int kPer = 16 / (int)sizeof(T);
+  if (d % kPer == 0 && (uintptr_t)q % 16 == 0) {
+    for (int c = 0; c < d; c += kPer) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p + c));
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const float x = to_f32(e[u]);
+        s = __fadd_rn(s, __fmul_rn(x, x));
+      }
+    }
+  } else {
+    for (int c = 0; c < d; ++c) {
+      const float x = to_f32(p[c]);
+      s = __fadd_rn(s, __fmul_rn(x, x));
+    }
   }
   qn[g] = __fsqrt_rn(s);
 }
