@@ -203,7 +203,7 @@ __device__ __forceinline__ void tile_bf16_wide(const __nv_bfloat16* __restrict__
       load16_bf16(a_base, a_rows, d, lrow, (kc + 1) * kChunkW + lcol, ra);
       load16_bf16(b_base, b_rows, d, lrow, (kc + 1) * kChunkW + lcol, rb);
     }
-#pragma unroll 4
+#pragma unroll 8
     for (int cc = 0; cc < kChunkW; ++cc) {
       const float4 a0 = *reinterpret_cast<const float4*>(&sm.a[buf][cc][ty * 4]);
       const float4 a1 = *reinterpret_cast<const float4*>(&sm.a[buf][cc][64 + ty * 4]);
