@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--seq", type=int, default=None, help="sequence length (default: the model's config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense causal FA comparator (launch lists)")
     ap.add_argument("--cpu-seq", type=int, default=8192, help="sequence length of the CPU reference sample")
     ap.add_argument("--strategy", choices=["key_permute", "query_permute", "both", "none"], default="key_permute",
                     help="permutation strategy (the paper's operating point is key_permute)")
@@ -346,21 +347,23 @@ def main():
                "timing": "host wall clock around the synchronous C-ABI call (pinned host buffers)"}
 
     # dense causal FlashAttention comparator (same kernel family, full causal grid)
-    dout = torch.empty_like(q)
-    for _ in range(args.warmup):
-        ops.dense_causal_attention(q, k, v, out=dout)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        ops.dense_causal_attention(q, k, v, out=dout)
-    e1.record(stream)
-    barrier()
-    dense_ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([dense_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dense_ms = t.item()
+    dense_ms = None
+    if not args.no_dense:
+        dout = torch.empty_like(q)
+        for _ in range(args.warmup):
+            ops.dense_causal_attention(q, k, v, out=dout)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ops.dense_causal_attention(q, k, v, out=dout)
+        e1.record(stream)
+        barrier()
+        dense_ms = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            t = torch.tensor([dense_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dense_ms = t.item()
 
     # FLOP accounting: executed = 4 B^2 d per selected block pair (band
     # tiles in full); dense-causal = 4 d N(N+1)/2 per head
@@ -403,7 +406,7 @@ def main():
                        "seq_len": n, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
                        "strategy": STRATEGY, "parallelism": f"heads{world}",
                        "l2": "inputs (1.5 GiB) > L2 (126 MB); no flush"},
-            "speedup_vs_dense_fa": dense_ms / ms,
+            "speedup_vs_dense_fa": (dense_ms / ms) if dense_ms else None,
             "dense_fa_ms": dense_ms,
             "effective_tflops": dense_flops / (ms * 1e-3) / 1e12,
             "executed_tflops_attention": achieved,
@@ -414,7 +417,7 @@ def main():
                          "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic, "peak_source": peak_src,
                          "algorithmic": "4*B^2*d FLOP per selected (query block, key block) pair"},
-            "dense_roofline_frac": (dense_flops / world / (dense_ms * 1e-3) / 1e12) / peak,
+            "dense_roofline_frac": ((dense_flops / world / (dense_ms * 1e-3) / 1e12) / peak) if dense_ms else None,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 if [ -z "$NO_NCU" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_bench.log 2>&1
+  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-dense > gpurun_out/ncu_launch_bench.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-attn_sm100} -s ${NCU_SKIP:-1} -c 1 \
   -o gpurun_out/prof -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 fi
