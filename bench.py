@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--cpu-seq", type=int, default=8192, help="sequence length of the CPU reference sample")
     ap.add_argument("--strategy", choices=["key_permute", "query_permute", "both", "none"], default="key_permute",
                     help="permutation strategy (the paper's operating point is key_permute)")
+    ap.add_argument("--top-k", type=int, default=0,
+                    help="select the top-k blocks per row instead of the tau threshold (extension)")
     args = ap.parse_args()
     global HQ, HKV, N, PREFIX, STRATEGY
     HQ, HKV, N, PREFIX = MODELS[args.model]
@@ -275,7 +277,7 @@ def main():
     q, k, v = make_inputs(torch, n, q0, q1, kv_list, "cuda")
     max_local = max(shard_of(r, world)[1] - shard_of(r, world)[0] for r in range(world))
     torch.cuda.synchronize()
-    cfg = ops.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy=STRATEGY)
+    cfg = ops.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy=STRATEGY, top_k=args.top_k)
     ws = ops.workspace(ops.workspace_size(q, k, cfg))
     # ranks with fewer heads pad their share of the gather (Qwen on 8 GPUs: 3 or 4)
     out_pad = torch.zeros(max_local, n, D, dtype=torch.bfloat16, device="cuda")
@@ -404,7 +406,7 @@ def main():
             "data": "synthetic (vertical-lines Q/K/V, seeded; selection by the real tau=0.9 algorithm)",
             "config": {"workload": f"{PREFIX}_{n // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
                        "seq_len": n, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
-                       "strategy": STRATEGY, "parallelism": f"heads{world}",
+                       "strategy": STRATEGY, "top_k": args.top_k or None, "parallelism": f"heads{world}",
                        "l2": "inputs (1.5 GiB) > L2 (126 MB); no flush"},
             "speedup_vs_dense_fa": (dense_ms / ms) if dense_ms else None,
             "dense_fa_ms": dense_ms,

@@ -69,7 +69,8 @@ typedef struct pbs_pipeline_config {
   int32_t strategy;     /* enum pbs_strategy */
   int32_t forced_first_block;
   int32_t forced_diagonal_band;
-  int32_t reserved;
+  int32_t top_k;        /* 0: cumulative threshold tau (the reference); > 0: keep the top_k admissible
+                           blocks per row by pooled score (extension: no reference oracle) */
   double scale; /* 0 => 1/sqrt(d) (attention.hpp:32-34) */
 } pbs_pipeline_config;
 
@@ -160,6 +161,13 @@ PBS_API int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_
  * kv_idx [H, T, T] (row-padded CSR), kv_cnt [H, T]. */
 PBS_API int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks,
                       int64_t block_size, int64_t segment_size, double tau,
+                      int32_t forced_first_block, int32_t forced_diagonal_band,
+                      uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, void* stream);
+/* Top-k selection (extension, the reference selects by threshold only): per row
+ * the top_k admissible blocks in the same stable descending order (ties by
+ * ascending index), plus the forced blocks. */
+PBS_API int pbs_select_blocks_top_k(const float* scores, int32_t num_heads, int64_t num_blocks,
+                      int64_t block_size, int64_t segment_size, int32_t top_k,
                       int32_t forced_first_block, int32_t forced_diagonal_band,
                       uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, void* stream);
 

@@ -42,7 +42,7 @@ class PipelineConfig(C.Structure):
         ("strategy", C.c_int32),
         ("forced_first_block", C.c_int32),
         ("forced_diagonal_band", C.c_int32),
-        ("reserved", C.c_int32),
+        ("top_k", C.c_int32),
         ("scale", C.c_double),
     ]
 
@@ -68,11 +68,11 @@ class Report(C.Structure):
 
 
 def make_config(block_size=128, segment_size=256, tau=0.9, strategy="key_permute",
-                forced_first_block=True, forced_diagonal_band=True, scale=0.0) -> PipelineConfig:
+                forced_first_block=True, forced_diagonal_band=True, scale=0.0, top_k=0) -> PipelineConfig:
     if isinstance(strategy, str):
         strategy = STRATEGIES[strategy]
     return PipelineConfig(block_size, segment_size, tau, strategy, int(forced_first_block),
-                          int(forced_diagonal_band), 0, scale)
+                          int(forced_diagonal_band), int(top_k), scale)
 
 
 class OracleError(RuntimeError):
@@ -188,11 +188,19 @@ class Oracle:
 
     # ---- a8 select_blocks (block_selection.hpp:171-206)
     def select_blocks(self, scores, causal, block_size, segment_size, tau,
-                      forced_first_block=True, forced_diagonal_band=True):
+                      forced_first_block=True, forced_diagonal_band=True, top_k=0):
+        """top_k > 0: the top-k extension (the C restatement only; the reference has none)."""
         dt = scores.dtype.type
         scores, causal = self._arr(scores, dt), self._arr(causal, dt)
         t_r, t_c = scores.shape
         mask = np.zeros((t_r, t_c), dtype=np.uint8)
+        if top_k:
+            assert self.kind == "oracle", "the reference has no top-k selection"
+            self._check(self._fn("select_blocks_top_k", dt)(
+                _p(scores, _F[dt]), _p(causal, _F[dt]), _SZ(t_r), _SZ(t_c), _SZ(block_size),
+                _SZ(segment_size), _SZ(top_k), int(forced_first_block), int(forced_diagonal_band),
+                _p(mask, C.c_uint8)))
+            return mask
         self._check(self._fn("select_blocks", dt)(
             _p(scores, _F[dt]), _p(causal, _F[dt]), _SZ(t_r), _SZ(t_c), _SZ(block_size),
             _SZ(segment_size), C.c_double(tau), int(forced_first_block), int(forced_diagonal_band),

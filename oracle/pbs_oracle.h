@@ -49,6 +49,9 @@ extern "C" {
   int pbso_select_blocks_##SFX(const REAL* scores, const REAL* causal, size_t t_r,             \
                                size_t t_c, size_t block, size_t segment, double tau,           \
                                int forced_first, int forced_band, uint8_t* mask);              \
+  int pbso_select_blocks_top_k_##SFX(const REAL* scores, const REAL* causal, size_t t_r,       \
+                                     size_t t_c, size_t block, size_t segment, size_t top_k,   \
+                                     int forced_first, int forced_band, uint8_t* mask);        \
   int pbso_attention_block_sparse_##SFX(const REAL* q, size_t n, const REAL* k,                \
                                         const REAL* v, size_t m, size_t d, size_t dv,          \
                                         size_t block, double scale, int causal,                \

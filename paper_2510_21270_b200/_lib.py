@@ -28,7 +28,7 @@ STRATEGIES = {"none": 0, "key_permute": 1, "query_permute": 2, "both": 3}
 EXPORTS = [
     "pbs_last_error", "pbs_version", "pbs_kernel_launches", "pbs_workspace_size", "pbs_estimate_key_importance",
     "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_apply_rows",
-    "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_block_sparse_attention_fwd",
+    "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_select_blocks_top_k", "pbs_block_sparse_attention_fwd",
     "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
     "pbs_coverage_workspace_size", "pbs_attention_coverage", "pbs_tensor_info_read", "pbs_tensor_load",
     "pbs_tensor_save", "pbs_debug_expf",
@@ -47,7 +47,7 @@ class PipelineConfig(C.Structure):
 
     _fields_ = [("block_size", C.c_int64), ("segment_size", C.c_int64), ("tau", C.c_double),
                 ("strategy", C.c_int32), ("forced_first_block", C.c_int32),
-                ("forced_diagonal_band", C.c_int32), ("reserved", C.c_int32), ("scale", C.c_double)]
+                ("forced_diagonal_band", C.c_int32), ("top_k", C.c_int32), ("scale", C.c_double)]
 
 
 class Report(C.Structure):
@@ -123,6 +123,7 @@ _SIGS = {
     "pbs_apply_rows": (C.c_int, [VP, VP, I32, I32, I64, I32, I32, VP, VP]),
     "pbs_meanpool_block_scores": (C.c_int, [VP, VP, C.POINTER(Shape), I64, I64, DBL, VP, VP, SZ, VP]),
     "pbs_select_blocks": (C.c_int, [VP, I32, I64, I64, I64, DBL, I32, I32, VP, VP, VP, VP]),
+    "pbs_select_blocks_top_k": (C.c_int, [VP, I32, I64, I64, I64, I32, I32, I32, VP, VP, VP, VP]),
     "pbs_block_sparse_attention_fwd": (C.c_int, [VP, VP, VP, I32, C.POINTER(Shape), I64, DBL, VP, VP, VP, VP,
                                                  VP, VP, VP, VP]),
     "pbs_dense_causal_attention_fwd": (C.c_int, [VP, VP, VP, C.POINTER(Shape), DBL, VP, VP]),

@@ -73,6 +73,7 @@ int check_cfg(const pbs_pipeline_config* c) {
   if (c->segment_size == 0 && c->strategy != PBS_STRATEGY_NONE)
     return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size 0 requires strategy none");
   if (c->scale < 0.0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "scale must be > 0");
+  if (c->top_k < 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "top_k must be >= 0 (0 selects by tau)");
   return PBS_OK;
 }
 
@@ -252,6 +253,18 @@ int pbs_select_blocks(const float* scores, int32_t num_heads, int64_t num_blocks
     return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size must be 0 or a multiple of the block size");
   return launch_select_from_scores(scores, num_heads, num_blocks, block_size, segment_size, tau, forced_first_block,
                                    forced_diagonal_band, mask, kv_idx, kv_cnt, as_stream(stream));
+}
+
+int pbs_select_blocks_top_k(const float* scores, int32_t num_heads, int64_t num_blocks, int64_t block_size,
+                            int64_t segment_size, int32_t top_k, int32_t forced_first_block,
+                            int32_t forced_diagonal_band, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
+                            void* stream) {
+  if (top_k < 1) return fail(PBS_ERR_CONFIG, "E_CONFIG", "top_k must be >= 1");
+  if (block_size <= 0) return fail(PBS_ERR_CONFIG, "E_CONFIG", "block size must be >= 1");
+  if (segment_size != 0 && (segment_size < block_size || segment_size % block_size != 0))
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "segment size must be 0 or a multiple of the block size");
+  return launch_select_from_scores(scores, num_heads, num_blocks, block_size, segment_size, 1.0, forced_first_block,
+                                   forced_diagonal_band, mask, kv_idx, kv_cnt, as_stream(stream), top_k);
 }
 
 int pbs_block_sparse_attention_fwd(const void* qp, const void* kp, const void* vp, int32_t kv_heads,
@@ -516,7 +529,7 @@ int pipeline_enqueue(const void* q, const void* k, const void* v, const pbs_shap
   if (int rc = launch_pool(kp, dt, kv_heads, hq, nullptr, n, d, b, kbar, st)) return rc;
   if (int rc = launch_score_select(qbar, kbar, static_cast<float*>(at(L.blog)), hq, t, d, b, s, scale, cfg->tau,
                                    cfg->forced_first_block, cfg->forced_diagonal_band, 1, nullptr, mask, kv_idx,
-                                   kv_cnt, row_cov, st))
+                                   kv_cnt, row_cov, st, cfg->top_k))
     return rc;
   tm.mark();
   // ---- stage 4: attention with the original-position element mask (173-176)

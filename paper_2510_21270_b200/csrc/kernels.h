@@ -49,7 +49,7 @@ int launch_pool(const void* x, int dtype, int src_heads, int dst_heads, const in
 int launch_score_select(const float* qbar, const float* kbar, float* logits_ws, int hq, int64_t t, int d,
                         int64_t block, int64_t segment, float scale, double tau, int forced_first, int forced_band,
                         int select, float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
-                        double* row_cov, cudaStream_t st);
+                        double* row_cov, cudaStream_t st, int top_k = 0);
 // mask -> per-row ascending key-block lists (the attention's CSR)
 int launch_mask_to_lists(const uint8_t* mask, int hq, int64_t t, int32_t* kv_idx, int32_t* kv_cnt, cudaStream_t st);
 // coverage[h] = mean over rows of exp(lse_sparse - lse_dense) (attention_coverage)
@@ -58,7 +58,7 @@ int launch_coverage_reduce(const float* lse_sparse, const float* lse_dense, int 
 // selection from precomputed scores (pbs_select_blocks)
 int launch_select_from_scores(const float* scores, int hq, int64_t t, int64_t block,
                               int64_t segment, double tau, int forced_first, int forced_band,
-                              uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, cudaStream_t st);
+                              uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, cudaStream_t st, int top_k = 0);
 
 // ---- stage 4 (attn_simt.cu / attn_sm100.cu) -----------------------------------
 struct AttnParams {

@@ -158,7 +158,7 @@ __device__ __forceinline__ float block_max(float v, float* red) {
 // in warp 0 as a broadcast chain: every lane pulls element k with a shuffle
 // and performs the identical add, so the order is exactly the reference's.
 __global__ void __launch_bounds__(kSelThreads) select_kernel(
-    int mode, const float* __restrict__ rows_in, int64_t t, int64_t block, int64_t segment, double tau,
+    int mode, const float* __restrict__ rows_in, int64_t t, int64_t block, int64_t segment, double tau, int top_k,
     int forced_first, int forced_band, int select, float* __restrict__ scores_out, uint8_t* __restrict__ mask,
     int32_t* __restrict__ kv_idx, int32_t* __restrict__ kv_cnt, double* __restrict__ row_cov) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
       else __syncthreads();
     }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && top_k > 0) {
+    s_take = (int)min64(top_k, a);  // top-k extension: the first k of the same order
+  } else if (tid == 0) {
     // one thread: the sorted values are fetched 8 ahead of the double chain
     double cum = 0.0;
     int take = (int)a;  // fallback: every admissible block (line 188)
@@ -348,7 +350,7 @@ int launch_pool(const void* x, int dtype, int src_heads, int dst_heads, const in
 }
 
 static int launch_select_common(int mode, const float* rows_in, int hq, int64_t t, int64_t block,
-                                int64_t segment, double tau, int forced_first, int forced_band, int select,
+                                int64_t segment, double tau, int top_k, int forced_first, int forced_band, int select,
                                 float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt, double* row_cov,
                                 cudaStream_t st) {
   if (t == 0 || hq == 0) return PBS_OK;
@@ -360,8 +362,8 @@ static int launch_select_common(int mode, const float* rows_in, int hq, int64_t 
     attr_set = true;
   }
   select_kernel<<<dim3((unsigned)t, (unsigned)hq), kSelThreads, smem, st>>>(
-      mode, rows_in, t, block, segment, tau, forced_first, forced_band, select, scores_out, mask, kv_idx, kv_cnt,
-      row_cov);
+      mode, rows_in, t, block, segment, tau, top_k, forced_first, forced_band, select, scores_out, mask, kv_idx,
+      kv_cnt, row_cov);
   PBS_LAUNCH_CHECK("select_kernel");
   return PBS_OK;
 }
@@ -369,19 +371,19 @@ static int launch_select_common(int mode, const float* rows_in, int hq, int64_t 
 int launch_score_select(const float* qbar, const float* kbar, float* logits_ws, int hq, int64_t t, int d,
                         int64_t block, int64_t segment, float scale, double tau, int forced_first, int forced_band,
                         int select, float* scores_out, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
-                        double* row_cov, cudaStream_t st) {
+                        double* row_cov, cudaStream_t st, int top_k) {
   if (t == 0 || hq == 0) return PBS_OK;
   const dim3 grid((unsigned)ceil_div(t, xgemm::kTile), (unsigned)ceil_div(t, xgemm::kTile), (unsigned)hq);
   block_logits_kernel<<<grid, xgemm::kThreads, 0, st>>>(qbar, kbar, t, d, block, segment, scale, logits_ws);
   PBS_LAUNCH_CHECK("block_logits_kernel");
-  return launch_select_common(0, logits_ws, hq, t, block, segment, tau, forced_first, forced_band, select,
+  return launch_select_common(0, logits_ws, hq, t, block, segment, tau, top_k, forced_first, forced_band, select,
                               scores_out, mask, kv_idx, kv_cnt, row_cov, st);
 }
 
 int launch_select_from_scores(const float* scores, int hq, int64_t t, int64_t block, int64_t segment, double tau,
                               int forced_first, int forced_band, uint8_t* mask, int32_t* kv_idx, int32_t* kv_cnt,
-                              cudaStream_t st) {
-  return launch_select_common(1, scores, hq, t, block, segment, tau, forced_first, forced_band, 1, nullptr, mask,
+                              cudaStream_t st, int top_k) {
+  return launch_select_common(1, scores, hq, t, block, segment, tau, top_k, forced_first, forced_band, 1, nullptr, mask,
                               kv_idx, kv_cnt, nullptr, st);
 }
 

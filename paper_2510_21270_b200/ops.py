@@ -66,12 +66,14 @@ def make_shape(q: torch.Tensor, k: torch.Tensor) -> Shape:
 
 
 def make_config(block_size=128, segment_size=256, tau=0.9, strategy="key_permute",
-                forced_first_block=True, forced_diagonal_band=True, scale=0.0) -> PipelineConfig:
-    """PipelineConfig defaults of the reference (pipeline.hpp:30-38)."""
+                forced_first_block=True, forced_diagonal_band=True, scale=0.0, top_k=0) -> PipelineConfig:
+    """PipelineConfig defaults of the reference (pipeline.hpp:30-38).
+    top_k > 0 selects the top_k admissible blocks per row instead of the tau
+    threshold (an extension: the reference has no top-k mode)."""
     if isinstance(strategy, str):
         strategy = _lib.STRATEGIES[strategy]
     return PipelineConfig(block_size, segment_size, tau, strategy, int(forced_first_block),
-                          int(forced_diagonal_band), 0, scale)
+                          int(forced_diagonal_band), int(top_k), scale)
 
 
 def workspace(nbytes: int, device=None) -> torch.Tensor:
@@ -146,15 +148,22 @@ def meanpool_block_scores(qp, kp, block_size, segment_size, scale=0.0):
     return out
 
 
-def select_blocks(scores, block_size, segment_size, tau, forced_first_block=True, forced_diagonal_band=True):
-    """(mask uint8 [H,T,T], kv_idx int32 [H,T,T], kv_cnt int32 [H,T])."""
+def select_blocks(scores, block_size, segment_size, tau, forced_first_block=True, forced_diagonal_band=True,
+                  top_k=0):
+    """(mask uint8 [H,T,T], kv_idx int32 [H,T,T], kv_cnt int32 [H,T]); top_k > 0
+    keeps the top_k admissible blocks per row instead of the tau prefix."""
     _check_dev(scores)
     h, t, _ = scores.shape
     mask = torch.empty(h, t, t, dtype=torch.uint8, device=scores.device)
     kv_idx = torch.empty(h, t, t, dtype=torch.int32, device=scores.device)
     kv_cnt = torch.empty(h, t, dtype=torch.int32, device=scores.device)
-    check(lib().pbs_select_blocks(_ptr(scores), h, t, block_size, segment_size, tau, int(forced_first_block),
-                                  int(forced_diagonal_band), _ptr(mask), _ptr(kv_idx), _ptr(kv_cnt), _stream()))
+    if top_k:
+        check(lib().pbs_select_blocks_top_k(_ptr(scores), h, t, block_size, segment_size, int(top_k),
+                                            int(forced_first_block), int(forced_diagonal_band), _ptr(mask),
+                                            _ptr(kv_idx), _ptr(kv_cnt), _stream()))
+    else:
+        check(lib().pbs_select_blocks(_ptr(scores), h, t, block_size, segment_size, tau, int(forced_first_block),
+                                      int(forced_diagonal_band), _ptr(mask), _ptr(kv_idx), _ptr(kv_cnt), _stream()))
     return mask, kv_idx, kv_cnt
 
 

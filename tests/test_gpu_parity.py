@@ -165,6 +165,45 @@ def test_pipeline_matches_oracle(ops, oracle, strategy, hq, hkv, n, d, b, s, tau
     assert res.report["selected_blocks"] == sel
 
 
+@pytest.mark.parametrize("n,b,s,k", [(2048, 128, 256, 3), (4096, 16, 64, 40), (1000, 32, 64, 1)])
+def test_select_top_k_bitexact(ops, oracle, n, b, s, k):
+    """The top-k extension (north star (3)): the first k admissible blocks of the
+    reference's stable order + forced blocks, against the C restatement."""
+    rng = np.random.default_rng(8)
+    tq, tk, tv, q, kk, v = bf16_inputs(rng, 2, 1, n, 64, kind="vertical_lines")
+    scores = ops.meanpool_block_scores(tq, tk, b, s)
+    mask, kv_idx, kv_cnt = ops.select_blocks(scores, b, s, 0.9, top_k=k)
+    mask, kv_idx, kv_cnt, scores = mask.cpu().numpy(), kv_idx.cpu().numpy(), kv_cnt.cpu().numpy(), scores.cpu().numpy()
+    t = -(-n // b)
+    causal = oracle.build_block_causal_mask(t, b, s)
+    for h in range(2):
+        wm = oracle.select_blocks(scores[h], causal, b, s, 0.9, top_k=k)
+        np.testing.assert_array_equal(mask[h], wm)
+        for i in range(t):
+            sel = np.flatnonzero(wm[i])
+            assert kv_cnt[h, i] == sel.size
+            np.testing.assert_array_equal(kv_idx[h, i, :sel.size], sel)
+
+
+@pytest.mark.parametrize("k", [4, 32])
+def test_pipeline_top_k_matches_oracle(ops, oracle, k):
+    from oracle import make_config as ocfg
+
+    rng = np.random.default_rng(12)
+    hq, hkv, n, d, b, s = 2, 1, 4096, 128, 128, 256
+    tq, tk, tv, q, kk, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0, block=b)
+    res = ops.pbs_attention(tq, tk, tv, ops.make_config(block_size=b, segment_size=s, top_k=k))
+    out, pi, mask = res.output.float().cpu().numpy(), res.pi.cpu().numpy(), res.mask.cpu().numpy()
+    for h in range(hq):
+        r = oracle.pbs_attention(q[h], kk[0], v[0], ocfg(block_size=b, segment_size=s, top_k=k))
+        np.testing.assert_array_equal(pi[h], r.pi)
+        np.testing.assert_array_equal(mask[h], r.mask)
+        err = np.abs(out[h] - r.output)
+        assert err.max() <= BF16_MAX and err.mean() <= BF16_MEAN, (h, err.max(), err.mean())
+        # at most k + forced (block 0 and the row's segment band) per row
+        assert (mask[h].sum(1) <= k + 1 + s // b).all()
+
+
 @pytest.mark.parametrize("kind", ["vertical_lines", "mixed", "gaussian"])
 def test_reference_fixtures_f32(ops, kind):
     """The committed reference runs (oracle/gen_golden.py) through the f32 device path."""

@@ -219,6 +219,28 @@ def test_select_brute_force_and_monotone(oracle):
         assert np.all(hi[lo > 0] > 0)
 
 
+def test_select_top_k_brute_force(oracle):
+    """The top-k extension (no reference counterpart): the first k blocks of
+    the reference's stable descending order (ties by ascending index) + forced."""
+    rng = np.random.default_rng(45)
+    for _ in range(40):
+        t = int(rng.integers(1, 12))
+        rows = np.zeros((t, t))
+        for i in range(t):
+            rows[i, :i + 1] = np.round(rng.random(i + 1), 1)  # rounded: plenty of ties
+        sc, causal = _scores(rows, 4, 0, oracle)
+        k = int(rng.integers(1, 6))
+        m = oracle.select_blocks(sc, causal, 4, 0, 0.9, False, False, top_k=k)
+        for i in range(t):
+            order = sorted(range(i + 1), key=lambda j: (-sc[i, j], j))
+            want = set(order[:k])
+            assert set(np.flatnonzero(m[i])) == want
+    rows = np.array([[1.0, 0, 0, 0], [0.1, 0.5, 0, 0], [0.1, 0.2, 0.2, 0], [0.2, 0.2, 0.3, 0.3]])
+    sc, causal = _scores(rows, 4, 0, oracle)
+    m = oracle.select_blocks(sc, causal, 4, 0, 0.9, True, False, top_k=2)
+    np.testing.assert_array_equal(m, [[1, 0, 0, 0], [1, 1, 0, 0], [1, 1, 1, 0], [1, 0, 1, 1]])
+
+
 def test_select_forced_band(oracle):
     """block_selection_test.cpp:233-252."""
     rows = np.zeros((8, 8))
