@@ -403,7 +403,8 @@ def main():
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (vertical-lines Q/K/V, seeded; selection by the real tau=0.9 algorithm)",
+            "data": ("synthetic (vertical-lines Q/K/V, seeded; selection by the real tau=0.9 algorithm)" if not args.top_k
+                     else f"synthetic (vertical-lines Q/K/V, seeded; top-{args.top_k} selection, an extension)"),
             "config": {"workload": f"{PREFIX}_{n // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
                        "seq_len": n, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
                        "strategy": STRATEGY, "top_k": args.top_k or None, "parallelism": f"heads{world}",
