@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(256) importance_exp_kernel(float* __restrict__
 // copy per tile (the whole ring in flight), warp 0 is the adder, one dependent
 // chain of N adds per lane.  Shapes whose row groups are not whole 16-byte
 // pieces (take % 4 != 0 or a partial row group) take 4-byte cp.async copies.
-constexpr int kJT = 128;    // keys per ring tile (one barrier round trip per 128 adds)
-constexpr int kRing = 8;    // 8 tiles = 128 KB in flight
+constexpr int kJT = 256;    // keys per ring tile (one barrier round trip per 256 adds)
+constexpr int kRing = 4;    // 4 tiles = 128 KB in flight
 
 __device__ __forceinline__ void tma_load_3d_f32(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                 int c2) {
@@ -219,11 +219,14 @@ __global__ void __launch_bounds__(64, 1) importance_denom_kernel(const __grid_co
       ptx::mbar_wait(&full[slot], (uint32_t)((t / kRing) & 1));
       const int cnt = (int)min64(kJT, n - t * kJT);
       if (cnt == kJT) {
-        float v[kJT];
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) v[jj] = ring[slot][jj][lane];
+        for (int j0 = 0; j0 < kJT; j0 += 128) {
+          float v[128];
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) denom = __fadd_rn(denom, v[jj]);
+          for (int jj = 0; jj < 128; ++jj) v[jj] = ring[slot][j0 + jj][lane];
+#pragma unroll
+          for (int jj = 0; jj < 128; ++jj) denom = __fadd_rn(denom, v[jj]);
+        }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&empty[slot]);
       } else {

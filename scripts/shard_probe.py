@@ -19,6 +19,6 @@ for world in (1, 2, 4, 8):
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
     r = ops.pbs_attention(q, k, v, cfg, report=True, out=out, return_perms=False, ws=ws).report
-    print(f"world {world}: {q1 - q0} heads {ms:.2f} ms (ideal {47.7 / world:.2f})",
+    print(f"world {world}: {q1 - q0} heads {ms:.2f} ms (1-GPU time / world: see world 1)",
           {kk: round(r[kk] / 1e3, 2) for kk in ("estimate_us", "permute_us", "select_us", "attention_us")})
     del q, k, v, out
