@@ -18,7 +18,9 @@
 //   warp 1       TMEM owner + MMA issuer (warp-collective, one elected lane):
 //                  S_w = Q K_e^T        (SS: Q, K K-major in smem), w = e & 1
 //                  O_w (+)= P_e V_e     (TS: P over S_w in TMEM, V MN-major)
-//                per item S_0, S_1, then per block e: PV(e), QK(e + 2)
+//                per item S_0, S_1, then per block e: PV(e), QK(e + 2); the
+//                PV of keys 0-63 starts when the group signals that half of P
+//                (p_half), the rest at p_full
 //   warps 4..7   softmax group 0: the item's visited blocks e = 0, 2, 4, ...
 //   warps 8..11  softmax group 1: blocks e = 1, 3, 5, ...
 // TMEM holds S_0 | S_1 | O_0 | O_1.  A softmax thread owns one query row (one
@@ -86,6 +88,7 @@ struct __align__(8) Barriers {
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[kGroups];  // S_w = Q K^T complete (and every earlier MMA: the group's previous PV)
+  uint64_t p_half[kGroups];  // P_w's first 64 keys written (the PV of those keys may start)
   uint64_t p_full[kGroups];  // P_w written into TMEM over S_w by the group's 128 threads
   uint64_t o_full, o_free;   // the item's last PV complete / both groups' epilogue read O
   uint64_t drained;  // every tcgen05 operation of the MMA issuer complete (before dealloc)
@@ -231,6 +234,30 @@ __device__ __forceinline__ void tc_mma_qk8(uint32_t d_tmem, uint64_t adesc, uint
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, t;\n"
       "}\n" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+
+// PV over 64 keys: 4 MMAs (K = 16 keys each), A = P in TMEM (+8 columns per
+// step), B = V rows advancing 16 x 128 bytes (encoded +128) per step.
+__device__ __forceinline__ void tc_mma_pv4(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, t, p;\n"
+      ".reg .b32 a1, a2, a3;\n"
+      ".reg .b64 b1, b2, b3;\n"
+      "setp.ne.b32 t, 1, 0;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "add.s32 a1, %1, 8;   add.s64 b1, %2, 128;\n"
+      "add.s32 a2, %1, 16;  add.s64 b2, %2, 256;\n"
+      "add.s32 a3, %1, 24;  add.s64 b3, %2, 384;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
@@ -588,7 +615,8 @@ __device__ __forceinline__ float load_scores(uint32_t tS, const int* ko, int qo,
 // PV MMA), one 32-key chunk at a time; returns sum p.  Packed f32x2 FMA/add;
 // kPolyPer16 of every 16 keys take the FMA-pipe polynomial.
 template <int kPolyPer16>
-__device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, float neg_m, uint32_t tP) {
+__device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, float neg_m, uint32_t tP,
+                                        uint64_t* half_bar) {
   const uint64_t sc2 = pk2(sc, sc), nm2 = pk2(neg_m, neg_m);
   uint64_t sum2[2] = {0ull, 0ull};
 #pragma unroll
@@ -610,6 +638,11 @@ __device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, fl
       pk[jp] = *reinterpret_cast<uint32_t*>(&b2);
     }
     TMEM_ST16(tP + c * 16, pk);
+    if (c == 1) {  // keys 0..63 are in TMEM: their half of the PV may start
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(half_bar);
+    }
   }
   float s0, s1, s2, s3;
   upk2(sum2[0], s0, s1);
@@ -653,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int w = 0; w < kGroups; ++w) {
       mbar_init(&bar->s_full[w], 1);
+      mbar_init(&bar->p_half[w], 128);
       mbar_init(&bar->p_full[w], 128);
     }
     mbar_init(&bar->o_full, 1);
@@ -748,14 +782,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int w = e & 1;
         const uint32_t stage = v_it % kVStages;
         mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
+        if (e == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // the previous epilogue read O_0 and O_1
+        // A = P [128 q x 128 kv] in TMEM (64 columns over S_w); B = V [128 kv x 128 d] MN-major SW128.
+        // Keys 0..63 go as soon as the group wrote them, keys 64..127 after the rest.
+        static_assert(kBN == 128, "two 64-key PV halves");
+        const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
+        mbar_wait(&bar->p_half[w], p_cnt[w] & 1);
+        tc_fence_after();
+        tc_mma_pv4(tmem + col_o(w), tmem + col_s(w), sdesc(v_base, kPanelBytes, 1024), idesc_pv, e < kGroups ? 0u : 1u);
         mbar_wait(&bar->p_full[w], p_cnt[w] & 1);
         ++p_cnt[w];
-        if (e == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // the previous epilogue read O_0 and O_1
         tc_fence_after();
-        const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
-        // A = P [128 q x 128 kv] in TMEM (64 columns over S_w); B = V [128 kv x 128 d] MN-major SW128
-        static_assert(kBN == 128, "tc_mma_pv8 covers 128 keys");
-        tc_mma_pv8(tmem + col_o(w), tmem + col_s(w), sdesc(v_base, kPanelBytes, 1024), idesc_pv, e < kGroups ? 0u : 1u);
+        tc_mma_pv4(tmem + col_o(w), tmem + col_s(w) + 32, sdesc(v_base + 64 * 128, kPanelBytes, 1024), idesc_pv, 1u);
         tc_commit_w(&bar->v_empty[stage]);
         if (e + 1 == len) tc_commit_w(&bar->o_full);
         ++v_it;
@@ -866,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             TMEM_ST32(tO + c * 32, o);
           }
         }
-        const float rs = emit_p<kPolyPer16>(r, sc, neg_m, tS);
+        const float rs = emit_p<kPolyPer16>(r, sc, neg_m, tS, &bar->p_half[w]);
         l = l * factor + rs;
         tmem_wait_st();
         tc_fence_before();
