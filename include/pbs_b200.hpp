@@ -50,6 +50,7 @@ struct PipelineConfig {
   bool forced_first_block = true;
   bool forced_diagonal_band = true;
   double scale = 0.0;
+  int top_k = 0;  // extension: > 0 keeps the top_k blocks per row instead of the tau prefix
 
   pbs_pipeline_config c() const {
     pbs_pipeline_config r{};
@@ -60,6 +61,7 @@ struct PipelineConfig {
     r.forced_first_block = forced_first_block ? 1 : 0;
     r.forced_diagonal_band = forced_diagonal_band ? 1 : 0;
     r.scale = scale;
+    r.top_k = top_k;
     return r;
   }
 };
@@ -97,6 +99,67 @@ inline void build_key_permutation(const float* scores, int heads, std::size_t n,
 inline void apply_rows(const int32_t* perm, const void* src, int src_heads, int dst_heads, std::size_t rows,
                        int cols, int dtype, void* dst, void* stream = nullptr) {
   check(pbs_apply_rows(perm, src, src_heads, dst_heads, (int64_t)rows, cols, dtype, dst, stream));
+}
+
+/// build_query_permutation (permutation.hpp:206-275); k may be K' (strategy both).
+inline void build_query_permutation(const void* q, const void* k, int k_heads, const pbs_shape& s,
+                                    std::size_t block, std::size_t segment, int32_t* perm, int32_t* inv, void* ws,
+                                    std::size_t ws_bytes, void* stream = nullptr) {
+  check(pbs_build_query_permutation(q, k, k_heads, &s, (int64_t)block, (int64_t)segment, perm, inv, ws, ws_bytes,
+                                    stream));
+}
+
+/// meanpool_block_scores (block_selection.hpp:120-161) under the segment-band mask.
+inline void meanpool_block_scores(const void* qp, const void* kp, const pbs_shape& s, std::size_t block,
+                                  std::size_t segment, double scale, float* scores, void* ws, std::size_t ws_bytes,
+                                  void* stream = nullptr) {
+  check(pbs_meanpool_block_scores(qp, kp, &s, (int64_t)block, (int64_t)segment, scale, scores, ws, ws_bytes,
+                                  stream));
+}
+
+/// select_blocks (block_selection.hpp:171-206); top_k > 0 selects by rank instead (extension).
+inline void select_blocks(const float* scores, int heads, std::size_t t, std::size_t block, std::size_t segment,
+                          double tau, uint8_t* mask, int32_t* kv_idx = nullptr, int32_t* kv_cnt = nullptr,
+                          bool forced_first = true, bool forced_band = true, int top_k = 0,
+                          void* stream = nullptr) {
+  if (top_k > 0)
+    check(pbs_select_blocks_top_k(scores, heads, (int64_t)t, (int64_t)block, (int64_t)segment, top_k,
+                                  forced_first ? 1 : 0, forced_band ? 1 : 0, mask, kv_idx, kv_cnt, stream));
+  else
+    check(pbs_select_blocks(scores, heads, (int64_t)t, (int64_t)block, (int64_t)segment, tau, forced_first ? 1 : 0,
+                            forced_band ? 1 : 0, mask, kv_idx, kv_cnt, stream));
+}
+
+/// attention_block_sparse (attention.hpp:259-310) over the selected blocks, with the
+/// original-position element mask (q_orig = sigma, k_orig = pi) and the fused un-permute.
+inline void attention_block_sparse(const void* qp, const void* kp, const void* vp, int kv_heads,
+                                   const pbs_shape& s, std::size_t block, const int32_t* kv_idx,
+                                   const int32_t* kv_cnt, void* out, const int32_t* q_orig = nullptr,
+                                   const int32_t* k_orig = nullptr, const int32_t* out_rows = nullptr,
+                                   int32_t* status = nullptr, double scale = 0.0, void* stream = nullptr) {
+  check(pbs_block_sparse_attention_fwd(qp, kp, vp, kv_heads, &s, (int64_t)block, scale, kv_idx, kv_cnt, q_orig,
+                                       k_orig, out_rows, out, status, stream));
+}
+
+/// The dense causal comparator (attention_tiled, causal, attention.hpp:314-321).
+inline void dense_causal_attention(const void* q, const void* k, const void* v, const pbs_shape& s, void* out,
+                                   double scale = 0.0, void* stream = nullptr) {
+  check(pbs_dense_causal_attention_fwd(q, k, v, &s, scale, out, stream));
+}
+
+/// PBST files (tensor_io.hpp) to and from device memory.
+inline pbs_tensor_info tensor_info(const char* path) {
+  pbs_tensor_info i{};
+  check(pbs_tensor_info_read(path, &i));
+  return i;
+}
+inline void load_tensor(const char* path, void* dst, int dst_dtype, void* stream = nullptr) {
+  check(pbs_tensor_load(path, dst, dst_dtype, stream));
+}
+inline void save_tensor(const char* path, const void* src, int src_dtype, std::size_t heads, std::size_t rows,
+                        std::size_t cols, bool f64_file = false, bool as_stack = true, void* stream = nullptr) {
+  check(pbs_tensor_save(path, src, src_dtype, (int64_t)heads, (int64_t)rows, (int64_t)cols, f64_file ? 1 : 0,
+                        as_stack ? 1 : 0, stream));
 }
 
 /// The full Algorithm 1 (pbs_attention, pipeline.hpp:107-193) on device buffers.
