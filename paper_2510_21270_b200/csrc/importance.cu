@@ -123,9 +123,34 @@ __global__ void __launch_bounds__(256) importance_exp_kernel(float* __restrict__
   const int64_t cnt = min64(kExpKeys, n - j0) * take;
   float* base = L + ((int64_t)h * n + j0) * take;
   if (take % 4 == 0 && take <= 1024) {
-    // four 16-byte loads in flight per thread before any exp
+    // four 16-byte loads in flight per thread before any exp.  When take
+    // divides 4 x blockDim (take = B = 128), a thread's row offset i never
+    // changes (the CTA starts on a key boundary): its four maxima are hoisted.
     float4* b4 = reinterpret_cast<float4*>(base);
     const int64_t n4 = cnt / 4;
+    if ((4 * (int)blockDim.x) % take == 0) {
+      const int i = (4 * (int)threadIdx.x) % take;
+      const float m0 = mx[i], m1 = mx[i + 1], m2 = mx[i + 2], m3 = mx[i + 3];
+      for (int64_t e0 = threadIdx.x; e0 < n4; e0 += 4 * (int64_t)blockDim.x) {
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t e = e0 + (int64_t)u * blockDim.x;
+          if (e < n4) x[u] = b4[e];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t e = e0 + (int64_t)u * blockDim.x;
+          if (e >= n4) break;
+          x[u].x = expf_glibc(__fsub_rn(x[u].x, m0), tab);
+          x[u].y = expf_glibc(__fsub_rn(x[u].y, m1), tab);
+          x[u].z = expf_glibc(__fsub_rn(x[u].z, m2), tab);
+          x[u].w = expf_glibc(__fsub_rn(x[u].w, m3), tab);
+          b4[e] = x[u];
+        }
+      }
+      return;
+    }
     for (int64_t e0 = threadIdx.x; e0 < n4; e0 += 4 * (int64_t)blockDim.x) {
       float4 x[4];
 #pragma unroll
