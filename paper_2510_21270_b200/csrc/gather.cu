@@ -37,9 +37,12 @@ __global__ void __launch_bounds__(256) apply_rows_vec_kernel(const int32_t* __re
       const int64_t r = base + (int64_t)u * kRowsPerPass + sub;
       rr[u] = r;
       if (r < total_rows) {
-        const int64_t h = r / rows, i = r % rows;
-        const int64_t s = perm ? __ldg(perm + r) : i;
-        const int4* sp = src + ((h / group) * rows + s) * kVecPerRow;
+        // 32-bit head / row split (total_rows < 2^31 is checked at launch):
+        // a 64-bit division per row cost more issue slots than the copy
+        const uint32_t r32 = (uint32_t)r, rows32 = (uint32_t)rows;
+        const uint32_t h = r32 / rows32, i = r32 - h * rows32;
+        const int64_t s = perm ? __ldg(perm + r) : (int64_t)i;
+        const int4* sp = src + ((int64_t)(h / (uint32_t)group) * rows + s) * kVecPerRow;
 #pragma unroll
         for (int w = 0; w < kVecPerLane; ++w) v[u][w] = __ldg(sp + col + w * 32);
       }
@@ -81,7 +84,8 @@ int launch_apply_rows(const int32_t* perm, const void* src, int src_heads, int d
   const int64_t total = rows * dst_heads;
   const int64_t row_bytes = (int64_t)cols * esize;
   const int blocks = (int)min64(ceil_div(total, 8 * 8), 148 * 16);
-  const bool aligned = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  const bool aligned = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0) &&
+                       total < ((int64_t)1 << 31);  // the vector kernels split rows in 32 bits
   if (aligned && row_bytes == 256) {
     apply_rows_vec_kernel<16><<<blocks, 256, 0, st>>>(perm, static_cast<const int4*>(src), group, rows, total,
                                                      static_cast<int4*>(dst));
