@@ -1180,14 +1180,13 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
     a.vis = vis;
     a.nvis = nvis;
   }
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_seen{0};
+  if (first_use_on_device(attr_seen)) {
     PBS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         SmemLayout::total));
     int dev = 0;
     PBS_CUDA_CHECK(cudaGetDevice(&dev));
     PBS_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    attr = true;
   }
   int grid = (int)min64(a.items, g_num_sms);
   if (const char* e = getenv("PBS_ATTN_GRID")) grid = (int)min64(grid, atoi(e) > 0 ? atoi(e) : grid);  // debug

@@ -540,12 +540,10 @@ int launch_importance_logits(const void* q, const void* k, int dtype, int hq, in
     auto kk = static_cast<const __nv_bfloat16*>(k);
     if (vec && d % xgemm::kChunkW == 0) {
       auto kern = importance_logits_kernel<__nv_bfloat16, true, true, true>;
-      static bool attr = false;
-      if (!attr) {
+      static std::atomic<uint64_t> attr_seen{0};
+      if (first_use_on_device(attr_seen))
         PBS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)sizeof(xgemm::SmemWide)));
-        attr = true;
-      }
       kern<<<grid, xgemm::kThreads, sizeof(xgemm::SmemWide), st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L,
                                                                    W.rowmax, h0);
     } else if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
@@ -570,11 +568,9 @@ int launch_importance_finish(int hq, int64_t n, int64_t block, float* scores, vo
   importance_exp_kernel<<<dim3((unsigned)ceil_div(n, kExpKeys), (unsigned)hq), 256, 0, st>>>(L, W.rowmax, take, n);
   PBS_LAUNCH_CHECK("importance_exp_kernel");
   const size_t smem = sizeof(float) * kRing * kJT * 32 + 2 * kRing * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_seen{0};
+  if (first_use_on_device(attr_seen))
     PBS_CUDA_CHECK(cudaFuncSetAttribute(importance_denom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
   alignas(64) CUtensorMap tm_e;
   const bool tma = (take % 4 == 0) && (take % 32 == 0);  // every CTA's 32 rows are whole 16-byte pieces
   if (tma) {
