@@ -247,6 +247,26 @@ def test_dense_causal_matches_sdpa(ops):
     assert err.max().item() <= BF16_MAX and err.mean().item() <= BF16_MEAN
 
 
+@pytest.mark.parametrize("growth", [6.0, 40.0])
+def test_dense_causal_running_max_growth(ops, growth):
+    """Logits that grow along the keys (key norms ramp up), so the online
+    softmax's running max rises block after block: the lazy rescale of O (max
+    grows by more than 2^8) runs many times per row, in both softmax groups."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n, d = 4096, 128
+    q = torch.randn(2, n, d, device="cuda", generator=g)
+    u = torch.randn(d, device="cuda", generator=g)
+    q = (q + 2.0 * u).to(torch.bfloat16)
+    ramp = torch.linspace(0.0, growth, n, device="cuda")[:, None]
+    k = (torch.randn(1, n, d, device="cuda", generator=g) * 0.5 + ramp * u / u.norm()).to(torch.bfloat16)
+    v = torch.randn(1, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    out = ops.dense_causal_attention(q, k, v).float()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float()[None], k.float().expand(2, n, d)[None],
+                                                           v.float().expand(2, n, d)[None], is_causal=True)[0]
+    err = (out - ref).abs()
+    assert err.max().item() <= BF16_MAX and err.mean().item() <= BF16_MEAN, (err.max().item(), err.mean().item())
+
+
 def test_tau_one_is_causal_attention(ops):
     """pipeline_test.cpp:27-58 (C4) on device: tau = 1 selects the full causal grid."""
     rng = np.random.default_rng(5)
