@@ -162,6 +162,12 @@ inline void save_tensor(const char* path, const void* src, int src_dtype, std::s
                         as_stack ? 1 : 0, stream));
 }
 
+/// The stage-5 un-permute (pipeline.hpp:178-180): dst[h][sigma[h][i]] = src[h][i].
+inline void unpermute(const int32_t* sigma, const void* src, int heads, std::size_t rows, int cols, int dtype,
+                      void* dst, void* stream = nullptr) {
+  check(pbs_unpermute(sigma, src, heads, (int64_t)rows, cols, dtype, dst, stream));
+}
+
 /// The full Algorithm 1 (pbs_attention, pipeline.hpp:107-193) on device buffers.
 inline std::size_t workspace_size(const pbs_shape& s, const PipelineConfig& cfg) {
   const pbs_pipeline_config c = cfg.c();

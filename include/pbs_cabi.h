@@ -144,6 +144,13 @@ PBS_API int pbs_build_query_permutation(const void* q, const void* k, int32_t k_
 PBS_API int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int32_t dst_heads,
                    int64_t rows, int32_t cols, int32_t dtype, void* dst, void* stream);
 
+/* Stage 5, the un-permute (pipeline.hpp:178-180, O = apply_rows(sigma^-1, O')):
+ * dst[h][sigma[h][i]] = src[h][i] over [H, rows, cols] buffers.  The fused
+ * pipeline does this in the attention epilogue (out_rows); this is the
+ * standalone operator. */
+PBS_API int pbs_unpermute(const int32_t* sigma, const void* src, int32_t num_heads, int64_t rows, int32_t cols,
+                  int32_t dtype, void* dst, void* stream);
+
 /* ---- stage 3: block scores + selection ---------------------------------- */
 
 /* meanpool_block_scores (block_selection.hpp:120-161) under the

@@ -222,6 +222,13 @@ int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int3
   return launch_apply_rows(perm, src, src_heads, dst_heads, rows, cols, esize_of(dtype), dst, as_stream(stream));
 }
 
+int pbs_unpermute(const int32_t* sigma, const void* src, int32_t num_heads, int64_t rows, int32_t cols,
+                  int32_t dtype, void* dst, void* stream) {
+  if (dtype != PBS_DTYPE_BF16 && dtype != PBS_DTYPE_F32) return fail(PBS_ERR_CONFIG, "E_CONFIG", "bad dtype");
+  if (num_heads < 0 || rows < 0 || cols < 0) return fail(PBS_ERR_CONFIG, "E_SHAPE", "unpermute: negative shape");
+  return launch_scatter_rows(sigma, src, num_heads, rows, cols, esize_of(dtype), dst, as_stream(stream));
+}
+
 int pbs_meanpool_block_scores(const void* qp, const void* kp, const pbs_shape* shape, int64_t block_size,
                               int64_t segment_size, double scale, float* scores, void* workspace,
                               size_t workspace_bytes, void* stream) {

@@ -35,6 +35,9 @@ int launch_identity(int32_t* perm, int heads, int64_t n, cudaStream_t st);
 int make_f32_map_3d(void* map, const float* base, int64_t d0, int64_t d1, int64_t d2, int box0, int box1);
 
 // ---- stage 2 (gather.cu) ------------------------------------------------------
+// the un-permute: dst[h][perm[h][i]] = src[h][i] (pipeline.hpp:178-180)
+int launch_scatter_rows(const int32_t* perm, const void* src, int heads, int64_t rows, int cols, int esize,
+                        void* dst, cudaStream_t st);
 int launch_apply_rows(const int32_t* perm, const void* src, int src_heads, int dst_heads,
                       int64_t rows, int cols, int esize, void* dst, cudaStream_t st);
 

@@ -11,6 +11,7 @@ and stream plumbing here.
     build_key_permutation     permutation.hpp:182-201 (+ flatten, inverse)
     build_query_permutation   permutation.hpp:206-275
     apply_rows                permutation.hpp:79-89
+    unpermute                 pipeline.hpp:178-180
     meanpool_block_scores     block_selection.hpp:120-161
     select_blocks             block_selection.hpp:171-206
     attention_block_sparse    attention.hpp:259-310
@@ -133,6 +134,16 @@ def apply_rows(perm, src, dst_heads=None):
     dst = torch.empty(hd, n, d, dtype=src.dtype, device=src.device)
     check(lib().pbs_apply_rows(_ptr(perm), _ptr(src), hs, hd, n, d, _dtype_code(src), _ptr(dst), _stream()))
     return dst
+
+
+def unpermute(sigma, src):
+    """The stage-5 un-permute (pipeline.hpp:178-180): out[h][sigma[h][i]] = src[h][i],
+    i.e. apply_rows(sigma^-1, src) without forming the inverse."""
+    _check_dev(sigma, src)
+    h, n, d = src.shape
+    out = torch.empty_like(src)
+    check(lib().pbs_unpermute(_ptr(sigma), _ptr(src), h, n, d, _dtype_code(src), _ptr(out), _stream()))
+    return out
 
 
 def meanpool_block_scores(qp, kp, block_size, segment_size, scale=0.0):

@@ -165,6 +165,23 @@ def test_pipeline_matches_oracle(ops, oracle, strategy, hq, hkv, n, d, b, s, tau
     assert res.report["selected_blocks"] == sel
 
 
+@pytest.mark.parametrize("d,dtype", [(128, torch.bfloat16), (64, torch.float32), (20, torch.bfloat16)])
+def test_unpermute_inverts_the_gather(ops, d, dtype):
+    """pbs_unpermute (pipeline.hpp:178-180): out[sigma[i]] = src[i] == apply_rows(sigma^-1, src)."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    h, n = 3, 1000
+    sigma = torch.stack([torch.randperm(n, generator=g, device="cuda") for _ in range(h)]).int()
+    x = torch.randn(h, n, d, generator=g, device="cuda").to(dtype)
+    xp = ops.apply_rows(sigma, x)
+    assert torch.equal(ops.unpermute(sigma, xp), x)
+    y = torch.randn(h, n, d, generator=g, device="cuda").to(dtype)
+    got = ops.unpermute(sigma, y).float().cpu().numpy()
+    for hh in range(h):
+        inv = np.argsort(sigma[hh].cpu().numpy())  # Permutation::inverse (permutation.hpp:51-55)
+        want = y[hh].float().cpu().numpy()[inv]   # apply_rows: out.row(i) = m.row(p[i]) (79-89)
+        np.testing.assert_array_equal(got[hh], want)
+
+
 @pytest.mark.parametrize("n,b,s,k", [(2048, 128, 256, 3), (4096, 16, 64, 40), (1000, 32, 64, 1)])
 def test_select_top_k_bitexact(ops, oracle, n, b, s, k):
     """The top-k extension (north star (3)): the first k admissible blocks of the
