@@ -753,11 +753,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
-    uint32_t q_it = 0, k_it = 0, v_it = 0, o_no = 0, p_cnt[kGroups] = {0, 0};
+    uint32_t q_it = 0, k_it = 0, v_it = 0, o_no = 0, p_cnt[kGroups] = {0, 0}, gbase = 0;
     auto issue_qk = [&](int e, int len) {
       const int w = e & 1;
       const uint32_t stage = k_it % kKStages;
+      if (lane == 0) trace_event(a, 10, gbase + e);
       mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
+      if (lane == 0) trace_event(a, 12, gbase + e);
       tc_fence_after();
       const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
       static_assert(kD == 128 && kPanelBytes == 1024 * 16, "tc_mma_qk8 descriptor steps");
@@ -765,6 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_commit_w(&bar->s_full[w]);
       tc_commit_w(&bar->k_empty[stage]);
       if (e + 1 == len) tc_commit_w(&bar->q_empty);  // every QK of the item issued: Q is free once they complete
+      if (lane == 0) trace_event(a, 2, gbase + e);
       ++k_it;
     };
     ItemStream items;
@@ -781,7 +784,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = 0; e < len; ++e) {
         const int w = e & 1;
         const uint32_t stage = v_it % kVStages;
+        if (lane == 0) trace_event(a, 3, gbase + e);
         mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
+        if (lane == 0) trace_event(a, 11, gbase + e);
         if (e == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // the previous epilogue read O_0 and O_1
         // A = P [128 q x 128 kv] in TMEM (64 columns over S_w); B = V [128 kv x 128 d] MN-major SW128.
         // Keys 0..63 go as soon as the group wrote them, keys 64..127 after the rest.
@@ -791,14 +796,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tc_mma_pv4(tmem + col_o(w), tmem + col_s(w), sdesc(v_base, kPanelBytes, 1024), idesc_pv, e < kGroups ? 0u : 1u);
         mbar_wait(&bar->p_full[w], p_cnt[w] & 1);
+        if (lane == 0) trace_event(a, 0, gbase + e);
         ++p_cnt[w];
         tc_fence_after();
         tc_mma_pv4(tmem + col_o(w), tmem + col_s(w) + 32, sdesc(v_base + 64 * 128, kPanelBytes, 1024), idesc_pv, 1u);
         tc_commit_w(&bar->v_empty[stage]);
         if (e + 1 == len) tc_commit_w(&bar->o_full);
+        if (lane == 0) trace_event(a, 1, gbase + e);
         ++v_it;
         if (e + kGroups < len) issue_qk(e + kGroups, len);
       }
+      gbase += len;
       ++o_no;
     }
     // nothing may still write TMEM when it is released
@@ -835,7 +843,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* xch = reinterpret_cast<float*>(smem + SmemLayout::xch);  // [2 items][kGroups][2][128]
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
-    uint32_t s_cnt = 0, o_cnt = 0;
+    uint32_t s_cnt = 0, o_cnt = 0, gbase = 0;  // gbase: blocks of earlier items (trace numbering)
+    const bool tr = (row == 0);
     ItemStream items;
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
@@ -857,7 +866,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           ko[row] = v;
           named_bar_sync(1 + w, 128);
         }
+        if (tr) trace_event(a, 7, gbase + e);
         mbar_wait(&bar->s_full[w], s_cnt & 1);
+        if (tr) trace_event(a, 4, gbase + e);
         ++s_cnt;
         tc_fence_after();
         uint32_t r[kCols];
@@ -878,6 +889,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1 + w, 128);  // ko may be refilled after this
         }
         const float hmax = load_scores<false>(tS, ko, qo, r);
+        if (tr) trace_event(a, 5, gbase + e);
         // online softmax (absorb, attention.hpp:96-126) in the log2 domain with
         // lazy rescaling: O_w is rescaled only when the max grows by more than 8
         const float m_new = fmaxf(m, hmax * sc);
@@ -908,8 +920,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         l = l * factor + rs;
         tmem_wait_st();
         tc_fence_before();
+        if (tr) trace_event(a, 6, gbase + e);
         mbar_arrive(&bar->p_full[w]);
       }
+      gbase += vis.len;
       // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138): merge
       // the two groups' (m, l, O), O / l -> out[out_rows[i]] (the fused
       // un-permute, pipeline.hpp:178); group w writes output columns [64 w, 64 w + 64)
@@ -1192,13 +1206,13 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   if (const char* e = getenv("PBS_ATTN_GRID")) grid = (int)min64(grid, atoi(e) > 0 ? atoi(e) : grid);  // debug
   const char* trace_path = getenv("PBS_ATTN_TRACE");
   if (trace_path) {
-    PBS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), 12 * kTraceEvents * 8, st));
-    PBS_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 12 * kTraceEvents * 8, st));
+    PBS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), 16 * kTraceEvents * 8, st));
+    PBS_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 16 * kTraceEvents * 8, st));
   }
   attn_sm100_kernel<<<grid, kThreads, SmemLayout::total, st>>>(mq, mk, mv, a);
   PBS_LAUNCH_CHECK("attn_sm100_kernel");
   if (trace_path) {  // debug only: synchronous dump of CTA 0's timeline
-    std::vector<unsigned long long> h(12 * kTraceEvents);
+    std::vector<unsigned long long> h(16 * kTraceEvents);
     PBS_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
     PBS_CUDA_CHECK(cudaStreamSynchronize(st));
     PBS_CUDA_CHECK(cudaFree(a.trace));

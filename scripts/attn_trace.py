@@ -1,56 +1,67 @@
-"""Debug: record CTA 0's attention pipeline timeline (PBS_ATTN_TRACE) on the
-C3 bench workload and print per-block phase latencies (SM clocks)."""
+"""Debug: CTA 0's attention pipeline timeline on the C3 bench workload.
+
+Needs a build with the trace events compiled in:
+    PBS_NVCC_EXTRA=-DPBS_ATTN_TRACE_EVENTS python -m paper_2510_21270_b200.build --force
+then PBS_ATTN_TRACE (set below) dumps clock64 stamps of CTA 0.  Events,
+indexed by the CTA-cumulative visited block g (group g % 2 within an item):
+  0 MMA sees P(g) complete   1 PV(g) issued      2 QK(g) issued      3 MMA starts waiting for V(g)
+  4 S(g) ready (softmax)     5 max(g) done       6 P(g) written      7 softmax starts waiting for S(g)
+  10 MMA starts waiting for K(g)   11 MMA sees V(g)   12 MMA sees K(g)
+
+    python scripts/attn_trace.py [N]          # record and analyse
+    python scripts/attn_trace.py --analyse F  # analyse a recorded dump
+"""
 import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch  # noqa: E402
 
-import bench  # noqa: E402
-from paper_2510_21270_b200 import ops  # noqa: E402
+def analyse(path):
+    t = np.fromfile(path, dtype=np.uint64).reshape(16, 4096).astype(np.int64)
+    mma_p, pv, qk, mma_w, sr, md, pd, sw = (t[i] for i in range(8))
+    kw, vs, ks = t[10], t[11], t[12]
+    if not (sr > 0).any():
+        sys.exit("no events: rebuild with PBS_NVCC_EXTRA=-DPBS_ATTN_TRACE_EVENTS")
+    g = np.arange(200, 3000)
+    ok = np.all([x[g] > 0 for x in (mma_p, pv, mma_w, sr, md, pd, sw, vs)], axis=0) & (sr[g + 2] > 0) & (qk[g + 2] > 0)
+    g = g[ok]
+    med = lambda x: float(np.median(x))  # noqa: E731
+    span = (sr[g[-1]] - sr[g[0]]) / max(1, g[-1] - g[0])
+    print(f"CTA 0: {len(g)} blocks; mean period per block {span:.0f} clk (ideal 1024: MMA 2 x 512, exp 16384 / 16)")
+    print("  softmax waits for S(g)                 ", med(sr[g] - sw[g]))
+    print("  S(g) ready -> max done (load + max)    ", med(md[g] - sr[g]))
+    print("  max done -> P(g) written (exp + store) ", med(pd[g] - md[g]))
+    print("  P(g) written -> MMA sees it            ", med(mma_p[g] - pd[g]))
+    print("  MMA waits for V(g)                     ", med(vs[g] - mma_w[g]))
+    print("  MMA sees P(g) -> PV(g) second half out ", med(pv[g] - mma_p[g]))
+    print("  PV(g) issued -> QK(g+2) issued         ", med(qk[g + 2] - pv[g]))
+    print("  MMA waits for K(g+2)                   ", med(ks[g + 2] - kw[g + 2]))
+    print("  QK(g+2) issued -> S(g+2) ready         ", med(sr[g + 2] - qk[g + 2]))
+    print("  P(g) written -> S(g+2) ready           ", med(sr[g + 2] - pd[g]))
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
-dense = len(sys.argv) > 2 and sys.argv[2] == "dense"
-q, k, v = bench.make_inputs(torch, n, 0, 32, list(range(8)), "cuda")
-cfg = ops.make_config(block_size=128, segment_size=256, tau=0.9, strategy="key_permute")
-path = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "attn_trace.bin")
-os.makedirs(os.path.dirname(path), exist_ok=True)
-for _ in range(2):
-    (ops.dense_causal_attention(q, k, v) if dense else ops.pbs_attention(q, k, v, cfg, report=False))
-torch.cuda.synchronize()
-os.environ["PBS_ATTN_TRACE"] = path
-(ops.dense_causal_attention(q, k, v) if dense else ops.pbs_attention(q, k, v, cfg, report=False))
-torch.cuda.synchronize()
-t = np.fromfile(path, dtype=np.uint64).reshape(12, 4096).astype(np.int64)
-names = ["mma_sees_p0", "mma_sees_p1", "pv_issue0", "pv_issue1", "qk_issue0", "qk_issue1", "s_ready0", "s_ready1",
-         "p_done0", "p_done1", "max_done0", "max_done1"]
-t0 = t[t > 0].min()
-lo, hi = 100, 1500
-sr, pd, md, qk, pv, ms, pvd = (t[6], t[8], t[10], t[4], t[2], t[0], t[3])
-b = np.arange(lo, hi)
-ok = (sr[b] > 0) & (pd[b] > 0) & (qk[b] > 0) & (pv[b] > 0) & (ms[b] > 0) & (sr[b + 2] > 0)
-b = b[ok]
-med = lambda x: float(np.median(x))
-print(f"CTA 0: blocks {len(b)}   (order per block b: QK(b+1) issued, PV(b-1)... see below)")
-print("  softmax: S(b) ready -> max done      ", med(md[b] - sr[b]))
-print("  softmax: max done -> P(b) written    ", med(pd[b] - md[b]))
-print("  P(b) written -> MMA sees P(b)        ", med(ms[b] - pd[b]))
-print("  MMA sees P(b) -> PV(b) issued        ", med(pv[b] - ms[b]))
-print("  PV(b) issued -> PV(b) complete       ", med(pvd[b] - pv[b]))
-print("  PV(b) issued -> QK(b+2) issued       ", med(qk[b + 2] - pv[b]))
-print("  QK(b+2) issued -> S(b+2) ready       ", med(sr[b + 2] - qk[b + 2]))
-print("  PV(b) complete -> S(b+2) ready       ", med(sr[b + 2] - pvd[b]))
-print("  P(b) written -> S(b+1) ready         ", med(sr[b + 1] - pd[b]))
-print("  period S(b) -> S(b+1)                ", med(sr[b + 1] - sr[b]))
-kf, vf, top = t[1], t[5], t[7]
-print("  PV(b) issued -> MMA at QK(b+2)       ", med(top[b + 2] - pv[b]))
-print("  MMA at QK(b+2) -> K(b+2) present     ", med(kf[b + 2] - top[b + 2]))
-print("  K(b+2) present -> QK(b+2) issued     ", med(qk[b + 2] - kf[b + 2]))
-print("  MMA sees P(b) -> V(b) present        ", med(vf[b] - ms[b]))
-lt, vg = t[9], t[11]
-print("  P(b) written -> loop top (b+1)       ", med(lt[b + 1] - pd[b]))
-print("  loop top -> visit entry (b+1)        ", med(vg[b + 1] - lt[b + 1]))
-print("  visit entry -> S(b+1) passed         ", med(sr[b + 1] - vg[b + 1]))
-print("  QK(b+1) issued -> PV(b) complete (>0: QK done before)", med(pvd[b] - qk[b + 1]))
+
+def record(n):
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+
+    import bench
+    from paper_2510_21270_b200 import ops
+    q, k, v = bench.make_inputs(torch, n, 0, 32, list(range(8)), "cuda")
+    cfg = ops.make_config(block_size=128, segment_size=256, tau=0.9, strategy="key_permute")
+    path = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "attn_trace.bin")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    for _ in range(2):
+        ops.pbs_attention(q, k, v, cfg, report=False)
+    torch.cuda.synchronize()
+    os.environ["PBS_ATTN_TRACE"] = path
+    ops.pbs_attention(q, k, v, cfg, report=False)
+    torch.cuda.synchronize()
+    return path
+
+
+if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--analyse":
+        analyse(sys.argv[2])
+    else:
+        analyse(record(int(sys.argv[1]) if len(sys.argv) > 1 else 131072))
