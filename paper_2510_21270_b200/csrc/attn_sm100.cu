@@ -444,6 +444,22 @@ __device__ __forceinline__ void trace_event(const KernelArgs& a, int kind, uint3
 #endif
 }
 
+// Span accounting (-DPBS_ATTN_SPANS, debug): every CTA sums the clock64 time
+// its MMA warp and one thread per softmax group spend in each pipeline phase
+// and adds the totals into a.trace[0..32) at exit; no per-event stores, so the
+// timings are those of the product build.
+#ifdef PBS_ATTN_SPANS
+#define SPAN_DECL unsigned long long sp_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long sp_t_ = clock64();
+#define SPAN(i) do { const long long n_ = clock64(); sp_[i] += (unsigned long long)(n_ - sp_t_); sp_t_ = n_; } while (0)
+#define SPAN_COUNT(i) (++sp_[i])
+#define SPAN_FLUSH(cond, base) do { if ((cond) && a.trace) for (int i_ = 0; i_ < 8; ++i_) atomicAdd(a.trace + (base) + i_, sp_[i_]); } while (0)
+#else
+#define SPAN_DECL
+#define SPAN(i) do { } while (0)
+#define SPAN_COUNT(i) do { } while (0)
+#define SPAN_FLUSH(cond, base) do { } while (0)
+#endif
+
 struct Item {
   int h;
   int64_t qb;
@@ -754,11 +770,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
     uint32_t q_it = 0, k_it = 0, v_it = 0, o_no = 0, p_cnt[kGroups] = {0, 0}, gbase = 0;
+    SPAN_DECL
     auto issue_qk = [&](int e, int len) {
       const int w = e & 1;
       const uint32_t stage = k_it % kKStages;
       if (lane == 0) trace_event(a, 10, gbase + e);
       mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
+      SPAN(5);
       if (lane == 0) trace_event(a, 12, gbase + e);
       tc_fence_after();
       const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
@@ -768,6 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_commit_w(&bar->k_empty[stage]);
       if (e + 1 == len) tc_commit_w(&bar->q_empty);  // every QK of the item issued: Q is free once they complete
       if (lane == 0) trace_event(a, 2, gbase + e);
+      SPAN(6);
       ++k_it;
     };
     ItemStream items;
@@ -776,6 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
       mbar_wait(&bar->q_full, q_it & 1);
       ++q_it;
+      SPAN(7);
       if (len == 0) {
         tc_commit_w(&bar->q_empty);
         continue;
@@ -788,14 +808,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
         if (lane == 0) trace_event(a, 11, gbase + e);
         if (e == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // the previous epilogue read O_0 and O_1
+        SPAN(0);
+        SPAN_COUNT(4);
         // A = P [128 q x 128 kv] in TMEM (64 columns over S_w); B = V [128 kv x 128 d] MN-major SW128.
         // Keys 0..63 go as soon as the group wrote them, keys 64..127 after the rest.
         static_assert(kBN == 128, "two 64-key PV halves");
         const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
         mbar_wait(&bar->p_half[w], p_cnt[w] & 1);
+        SPAN(1);
         tc_fence_after();
         tc_mma_pv4(tmem + col_o(w), tmem + col_s(w), sdesc(v_base, kPanelBytes, 1024), idesc_pv, e < kGroups ? 0u : 1u);
+        SPAN(2);
         mbar_wait(&bar->p_full[w], p_cnt[w] & 1);
+        SPAN(1);
         if (lane == 0) trace_event(a, 0, gbase + e);
         ++p_cnt[w];
         tc_fence_after();
@@ -803,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit_w(&bar->v_empty[stage]);
         if (e + 1 == len) tc_commit_w(&bar->o_full);
         if (lane == 0) trace_event(a, 1, gbase + e);
+        SPAN(3);
         ++v_it;
         if (e + kGroups < len) issue_qk(e + kGroups, len);
       }
@@ -812,6 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // nothing may still write TMEM when it is released
     tc_commit_w(&bar->drained);
     mbar_wait(&bar->drained, 0);
+    SPAN_FLUSH(lane == 0, 0);
    } else {
     // ===================== scheduler: claim items in order, publish them =========
     if (lane == 0) {
@@ -845,6 +872,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
     uint32_t s_cnt = 0, o_cnt = 0, gbase = 0;  // gbase: blocks of earlier items (trace numbering)
     const bool tr = (row == 0);
+    SPAN_DECL
     ItemStream items;
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
@@ -867,7 +895,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1 + w, 128);
         }
         if (tr) trace_event(a, 7, gbase + e);
+        SPAN(0);
         mbar_wait(&bar->s_full[w], s_cnt & 1);
+        SPAN(1);
+        SPAN_COUNT(7);
         if (tr) trace_event(a, 4, gbase + e);
         ++s_cnt;
         tc_fence_after();
@@ -889,6 +920,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1 + w, 128);  // ko may be refilled after this
         }
         const float hmax = load_scores<false>(tS, ko, qo, r);
+        SPAN(2);
         if (tr) trace_event(a, 5, gbase + e);
         // online softmax (absorb, attention.hpp:96-126) in the log2 domain with
         // lazy rescaling: O_w is rescaled only when the max grows by more than 8
@@ -916,12 +948,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             TMEM_ST32(tO + c * 32, o);
           }
         }
+        SPAN(3);
         const float rs = emit_p<kPolyPer16>(r, sc, neg_m, tS, &bar->p_half[w]);
         l = l * factor + rs;
         tmem_wait_st();
         tc_fence_before();
         if (tr) trace_event(a, 6, gbase + e);
         mbar_arrive(&bar->p_full[w]);
+        SPAN(4);
       }
       gbase += vis.len;
       // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138): merge
@@ -986,7 +1020,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bar->o_free);
+      SPAN(5);
     }
+    SPAN(6);
+    SPAN_FLUSH(row == 0, 16 + 8 * w);
   }
   tc_fence_before();
   __syncthreads();

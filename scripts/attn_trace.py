@@ -10,6 +10,10 @@ indexed by the CTA-cumulative visited block g (group g % 2 within an item):
 
     python scripts/attn_trace.py [N]          # record and analyse
     python scripts/attn_trace.py --analyse F  # analyse a recorded dump
+
+A -DPBS_ATTN_SPANS build instead sums, over every CTA, the clock64 time the
+MMA warp and one thread per softmax group spend in each phase (no per-event
+stores, so the product's timing); `--spans F` prints the per-block averages.
 """
 import os
 import sys
@@ -41,6 +45,28 @@ def analyse(path):
     print("  P(g) written -> S(g+2) ready           ", med(sr[g + 2] - pd[g]))
 
 
+MMA_SPANS = ["wait V (+ O free)", "wait P half/full", "PV keys 0-63 issue", "PV keys 64-127 issue + commits",
+             None, "wait K", "QK issue + commits", "item fetch + wait Q"]
+SM_SPANS = ["visit / item", "wait S", "mask + load + max", "rescale", "exp + P store + arrive", "epilogue", "tail"]
+
+
+def spans(path):
+    t = np.fromfile(path, dtype=np.uint64)[:32].astype(np.float64)
+    nb = t[4]
+    print(f"MMA warp, per block ({nb:.0f} blocks over all CTAs), SM cycles:")
+    for i, name in enumerate(MMA_SPANS):
+        if name:
+            print(f"  {name:34s} {t[i] / nb:8.0f}")
+    print(f"  {'total':34s} {sum(t[i] for i in range(8) if MMA_SPANS[i]) / nb:8.0f}")
+    for w in range(2):
+        b = 16 + 8 * w
+        n = t[b + 7]
+        print(f"softmax group {w}, per own block ({n:.0f}):")
+        for i, name in enumerate(SM_SPANS):
+            print(f"  {name:34s} {t[b + i] / n:8.0f}")
+        print(f"  {'total':34s} {sum(t[b + i] for i in range(7)) / n:8.0f}")
+
+
 def record(n):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -63,5 +89,7 @@ def record(n):
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[1] == "--analyse":
         analyse(sys.argv[2])
+    elif len(sys.argv) > 1 and sys.argv[1] == "--spans":
+        spans(sys.argv[2] if len(sys.argv) > 2 else record(131072))
     else:
         analyse(record(int(sys.argv[1]) if len(sys.argv) > 1 else 131072))
