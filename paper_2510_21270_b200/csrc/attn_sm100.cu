@@ -58,8 +58,12 @@ namespace {
 constexpr int kBM = 128;      // query rows per tile (= block size B)
 constexpr int kBN = 128;      // keys per tile (= block size B)
 constexpr int kD = 128;       // head dim
-constexpr int kKStages = 3;   // K ring depth (freed as soon as QK^T completes)
-constexpr int kVStages = 2;   // V ring depth (freed when PV completes)
+#ifndef PBS_ATTN_K_STAGES
+#define PBS_ATTN_K_STAGES 3
+#define PBS_ATTN_V_STAGES 2
+#endif
+constexpr int kKStages = PBS_ATTN_K_STAGES;  // K ring depth (freed as soon as QK^T completes)
+constexpr int kVStages = PBS_ATTN_V_STAGES;  // V ring depth (freed when PV completes)
 // Two softmax warpgroups take alternate visited blocks of an item (split-KV
 // inside the CTA): each thread owns one query row (one TMEM lane) and all 128
 // keys of its warpgroup's blocks, with its own running max, sum and O
