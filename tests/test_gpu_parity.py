@@ -165,6 +165,31 @@ def test_pipeline_matches_oracle(ops, oracle, strategy, hq, hkv, n, d, b, s, tau
     assert res.report["selected_blocks"] == sel
 
 
+@pytest.mark.parametrize("strategy", ["key_permute", "none", "query_permute"])
+@pytest.mark.parametrize("n", [1, 100, 128, 129, 383])
+def test_pipeline_tiny_and_ragged_lengths(ops, oracle, strategy, n):
+    """Sequence lengths at and around one block on the tcgen05 path (d = 128,
+    B = 128, bf16): a single key, a partial only block, exactly one block, one
+    key past it, a segment plus a ragged block."""
+    from oracle import make_config as ocfg
+
+    rng = np.random.default_rng(n)
+    hq, hkv, d, b, s, tau = 2, 1, 128, 128, 256, 0.9
+    tq, tk, tv, q, k, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0)
+    if strategy == "none":
+        s = 0
+    res = ops.pbs_attention(tq, tk, tv, ops.make_config(block_size=b, segment_size=s, tau=tau, strategy=strategy))
+    out = res.output.float().cpu().numpy()
+    assert np.isfinite(out).all()
+    for h in range(hq):
+        r = oracle.pbs_attention(q[h], k[0], v[0], ocfg(block_size=b, segment_size=s, tau=tau, strategy=strategy))
+        np.testing.assert_array_equal(res.pi[h].cpu().numpy(), r.pi)
+        np.testing.assert_array_equal(res.sigma[h].cpu().numpy(), r.sigma)
+        np.testing.assert_array_equal(res.mask[h].cpu().numpy(), r.mask)
+        err = np.abs(out[h] - r.output)
+        assert err.max() <= BF16_MAX and err.mean() <= BF16_MEAN, (h, err.max(), err.mean())
+
+
 @pytest.mark.parametrize("d,dtype", [(128, torch.bfloat16), (64, torch.float32), (20, torch.bfloat16)])
 def test_unpermute_inverts_the_gather(ops, d, dtype):
     """pbs_unpermute (pipeline.hpp:178-180): out[sigma[i]] = src[i] == apply_rows(sigma^-1, src)."""
