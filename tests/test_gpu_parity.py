@@ -246,6 +246,27 @@ def test_pipeline_top_k_matches_oracle(ops, oracle, k):
         assert (mask[h].sum(1) <= k + 1 + s // b).all()
 
 
+@pytest.mark.parametrize("tau,top_k", [(0.0, 0), (0.9, 1000), (0.9, 1)])
+def test_selection_extremes_match_oracle(ops, oracle, tau, top_k):
+    """tau = 0 (forced blocks only), top_k beyond every row's admissible count
+    (everything admissible) and top_k = 1, through the whole pipeline."""
+    from oracle import make_config as ocfg
+
+    rng = np.random.default_rng(13)
+    hq, hkv, n, d, b, s = 2, 1, 2048 + 77, 128, 128, 256
+    tq, tk, tv, q, kk, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0, block=b)
+    res = ops.pbs_attention(tq, tk, tv, ops.make_config(block_size=b, segment_size=s, tau=tau, top_k=top_k))
+    out, pi, mask = res.output.float().cpu().numpy(), res.pi.cpu().numpy(), res.mask.cpu().numpy()
+    for h in range(hq):
+        r = oracle.pbs_attention(q[h], kk[0], v[0], ocfg(block_size=b, segment_size=s, tau=tau, top_k=top_k))
+        np.testing.assert_array_equal(pi[h], r.pi)
+        np.testing.assert_array_equal(mask[h], r.mask)
+        err = np.abs(out[h] - r.output)
+        assert err.max() <= BF16_MAX and err.mean() <= BF16_MEAN, (h, err.max(), err.mean())
+    if top_k >= 1000:
+        assert res.report["selected_blocks"] == res.report["total_admissible_blocks"]
+
+
 @pytest.mark.parametrize("kind", ["vertical_lines", "mixed", "gaussian"])
 def test_reference_fixtures_f32(ops, kind):
     """The committed reference runs (oracle/gen_golden.py) through the f32 device path."""
