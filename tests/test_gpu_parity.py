@@ -165,7 +165,7 @@ def test_pipeline_matches_oracle(ops, oracle, strategy, hq, hkv, n, d, b, s, tau
     assert res.report["selected_blocks"] == sel
 
 
-@pytest.mark.parametrize("strategy", ["key_permute", "none", "query_permute"])
+@pytest.mark.parametrize("strategy", ["key_permute", "none", "query_permute", "both"])
 @pytest.mark.parametrize("n", [1, 100, 128, 129, 383])
 def test_pipeline_tiny_and_ragged_lengths(ops, oracle, strategy, n):
     """Sequence lengths at and around one block on the tcgen05 path (d = 128,
