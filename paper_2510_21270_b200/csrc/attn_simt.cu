@@ -123,6 +123,16 @@ int launch_attention_simt(const AttnParams& p, cudaStream_t st) {
   if (t == 0) return PBS_OK;
   const int subtiles = (int)ceil_div(p.block, kRows);
   const size_t smem = (size_t)2 * kKeys * p.d * 4 + kKeys * 4;
+  // head dims above 192 need more than the 48 KB default (d = 256: 64 KB + 128 B)
+  static DeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, [] {
+        const int most = (int)((size_t)2 * kKeys * 64 * kLanes * 4 + kKeys * 4);
+        PBS_CUDA_CHECK(cudaFuncSetAttribute(attn_simt_kernel<__nv_bfloat16>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, most));
+        PBS_CUDA_CHECK(cudaFuncSetAttribute(attn_simt_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, most));
+        return (int)PBS_OK;
+      }))
+    return rc;
   dim3 grid((unsigned)(t * subtiles), (unsigned)p.hq);
   if (p.dtype == PBS_DTYPE_BF16)
     attn_simt_kernel<__nv_bfloat16><<<grid, kRows * kLanes, smem, st>>>(p, t, subtiles);

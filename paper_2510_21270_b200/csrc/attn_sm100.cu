@@ -1117,30 +1117,38 @@ int make_map(CUtensorMap* map, const void* base, int heads, int64_t n) {
   return PBS_OK;
 }
 
-int g_num_sms = 0;
-
 // Library-owned scratch for calls that pass none (the block-sparse / dense C-ABI
 // entries): one grow-only device buffer per stream, so back-to-back calls never
 // go through the allocator (a stream-ordered malloc/free per call showed up as
 // occasional 10-30 ms stalls when the pool returned memory to the driver).
 // Work on one stream is ordered, so the buffer is reused safely by that stream.
 void* stream_scratch(cudaStream_t st, size_t bytes) {
+  struct Entry {
+    int device;
+    cudaStream_t stream;
+    void* ptr;
+    size_t bytes;
+  };
   static std::mutex mu;
-  static std::vector<std::pair<cudaStream_t, std::pair<void*, size_t>>> cache;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
+  // keyed by (device, stream): the legacy default stream (handle 0) exists once per device
   for (auto& e : cache) {
-    if (e.first != st) continue;
-    if (e.second.second >= bytes) return e.second.first;
+    if (e.device != dev || e.stream != st) continue;
+    if (e.bytes >= bytes) return e.ptr;
     cudaStreamSynchronize(st);  // the old buffer may still be in use by this stream
-    cudaFree(e.second.first);
-    void* p = nullptr;
-    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-    e.second = {p, bytes};
-    return p;
+    cudaFree(e.ptr);
+    e.ptr = nullptr;
+    e.bytes = 0;
+    if (cudaMalloc(&e.ptr, bytes) != cudaSuccess) return nullptr;
+    e.bytes = bytes;
+    return e.ptr;
   }
   void* p = nullptr;
   if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-  cache.push_back({st, {p, bytes}});
+  cache.push_back({dev, st, p, bytes});
   return p;
 }
 
@@ -1235,15 +1243,14 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
     a.vis = vis;
     a.nvis = nvis;
   }
-  static std::atomic<uint64_t> attr_seen{0};
-  if (first_use_on_device(attr_seen)) {
-    PBS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        SmemLayout::total));
-    int dev = 0;
-    PBS_CUDA_CHECK(cudaGetDevice(&dev));
-    PBS_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  int grid = (int)min64(a.items, g_num_sms);
+  static DeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, [] {
+        PBS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            SmemLayout::total));
+        return (int)PBS_OK;
+      }))
+    return rc;
+  int grid = (int)min64(a.items, num_sms());
   if (const char* e = getenv("PBS_ATTN_GRID")) grid = (int)min64(grid, atoi(e) > 0 ? atoi(e) : grid);  // debug
   const char* trace_path = getenv("PBS_ATTN_TRACE");
   if (trace_path) {

@@ -27,6 +27,17 @@ std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int num_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) return 148;
+  cache[dev].store(v, std::memory_order_relaxed);
+  return v;
+}
+
 void set_error(const char* prefix, const std::string& msg) { g_err = std::string(prefix) + ": " + msg; }
 
 int fail(int code, const char* prefix, const std::string& msg) {
@@ -646,8 +657,13 @@ int pbs_attention(const void* q, const void* k, const void* v, const pbs_shape* 
 // H2D of group g+1 and D2H of group g-1 overlap the compute of group g.  Heads
 // share nothing, so the result is identical to one whole call.
 namespace {
+// One arena = device memory for two group slots (+ the estimate-first
+// buffers), three streams and their events, on one device.  Calls check an
+// arena out of a per-process pool and return it when they finish, so
+// concurrent host callers (one per thread, like pbs_main.cpp:99-122's head
+// fan-out) each get their own arena and never serialise on each other; a
+// sequential caller reuses the same arena call after call.
 struct Arena {
-  std::mutex mu;
   void* ptr = nullptr;
   size_t bytes = 0;
   int device = -1;
@@ -661,7 +677,44 @@ struct Arena {
   char* pinned = nullptr;
   size_t pinned_bytes = 0;
 };
-Arena g_arena;
+
+struct ArenaPool {
+  std::mutex mu;
+  std::vector<Arena*> idle;
+};
+ArenaPool g_pool;
+
+// an idle arena of the current device (streams and events are per device), or a new one
+Arena* arena_acquire(int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool.mu);
+    for (size_t i = 0; i < g_pool.idle.size(); ++i) {
+      if (g_pool.idle[i]->device != dev) continue;
+      Arena* a = g_pool.idle[i];
+      g_pool.idle.erase(g_pool.idle.begin() + (long)i);
+      return a;
+    }
+  }
+  Arena* a = new Arena();
+  a->device = dev;
+  return a;
+}
+
+void arena_release(Arena* a) {
+  std::lock_guard<std::mutex> lk(g_pool.mu);
+  g_pool.idle.push_back(a);
+}
+
+struct ArenaLease {
+  Arena* a;
+  explicit ArenaLease(int dev) : a(arena_acquire(dev)) {}
+  ~ArenaLease() {
+    // an early error return may leave copies in flight on the arena's streams
+    for (auto s : a->st)
+      if (s) cudaStreamSynchronize(s);
+    arena_release(a);
+  }
+};
 
 int arena_streams(Arena& A) {
   if (A.st[0]) return PBS_OK;
@@ -703,16 +756,10 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   const size_t kall_b = (size_t)hkv * kvb, qtail_b = (size_t)hq * take * d * es;
   const size_t imp_b = importance_workspace_bytes((int)hq, n, cfg->block_size);
   const size_t est_bytes = est_first ? al(kall_b) + al(qtail_b) + al(imp_b) + 3 * al((size_t)hq * n * 4) : 0;
-  std::lock_guard<std::mutex> lk(g_arena.mu);
-  Arena& A = g_arena;
   int dev = 0;
   PBS_CUDA_CHECK(cudaGetDevice(&dev));
-  if (A.device != dev) {  // streams and events belong to the device they were made on
-    A.st[0] = A.st[1] = A.st[2] = nullptr;
-    if (A.ptr) cudaFree(A.ptr);
-    A.ptr = nullptr;
-    A.bytes = 0;
-  }
+  ArenaLease lease(dev);
+  Arena& A = *lease.a;
   if (int rc = arena_streams(A)) return rc;
   if (A.bytes < slot * nslots + est_bytes) {
     if (A.ptr) cudaFree(A.ptr);
@@ -721,7 +768,6 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     PBS_CUDA_CHECK(cudaMalloc(&A.ptr, slot * nslots + est_bytes));
     A.bytes = slot * nslots + est_bytes;
   }
-  A.device = dev;
   struct Slot {
     char *q, *k, *v, *out, *ws;
     int32_t *sig, *pi;

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <string>
 
 #include "../../include/pbs_cabi.h"
@@ -35,14 +36,30 @@ void count_launch();
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// true the first time a call site runs on the current device (function
-// attributes such as the dynamic shared-memory size are per device)
-inline bool first_use_on_device(std::atomic<uint64_t>& seen) {
+// Per-device one-time setup of a call site (function attributes such as the
+// dynamic shared-memory size are per device).  The device's bit is set only
+// after the setup succeeded, under a lock, so a second host thread never
+// launches before the attribute is in place and a failed setup is retried.
+struct DeviceOnce {
+  std::atomic<uint64_t> done{0};
+  std::mutex mu;
+};
+template <class F>
+int once_per_device(DeviceOnce& o, F&& setup) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  PBS_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return setup();
   const uint64_t bit = 1ull << dev;
-  return (seen.fetch_or(bit) & bit) == 0;
+  if (o.done.load(std::memory_order_acquire) & bit) return PBS_OK;
+  std::lock_guard<std::mutex> lk(o.mu);
+  if (o.done.load(std::memory_order_relaxed) & bit) return PBS_OK;
+  if (int rc = setup()) return rc;
+  o.done.fetch_or(bit, std::memory_order_release);
+  return PBS_OK;
 }
+
+// SM count of the current device (cached per device)
+int num_sms();
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }

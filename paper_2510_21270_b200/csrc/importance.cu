@@ -540,10 +540,13 @@ int launch_importance_logits(const void* q, const void* k, int dtype, int hq, in
     auto kk = static_cast<const __nv_bfloat16*>(k);
     if (vec && d % xgemm::kChunkW == 0) {
       auto kern = importance_logits_kernel<__nv_bfloat16, true, true, true>;
-      static std::atomic<uint64_t> attr_seen{0};
-      if (first_use_on_device(attr_seen))
-        PBS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)sizeof(xgemm::SmemWide)));
+      static DeviceOnce attr_once;
+      if (int rc = once_per_device(attr_once, [&] {
+            PBS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)sizeof(xgemm::SmemWide)));
+            return (int)PBS_OK;
+          }))
+        return rc;
       kern<<<grid, xgemm::kThreads, sizeof(xgemm::SmemWide), st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L,
                                                                    W.rowmax, h0);
     } else if (vec) importance_logits_kernel<__nv_bfloat16, true, true><<<grid, xgemm::kThreads, 0, st>>>(qq, kk, group, n, q_rows, d, take, scale, W.L, W.rowmax, h0);
@@ -568,9 +571,13 @@ int launch_importance_finish(int hq, int64_t n, int64_t block, float* scores, vo
   importance_exp_kernel<<<dim3((unsigned)ceil_div(n, kExpKeys), (unsigned)hq), 256, 0, st>>>(L, W.rowmax, take, n);
   PBS_LAUNCH_CHECK("importance_exp_kernel");
   const size_t smem = sizeof(float) * kRing * kJT * 32 + 2 * kRing * sizeof(uint64_t);
-  static std::atomic<uint64_t> attr_seen{0};
-  if (first_use_on_device(attr_seen))
-    PBS_CUDA_CHECK(cudaFuncSetAttribute(importance_denom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static DeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, [&] {
+        PBS_CUDA_CHECK(
+            cudaFuncSetAttribute(importance_denom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        return (int)PBS_OK;
+      }))
+    return rc;
   alignas(64) CUtensorMap tm_e;
   const bool tma = (take % 4 == 0) && (take % 32 == 0);  // every CTA's 32 rows are whole 16-byte pieces
   if (tma) {
@@ -612,6 +619,14 @@ int launch_segmented_sort(const void* keys, int key_kind, int heads, int64_t n, 
     while (pow2 < segment) pow2 <<= 1;
     const int threads = std::max(32, std::min(1024, pow2 / 2));
     const size_t smem = sizeof(unsigned long long) * pow2;
+    // segments of 4097..8192 keys need 64 KB of shared memory
+    static DeviceOnce attr_once;
+    if (int rc = once_per_device(attr_once, [] {
+          PBS_CUDA_CHECK(cudaFuncSetAttribute(segmented_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)(sizeof(unsigned long long) * 8192)));
+          return (int)PBS_OK;
+        }))
+      return rc;
     segmented_sort_kernel<<<dim3((unsigned)groups, (unsigned)heads), threads, smem, st>>>(
         keys, key_kind, n, (int)segment, pow2, perm, inv);
     PBS_LAUNCH_CHECK("segmented_sort_kernel");

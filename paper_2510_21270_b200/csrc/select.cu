@@ -356,9 +356,12 @@ static int launch_select_common(int mode, const float* rows_in, int hq, int64_t 
   if (t == 0 || hq == 0) return PBS_OK;
   if (t > 16384) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "block grid wider than 16384 blocks");
   const size_t smem = select_smem(t);
-  static std::atomic<uint64_t> attr_seen{0};
-  if (first_use_on_device(attr_seen))
-    PBS_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  static DeviceOnce attr_once;
+  if (int rc = once_per_device(attr_once, [] {
+        PBS_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        return (int)PBS_OK;
+      }))
+    return rc;
   select_kernel<<<dim3((unsigned)t, (unsigned)hq), kSelThreads, smem, st>>>(
       mode, rows_in, t, block, segment, tau, top_k, forced_first, forced_band, select, scores_out, mask, kv_idx,
       kv_cnt, row_cov);

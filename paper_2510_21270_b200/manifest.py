@@ -174,6 +174,12 @@ def run_manifest(m: RunManifest, base_dir=".") -> dict:
         raise _config_error(f"q/k/v head counts differ ({hc[0]}, {hc[1]}, {hc[2]})")
     if hc[0] == 0:
         raise _config_error("inputs hold no heads")
+    # pbs_attention's checks (pipeline.hpp:111-116), before any tensor is loaded
+    (qr, qc), (kr, kc), (vr, vc) = ((i["rows"], i["cols"]) for i in infos)
+    if qr != kr:
+        raise _config_error(f"pipeline expects self-attention: N == M, got {qr} vs {kr}")
+    if qc != kc or kr != vr or vc != kc:
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: pipeline inputs have inconsistent shapes")
     q, k, v = (ops.load_tensor(resolve(x), dtype=torch.bfloat16) for x in (m.q, m.k, m.v))
     from_stack = any(i["ndim"] == 3 for i in infos)
     q, k, v = (x if x.dim() == 3 else x.unsqueeze(0) for x in (q, k, v))

@@ -60,9 +60,26 @@ def _check_dev(*ts):
             raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: tensors must be contiguous CUDA tensors")
 
 
-def make_shape(q: torch.Tensor, k: torch.Tensor) -> Shape:
+def make_shape(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor | None = None) -> Shape:
+    """pbs_shape of [Hq, N, d] queries over [Hkv, N, d] keys (and values).
+    The C ABI carries one N and one d, so mismatched inputs are refused here
+    with the reference's texts (pipeline.hpp:111-116) before any kernel could
+    read past a shorter tensor."""
+    for name, x in (("Q", q), ("K", k), ("V", v)):
+        if x is not None and x.dim() != 3:
+            raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, f"E_SHAPE: {name} must be a [heads, rows, cols] stack")
+    if q.dtype != k.dtype or (v is not None and v.dtype != k.dtype):
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_CONFIG: Q, K and V must share one dtype")
     hq, n, d = q.shape
     hkv = k.shape[0]
+    if k.shape[1] != n:
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG,
+                               f"E_CONFIG: pipeline expects self-attention: N == M, got {n} vs {k.shape[1]}")
+    if k.shape[2] != d or (v is not None and tuple(v.shape) != tuple(k.shape)):
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: pipeline inputs have inconsistent shapes")
+    if hkv <= 0 or hq % hkv != 0:
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG,
+                               "E_SHAPE: num_q_heads must be a positive multiple of num_kv_heads")
     return Shape(_dtype_code(q), hq, hkv, d, n)
 
 
@@ -184,7 +201,7 @@ def attention_block_sparse(qp, kp, vp, block_size, kv_idx, kv_cnt, q_orig=None, 
     `out` / `status` (int32 [2]) may be preallocated: the call then allocates
     nothing and never synchronises (check_status=False)."""
     _check_dev(qp, kp, vp, kv_idx, kv_cnt, q_orig, k_orig, out_rows)
-    shape = make_shape(qp, kp)
+    shape = make_shape(qp, kp, vp)
     out = torch.empty_like(qp) if out is None else out
     if status is None:
         status = torch.empty(2, dtype=torch.int32, device=qp.device)
@@ -202,7 +219,7 @@ def attention_block_sparse(qp, kp, vp, block_size, kv_idx, kv_cnt, q_orig=None, 
 def dense_causal_attention(q, k, v, scale=0.0, out=None):
     """The project's dense causal FlashAttention (GQA: kv head h // G)."""
     _check_dev(q, k, v)
-    shape = make_shape(q, k)
+    shape = make_shape(q, k, v)
     out = torch.empty_like(q) if out is None else out
     check(lib().pbs_dense_causal_attention_fwd(_ptr(q), _ptr(k), _ptr(v), C.byref(shape), scale, _ptr(out),
                                                _stream()))
@@ -233,7 +250,7 @@ def pbs_attention(q, k, v, cfg: PipelineConfig | None = None, report=True, out=N
     report=False it is fully stream-ordered (graph-capturable)."""
     cfg = cfg or make_config()
     _check_dev(q, k, v)
-    shape = make_shape(q, k)
+    shape = make_shape(q, k, v)
     hq, n, d = q.shape
     t = -(-n // max(int(cfg.block_size), 1))
     need = lib().pbs_workspace_size(C.byref(shape), C.byref(cfg))
@@ -260,7 +277,7 @@ def pbs_attention_host(q, k, v, cfg: PipelineConfig | None = None, return_perms=
     for x in (q, k, v):
         if x.is_cuda or not x.is_contiguous():
             raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: host tensors must be contiguous CPU tensors")
-    shape = make_shape(q, k)
+    shape = make_shape(q, k, v)
     hq, n, d = q.shape
     t = -(-n // max(int(cfg.block_size), 1))
     out = torch.empty_like(q) if out is None else out

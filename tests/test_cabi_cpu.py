@@ -117,3 +117,25 @@ def test_cpp_dropin_compiles_and_links(lib, tmp_path):
     if not torch.cuda.is_available():
         r = subprocess.run([str(exe), "256", "64"], capture_output=True, text=True)
         assert r.returncode == 1 and r.stderr.startswith("E_CUDA:") and r.stderr.count("\n") == 1
+
+
+def test_ops_refuse_mismatched_inputs():
+    """ops.make_shape: K/V must match Q's N and d (the ABI carries one of each),
+    with the reference's error texts (pipeline.hpp:111-116)."""
+    import torch
+
+    from paper_2510_21270_b200 import _lib, ops
+
+    q = torch.zeros(4, 256, 64, dtype=torch.bfloat16)
+    k = torch.zeros(2, 256, 64, dtype=torch.bfloat16)
+    assert ops.make_shape(q, k, k).seq_len == 256
+    with pytest.raises(_lib.ConfigError, match="E_CONFIG: pipeline expects self-attention: N == M, got 256 vs 128"):
+        ops.make_shape(q, torch.zeros(2, 128, 64, dtype=torch.bfloat16))
+    with pytest.raises(_lib.ConfigError, match="E_SHAPE: pipeline inputs have inconsistent shapes"):
+        ops.make_shape(q, torch.zeros(2, 256, 32, dtype=torch.bfloat16))
+    with pytest.raises(_lib.ConfigError, match="E_SHAPE: pipeline inputs have inconsistent shapes"):
+        ops.make_shape(q, k, torch.zeros(2, 200, 64, dtype=torch.bfloat16))
+    with pytest.raises(_lib.ConfigError, match="E_SHAPE: num_q_heads"):
+        ops.make_shape(q, torch.zeros(3, 256, 64, dtype=torch.bfloat16))
+    with pytest.raises(_lib.ConfigError, match="E_CONFIG: Q, K and V must share one dtype"):
+        ops.make_shape(q, k.float())
