@@ -142,11 +142,13 @@ _SIGS = {
 }
 
 
-def load(path: str = LIB_PATH):
-    """Load libpbs_b200.so (raises if it is missing: there is no CPU fallback)."""
+def load(path: str | None = None):
+    """Load libpbs_b200.so (raises if it is missing: there is no CPU fallback).
+    PBS_B200_LIB names another build of the same library (A/B timing only)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PBS_B200_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing; build it with `python -m paper_2510_21270_b200.build` "
                           "(the PBS-Attn path has no CPU fallback)")

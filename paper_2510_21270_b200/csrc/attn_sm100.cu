@@ -7,41 +7,45 @@
 // in the list of key blocks a query block visits.
 //
 // Tile: B = 128 query rows x 128 keys, d = 128, bf16 in, fp32 accumulate.
-// Persistent CTAs (one per SM) take (head, query-block) work items from a
-// global counter (warp 3 publishes them through an mbarrier ring), ordered one
-// KV source at a time for L2 locality, heaviest query blocks first.
+// Work item: a PAIR of query tiles of one head, query blocks 2p and 2p + 1
+// (under B = 128, S = 256 the two blocks of one segment).  The CTA streams the
+// union of the two tiles' visited key blocks once through shared memory and
+// each K/V tile feeds both query tiles, so the K/V bytes moved per tensor-core
+// FLOP halve against one tile per item (the L2 -> SM traffic was the MMA
+// warp's main wait).  Persistent CTAs (one per SM) take items from a global
+// counter (warp 3 publishes them through an mbarrier ring), ordered one KV
+// source at a time for L2 locality, heaviest pairs first.
 // Warp roles (384 threads; setmaxnreg gives the softmax 208 registers):
-//   warp 0       TMA producer for Q (once per item) and K (3-stage ring)
-//   warp 2       TMA producer for V (2-stage ring)
+//   warp 0       TMA producer for Q_0, Q_1 (once per item) and K (ring)
+//   warp 2       TMA producer for V (ring)
 //                (cp.async.bulk.tensor through 3-D [H, N, d] maps, SW128)
 //   warp 3       item scheduler
-//   warp 1       TMEM owner + MMA issuer (warp-collective, one elected lane):
-//                  S_w = Q K_e^T        (SS: Q, K K-major in smem), w = e & 1
-//                  O_w (+)= P_e V_e     (TS: P over S_w in TMEM, V MN-major)
-//                per item S_0, S_1, then per block e: PV(e), QK(e + 2); the
-//                PV of keys 0-63 starts when the group signals that half of P
-//                (p_half), the rest at p_full
-//   warps 4..7   softmax group 0: the item's visited blocks e = 0, 2, 4, ...
-//   warps 8..11  softmax group 1: blocks e = 1, 3, 5, ...
+//   warp 1       TMEM owner + MMA issuer (warp-collective, one elected lane).
+//                Per union entry u, for tile w = 0 then 1:
+//                  O_w (+)= P_w(u-1) V_{u-1}  (TS: P over S_w in TMEM, V MN-major)
+//                  S_w = Q_w K_u^T            (SS: Q_w, K K-major in smem)
+//                each only where tile w visits the block; the PV of keys 0-63
+//                starts when the group signals that half of P (p_half).
+//   warps 4..7   softmax group 0: query tile 0 (block 2p)
+//   warps 8..11  softmax group 1: query tile 1 (block 2p + 1)
 // TMEM holds S_0 | S_1 | O_0 | O_1.  A softmax thread owns one query row (one
-// TMEM lane) and all 128 keys of its group's blocks, with the group's own
-// running max, sum and accumulator (split-KV inside the CTA): no exchange
-// between threads per block, and the two warps of an SM sub-partition work on
-// different blocks, so one's exponentials overlap the other's loads.  Per
-// block: 4 x tcgen05.ld 32x32b.x32 (partial blocks masked in TMEM first), row
-// max (3-input FMNMX), online softmax in the exp2 domain with lazy rescaling
-// (O_w rescaled only when the max grows by more than 8), p = 2^(s c - m) on the
-// MUFU written back over S_w as bf16 (tcgen05.st), then p_full.  The epilogue
-// merges the two groups' (m, l, O) once per item and writes O / l straight to
-// row out_rows[i] (the fused un-permute, pipeline.hpp:178).
+// TMEM lane) and all 128 keys of each block its tile visits, with its own
+// running max, sum and accumulator; the two warps of an SM sub-partition
+// belong to different tiles, so one's exponentials overlap the other's loads.
+// Per block: 4 x tcgen05.ld 32x32b.x32 (partial blocks masked in TMEM first),
+// row max (3-input FMNMX), online softmax in the exp2 domain with lazy
+// rescaling (O_w rescaled only when the max grows by more than 8),
+// p = 2^(s c - m) on the MUFU written back over S_w as bf16 (tcgen05.st), then
+// p_full.  The epilogue writes O_w / l straight to row out_rows[i] (the fused
+// un-permute, pipeline.hpp:178); the tiles finish independently (no merge).
 // Block classes follow AdmissibilityIndex::classify (attention.hpp:167-174):
 // per-block [min, max] of original positions; `none` blocks are skipped by
 // every role (an exact no-op, attention.hpp:286), `full` blocks skip the
 // per-element test, `partial` ones compare k_orig[j] <= q_orig[i].  A small
-// pre-pass (visit_kernel) writes, per (head, query block), the compacted list
-// of visited key blocks with the class packed in; every role prefetches it 32
-// entries at a time and broadcasts entries by warp shuffle, so the hot loop
-// has no dependent global loads.
+// pre-pass (visit_pair_kernel) writes, per item, the ascending union of the
+// two tiles' visited key blocks with both tiles' classes packed in; every
+// role prefetches it 32 entries at a time and broadcasts entries by warp
+// shuffle, so the hot loop has no dependent global loads.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -59,26 +63,25 @@ constexpr int kBM = 128;      // query rows per tile (= block size B)
 constexpr int kBN = 128;      // keys per tile (= block size B)
 constexpr int kD = 128;       // head dim
 #ifndef PBS_ATTN_K_STAGES
-#define PBS_ATTN_K_STAGES 3
+#define PBS_ATTN_K_STAGES 2
 #define PBS_ATTN_V_STAGES 2
 #endif
-constexpr int kKStages = PBS_ATTN_K_STAGES;  // K ring depth (freed as soon as QK^T completes)
-constexpr int kVStages = PBS_ATTN_V_STAGES;  // V ring depth (freed when PV completes)
-// Two softmax warpgroups take alternate visited blocks of an item (split-KV
-// inside the CTA): each thread owns one query row (one TMEM lane) and all 128
-// keys of its warpgroup's blocks, with its own running max, sum and O
-// accumulator; the two states merge once per item in the epilogue.
-constexpr int kGroups = 2;
-constexpr int kCols = kBN;                        // key columns per softmax thread
+constexpr int kKStages = PBS_ATTN_K_STAGES;  // K ring depth (freed once both tiles' QK^T complete)
+constexpr int kVStages = PBS_ATTN_V_STAGES;  // V ring depth (freed once both tiles' PV complete)
+constexpr int kGroups = 2;                   // softmax warpgroups = query tiles per item
+constexpr int kCols = kBN;                   // key columns per softmax thread
 constexpr int kSoftmaxThreads = 128 * kGroups;
 constexpr int kThreads = 128 + kSoftmaxThreads;
 constexpr int kRegsControl = 72;                  // setmaxnreg: producers / MMA issuer / scheduler
 constexpr int kRegsSoftmax = 208;                 //             softmax warpgroups
 static_assert((168 - kRegsControl) * 128 >= (kRegsSoftmax - 168) * kSoftmaxThreads, "register file split");
 // keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the
-// MUFU; 0: with two groups on alternate blocks the MUFU keeps up (A/B on the box:
-// 0 / 2 / 4 of 16 -> 61 / 62 / 66 ms x GHz for the 128K attention)
-constexpr int kPolyPer16 = 0;
+// MUFU; 0: with two groups working on different tiles the MUFU keeps up
+// (round 1 A/B on the box: 0 / 2 / 4 of 16 -> 61 / 62 / 66 ms x GHz at 128K)
+#ifndef PBS_POLY_PER16
+#define PBS_POLY_PER16 0
+#endif
+constexpr int kPolyPer16 = PBS_POLY_PER16;
 constexpr int kItemRing = 4;
 constexpr int kItemConsumers = 3 + kSoftmaxThreads / 32;  // warps 0, 1, 2 and the softmax warps
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
@@ -86,31 +89,34 @@ constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
 constexpr uint32_t kTmemCols = 512;               // S0 | S1 | O0 | O1
 __host__ __device__ constexpr uint32_t col_s(int w) { return (uint32_t)w * 128u; }
 __host__ __device__ constexpr uint32_t col_o(int w) { return 256u + (uint32_t)w * 128u; }
+// union entry: kb | class of tile 0 << 26 | class of tile 1 << 28
+constexpr int kKbBits = 26;
+constexpr uint32_t kKbMask = (1u << kKbBits) - 1u;
 
 struct __align__(8) Barriers {
-  uint64_t q_full, q_empty;
+  uint64_t q_full[kGroups], q_empty[kGroups];
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
-  uint64_t s_full[kGroups];  // S_w = Q K^T complete (and every earlier MMA: the group's previous PV)
+  uint64_t s_full[kGroups];  // S_w = Q_w K^T complete (and every earlier MMA: tile w's previous PV)
   uint64_t p_half[kGroups];  // P_w's first 64 keys written (the PV of those keys may start)
   uint64_t p_full[kGroups];  // P_w written into TMEM over S_w by the group's 128 threads
-  uint64_t o_full, o_free;   // the item's last PV complete / both groups' epilogue read O
+  uint64_t o_full[kGroups];  // tile w's last PV of the item complete
+  uint64_t o_free[kGroups];  // group w's epilogue read O_w
   uint64_t drained;  // every tcgen05 operation of the MMA issuer complete (before dealloc)
   // dynamic work distribution: warp 3 claims items from a global counter and
   // publishes them through this ring to the 11 consumer warps
-  uint64_t item_full[4], item_empty[4];
-  int32_t item_ring[4];
+  uint64_t item_full[kItemRing], item_empty[kItemRing];
+  int32_t item_ring[kItemRing];
   uint32_t tmem_base;
 };
 
 struct SmemLayout {
   // 1024-byte aligned tiles (SW128 atoms)
-  static constexpr int q = 0;
-  static constexpr int k = q + kTileBytes;
+  static constexpr int q = 0;                              // Q_0 | Q_1
+  static constexpr int k = q + kGroups * kTileBytes;
   static constexpr int v = k + kKStages * kTileBytes;
   static constexpr int korig = v + kVStages * kTileBytes;  // int [kGroups][128]
-  static constexpr int xch = korig + kGroups * 128 * 4;    // float [2 items][kGroups][2 (m, l)][128]
-  static constexpr int bars = xch + 2 * kGroups * 2 * 128 * 4;
+  static constexpr int bars = korig + kGroups * 128 * 4;
   static constexpr int total = bars + sizeof(Barriers) + 1024;  // + alignment slack
 };
 static_assert(SmemLayout::total <= 232448, "shared memory budget");
@@ -165,39 +171,10 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
 // Warp-collective forms: the whole (converged) warp executes these and one
 // elected lane issues.  Keeping the issuing code warp-uniform lets the
 // descriptors live in uniform registers; a `lane == 0` branch instead makes the
 // compiler wrap every tcgen05.mma in a waterfall loop of R2UR conversions.
-__device__ __forceinline__ void tc_mma_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p, e;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                            uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p, e;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 __device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n"
@@ -260,77 +237,6 @@ __device__ __forceinline__ void tc_mma_pv4(uint32_t d_tmem, uint32_t a_tmem, uin
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// PV over 128 keys: 8 MMAs (K = 16 keys each) with A = P in TMEM (8 columns per
-// step) and B = V rows advancing 16 x 128 bytes (encoded +128) per step.
-__device__ __forceinline__ void tc_mma_pv8(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                           uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred e, t, p;\n"
-      ".reg .b32 a1, a2, a3, a4, a5, a6, a7;\n"
-      ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n"
-      "setp.ne.b32 t, 1, 0;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "add.s32 a1, %1, 8;   add.s64 b1, %2, 128;\n"
-      "add.s32 a2, %1, 16;  add.s64 b2, %2, 256;\n"
-      "add.s32 a3, %1, 24;  add.s64 b3, %2, 384;\n"
-      "add.s32 a4, %1, 32;  add.s64 b4, %2, 512;\n"
-      "add.s32 a5, %1, 40;  add.s64 b5, %2, 640;\n"
-      "add.s32 a6, %1, 48;  add.s64 b6, %2, 768;\n"
-      "add.s32 a7, %1, 56;  add.s64 b7, %2, 896;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, t;\n"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// TMEM[128 lanes x 8 columns] <- 128 rows x 256 bits of a shared-memory matrix
-// (same descriptor format as the MMA operands; executes in order with tcgen05.mma)
-__device__ __forceinline__ void tc_cp_w(uint32_t d_tmem, uint64_t sdesc_) {
-  asm volatile(
-      "{\n"
-      ".reg .pred e;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(sdesc_)
-      : "memory");
-}
-
-// D[tmem] (+)= A[smem] * B[smem]
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// D[tmem] (+)= A[tmem] * B[smem]  (A = P written back into TMEM)
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
@@ -416,6 +322,7 @@ __host__ __device__ constexpr uint32_t make_idesc(uint32_t a_mn_major, uint32_t 
 struct KernelArgs {
   int hq, kv_heads, group;
   int64_t n, t;
+  int64_t npairs;  // ceil(t / 2): items are (head, pair of query blocks 2p, 2p + 1)
   float scale_log2;
   const int32_t* kv_idx;
   const int32_t* kv_cnt;
@@ -428,25 +335,13 @@ struct KernelArgs {
   float* lse;  // [hq][n] in output-row order, or nullptr
   __nv_bfloat16* out;
   int causal;   // identity element mask when q_orig/k_orig are null
-  int dense;    // dense causal list (kb = 0..qb)
+  int dense;    // dense causal lists (kb = 0..qb)
   int64_t items;
-  const int32_t* vis;   // [hq][t][t] visited blocks (kb | cls << 30), sparse mode
-  const int32_t* nvis;  // [hq][t]
+  const int32_t* vis;   // [hq][npairs][t] union lists (kb | c0 << 26 | c1 << 28), sparse mode
+  const int32_t* nvis;  // [hq][npairs]
   int32_t* item_counter;  // zeroed before the launch; items are claimed in order (heaviest first)
-  unsigned long long* trace;  // debug timeline of CTA 0 (PBS_ATTN_TRACE), else nullptr
+  unsigned long long* trace;  // span sums (-DPBS_ATTN_SPANS with PBS_ATTN_TRACE), else nullptr
 };
-
-// debug timeline (PBS_ATTN_TRACE=file): CTA 0 records clock64 at pipeline events
-constexpr int kTraceEvents = 4096;
-// Compiled in only with -DPBS_ATTN_TRACE_EVENTS (PBS_NVCC_EXTRA at build time):
-// the checks cost issue slots in the hot loops.
-__device__ __forceinline__ void trace_event(const KernelArgs& a, int kind, uint32_t n) {
-#ifdef PBS_ATTN_TRACE_EVENTS
-  if (a.trace && blockIdx.x == 0 && n < kTraceEvents) a.trace[kind * kTraceEvents + n] = clock64();
-#else
-  (void)a, (void)kind, (void)n;
-#endif
-}
 
 // Span accounting (-DPBS_ATTN_SPANS, debug): every CTA sums the clock64 time
 // its MMA warp and one thread per softmax group spend in each pipeline phase
@@ -466,63 +361,51 @@ __device__ __forceinline__ void trace_event(const KernelArgs& a, int kind, uint3
 
 struct Item {
   int h;
-  int64_t qb;
+  int64_t p;  // query blocks 2p (tile 0) and 2p + 1 (tile 1, when < t)
 };
 
 __device__ __forceinline__ Item item_of(const KernelArgs& a, int64_t idx) {
   // L2 locality: all CTAs sweep one KV source at a time (per q head for the
-  // per-head permuted K'/V', per GQA group for shared K/V), heaviest query
-  // blocks first inside it.
+  // per-head permuted K'/V', per GQA group for shared K/V), heaviest pairs
+  // first inside it.
   Item it;
-  const int64_t per = a.t * (a.kv_heads == a.hq ? 1 : a.group);
+  const int64_t per = a.npairs * (a.kv_heads == a.hq ? 1 : a.group);
   const int64_t grp = idx / per, rem = idx % per;
   if (a.kv_heads == a.hq) {
     it.h = (int)grp;
-    it.qb = a.t - 1 - rem;
+    it.p = a.npairs - 1 - rem;
   } else {
     it.h = (int)(grp * a.group + rem % a.group);
-    it.qb = a.t - 1 - rem / a.group;
+    it.p = a.npairs - 1 - rem / a.group;
   }
   return it;
 }
 
-__device__ __forceinline__ int list_len(const KernelArgs& a, const Item& it) {
-  if (a.dense) return (int)(it.qb + 1);
-  return a.kv_cnt[(int64_t)it.h * a.t + it.qb];
-}
-
-__device__ __forceinline__ int64_t list_at(const KernelArgs& a, const Item& it, int e) {
-  if (a.dense) return e;
-  return a.kv_idx[((int64_t)it.h * a.t + it.qb) * a.t + e];
-}
-
-__device__ __forceinline__ int2 q_range(const KernelArgs& a, const Item& it) {
-  if (a.q_mm) return a.q_mm[(int64_t)it.h * a.t + it.qb];
-  const int64_t lo = it.qb * kBM;
+__device__ __forceinline__ int2 q_range(const KernelArgs& a, int h, int64_t qb) {
+  if (a.q_mm) return a.q_mm[(int64_t)h * a.t + qb];
+  const int64_t lo = qb * kBM;
   return make_int2((int)lo, (int)(min64(a.n, lo + kBM) - 1));
 }
-__device__ __forceinline__ int2 k_range(const KernelArgs& a, const Item& it, int64_t kb) {
-  if (a.k_mm) return a.k_mm[(int64_t)it.h * a.t + kb];
+__device__ __forceinline__ int2 k_range(const KernelArgs& a, int h, int64_t kb) {
+  if (a.k_mm) return a.k_mm[(int64_t)h * a.t + kb];
   const int64_t lo = kb * kBN;
   return make_int2((int)lo, (int)(min64(a.n, lo + kBN) - 1));
 }
 
 // 0 none, 1 partial, 2 full (AdmissibilityIndex::classify); a ragged key block is
 // treated as partial so that keys past N are masked.
-__device__ __forceinline__ int block_class(const KernelArgs& a, const Item& it, int64_t kb) {
+__device__ __forceinline__ int block_class(const KernelArgs& a, int h, int64_t qb, int64_t kb) {
   const bool masked = a.causal || a.q_orig || a.k_orig;
   const bool ragged = (kb + 1) * kBN > a.n;
   if (!masked) return ragged ? 1 : 2;
-  const int2 qr = q_range(a, it), kr = k_range(a, it, kb);
+  const int2 qr = q_range(a, h, qb), kr = k_range(a, h, kb);
   if (kr.y <= qr.x) return ragged ? 1 : 2;
   if (kr.x > qr.y) return 0;
   return 1;
 }
 
-
-// visited-block cursor: dense causal lists are computed, sparse lists come from
-// visited-block cursor: dense causal lists are computed, sparse lists come from
-// the pre-pass (vis[h][qb][e] = kb | cls << 30), prefetched 32 entries per warp.
+// visited-block cursor over an item's union list: dense causal lists are
+// computed, sparse lists come from the pre-pass, prefetched 32 entries per warp.
 struct Visit {
   const int32_t* list;
   int len;
@@ -536,21 +419,24 @@ __device__ __forceinline__ Visit visit_begin(const KernelArgs& a, const Item& it
   v.cache = 0;
   if (a.dense) {
     v.list = nullptr;
-    v.len = (int)(it.qb + 1);
+    v.len = (int)(min64(2 * it.p + 1, a.t - 1) + 1);  // 0 .. last query block of the pair
   } else {
-    v.list = a.vis + ((int64_t)it.h * a.t + it.qb) * a.t;
-    v.len = a.nvis[(int64_t)it.h * a.t + it.qb];
+    v.list = a.vis + ((int64_t)it.h * a.npairs + it.p) * a.t;
+    v.len = a.nvis[(int64_t)it.h * a.npairs + it.p];
   }
   return v;
 }
 
-// all 32 lanes of the warp must call this with the same e (e non-decreasing)
+// all 32 lanes of the warp must call this with the same e (e non-decreasing);
+// c0 / c1: the block's class for tile 0 / tile 1 (0 = not visited by that tile)
 __device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, Visit& v, int e, int lane,
-                                          int64_t& kb, int& cls) {
+                                          int64_t& kb, int& c0, int& c1) {
   if (a.dense) {
     kb = e;
     const bool ragged = (kb + 1) * kBN > a.n;
-    cls = (kb == it.qb || ragged) ? 1 : 2;
+    const int64_t qb0 = 2 * it.p, qb1 = qb0 + 1;
+    c0 = kb < qb0 ? (ragged ? 1 : 2) : (kb == qb0 ? 1 : 0);
+    c1 = qb1 < a.t ? ((kb < qb1 && !ragged) ? 2 : 1) : 0;
     return;
   }
   if (e >= v.base + 32) {
@@ -558,8 +444,9 @@ __device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, V
     v.cache = (v.base + lane < v.len) ? (uint32_t)__ldg(v.list + v.base + lane) : 0u;
   }
   const uint32_t x = __shfl_sync(0xffffffffu, v.cache, e - v.base);
-  kb = x & 0x3fffffffu;
-  cls = (int)(x >> 30);
+  kb = x & kKbMask;
+  c0 = (int)((x >> kKbBits) & 3u);
+  c1 = (int)((x >> (kKbBits + 2)) & 3u);
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
@@ -605,18 +492,12 @@ __device__ __forceinline__ void exp2_poly2(float y0, float y1, float& p0, float&
   p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
 }
 
-// Pass 1 (per visited block): this thread's kCols scores, masked, and their max
+// Pass 1 (per visited block): this thread's kCols scores and their max
 // (3-input FMNMX, eight independent chains).
-template <bool kPartial>
-__device__ __forceinline__ float load_scores(uint32_t tS, const int* ko, int qo, uint32_t (&r)[kCols]) {
+__device__ __forceinline__ float load_scores(uint32_t tS, uint32_t (&r)[kCols]) {
 #pragma unroll
   for (int c = 0; c < kCols / 32; ++c) TMEM_LD32(tS + c * 32, (r + c * 32));
   tmem_wait_ld();
-  if (kPartial) {
-#pragma unroll
-    for (int j = 0; j < kCols; ++j)
-      if (ko[j] > qo) r[j] = 0xff800000u;  // -inf: inadmissible (attention.hpp:298-300)
-  }
   float mx[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) mx[u] = __uint_as_float(r[u]);
@@ -694,8 +575,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar->q_full, 1);
-    mbar_init(&bar->q_empty, 1);
+    for (int w = 0; w < kGroups; ++w) {
+      mbar_init(&bar->q_full[w], 1);
+      mbar_init(&bar->q_empty[w], 1);
+      mbar_init(&bar->s_full[w], 1);
+      mbar_init(&bar->p_half[w], 128);
+      mbar_init(&bar->p_full[w], 128);
+      mbar_init(&bar->o_full[w], 1);
+      mbar_init(&bar->o_free[w], 128);
+    }
     for (int s = 0; s < kKStages; ++s) {
       mbar_init(&bar->k_full[s], 1);
       mbar_init(&bar->k_empty[s], 1);
@@ -704,13 +592,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar->v_full[s], 1);
       mbar_init(&bar->v_empty[s], 1);
     }
-    for (int w = 0; w < kGroups; ++w) {
-      mbar_init(&bar->s_full[w], 1);
-      mbar_init(&bar->p_half[w], 128);
-      mbar_init(&bar->p_full[w], 128);
-    }
-    mbar_init(&bar->o_full, 1);
-    mbar_init(&bar->o_free, kSoftmaxThreads);
     mbar_init(&bar->drained, 1);
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(&bar->item_full[i], 1);
@@ -732,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1)
    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
    if (warp == 0 || warp == 2) {
     // ===================== TMA producers (lane 0 issues) =====================
-    // warp 0: Q + K ring; warp 2: V ring
+    // warp 0: Q_0, Q_1 + the K ring; warp 2: the V ring.  Both walk the union list.
     const bool kp = (warp == 0);
     uint32_t q_it = 0, it_k = 0;
     ItemStream items;
@@ -741,16 +622,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kvh = it.h / a.group;
       Visit vis = visit_begin(a, it);
       if (kp && lane == 0) {
-        mbar_wait(&bar->q_empty, (q_it & 1) ^ 1);
-        mbar_expect_tx(&bar->q_full, kTileBytes);
-        for (int p = 0; p < 2; ++p)
-          tma_load_3d(smem + SmemLayout::q + p * kPanelBytes, &tm_q, &bar->q_full, p * 64, (int)(it.qb * kBM), it.h);
+        for (int w = 0; w < kGroups; ++w) {
+          int64_t qb = 2 * it.p + w;
+          if (qb >= a.t) qb = 2 * it.p;  // a lone last tile: tile 1's buffer gets tile 0's rows (never read)
+          mbar_wait(&bar->q_empty[w], (q_it & 1) ^ 1);
+          mbar_expect_tx(&bar->q_full[w], kTileBytes);
+          for (int p = 0; p < 2; ++p)
+            tma_load_3d(smem + SmemLayout::q + w * kTileBytes + p * kPanelBytes, &tm_q, &bar->q_full[w], p * 64,
+                        (int)(qb * kBM), it.h);
+        }
       }
       ++q_it;
       for (int e = 0; e < vis.len; ++e) {
         int64_t kb;
-        int cls;
-        visit_get(a, it, vis, e, lane, kb, cls);
+        int c0, c1;
+        visit_get(a, it, vis, e, lane, kb, c0, c1);
         if (lane == 0) {
           const int nst = kp ? kKStages : kVStages;
           const int s = (int)(it_k % nst);
@@ -767,77 +653,98 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
    } else if (warp == 1) {
     // ===================== MMA issuer (warp-collective, one elected lane) ========
-    // Per item: S_0 = Q K_0^T, S_1 = Q K_1^T, then for e = 0, 1, ...:
-    //   O_w (+)= P_e V_e (w = e & 1, once the group's softmax wrote P_e over S_w)
-    //   S_w = Q K_{e+2}^T (after that PV in issue order: it overwrites P_e)
+    // Union entry u, tile w = 0 then 1:
+    //   O_w (+)= P_w(u-1) V_{u-1}  if tile w visited entry u-1 (its softmax wrote P over S_w)
+    //   S_w = Q_w K_u^T            if tile w visits entry u (after that PV in issue
+    //                              order: it overwrites P_w)
+    // so K_u and V_{u-1} are each consumed within one step and free right after.
     const uint32_t idesc_qk = make_idesc(0, 0);  // Q K-major, K K-major
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
-    uint32_t q_it = 0, k_it = 0, v_it = 0, o_no = 0, p_cnt[kGroups] = {0, 0}, gbase = 0;
+    uint32_t q_it = 0, k_it = 0, v_it = 0, o_no[kGroups] = {0, 0}, p_cnt[kGroups] = {0, 0};
     SPAN_DECL
-    auto issue_qk = [&](int e, int len) {
-      const int w = e & 1;
-      const uint32_t stage = k_it % kKStages;
-      if (lane == 0) trace_event(a, 10, gbase + e);
-      mbar_wait(&bar->k_full[stage], (k_it / kKStages) & 1);
-      SPAN(5);
-      if (lane == 0) trace_event(a, 12, gbase + e);
-      tc_fence_after();
-      const uint32_t k_base = smem_u32(smem + SmemLayout::k + stage * kTileBytes);
-      static_assert(kD == 128 && kPanelBytes == 1024 * 16, "tc_mma_qk8 descriptor steps");
-      tc_mma_qk8(tmem + col_s(w), sdesc(q_base, 16, 1024), sdesc(k_base, 16, 1024), idesc_qk);
-      tc_commit_w(&bar->s_full[w]);
-      tc_commit_w(&bar->k_empty[stage]);
-      if (e + 1 == len) tc_commit_w(&bar->q_empty);  // every QK of the item issued: Q is free once they complete
-      if (lane == 0) trace_event(a, 2, gbase + e);
-      SPAN(6);
-      ++k_it;
-    };
     ItemStream items;
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
-      const int len = a.dense ? (int)(it.qb + 1) : a.nvis[(int64_t)it.h * a.t + it.qb];
-      mbar_wait(&bar->q_full, q_it & 1);
+      Visit vis = visit_begin(a, it);
+      for (int w = 0; w < kGroups; ++w) mbar_wait(&bar->q_full[w], q_it & 1);
       ++q_it;
       SPAN(7);
-      if (len == 0) {
-        tc_commit_w(&bar->q_empty);
+      if (vis.len == 0) {
+        for (int w = 0; w < kGroups; ++w) tc_commit_w(&bar->q_empty[w]);
         continue;
       }
-      for (int e = 0; e < len && e < kGroups; ++e) issue_qk(e, len);
-      for (int e = 0; e < len; ++e) {
-        const int w = e & 1;
-        const uint32_t stage = v_it % kVStages;
-        if (lane == 0) trace_event(a, 3, gbase + e);
-        mbar_wait(&bar->v_full[stage], (v_it / kVStages) & 1);
-        if (lane == 0) trace_event(a, 11, gbase + e);
-        if (e == 0) mbar_wait(&bar->o_free, (o_no & 1) ^ 1);  // the previous epilogue read O_0 and O_1
+      bool pend[kGroups] = {false, false}, first[kGroups] = {true, true};
+      for (int u = 0; u <= vis.len; ++u) {
+        int64_t kb = 0;
+        int cls[kGroups] = {0, 0};
+        if (u < vis.len) visit_get(a, it, vis, u, lane, kb, cls[0], cls[1]);
+        uint32_t v_base = 0;
+        if (u > 0) {
+          const uint32_t vs = v_it % kVStages;
+          mbar_wait(&bar->v_full[vs], (v_it / kVStages) & 1);
+          v_base = smem_u32(smem + SmemLayout::v + vs * kTileBytes);
+        }
+        const uint32_t ks = k_it % kKStages;
+        const uint32_t k_base = smem_u32(smem + SmemLayout::k + ks * kTileBytes);
+        bool k_seen = false;
         SPAN(0);
-        SPAN_COUNT(4);
-        // A = P [128 q x 128 kv] in TMEM (64 columns over S_w); B = V [128 kv x 128 d] MN-major SW128.
-        // Keys 0..63 go as soon as the group wrote them, keys 64..127 after the rest.
-        static_assert(kBN == 128, "two 64-key PV halves");
-        const uint32_t v_base = smem_u32(smem + SmemLayout::v + stage * kTileBytes);
-        mbar_wait(&bar->p_half[w], p_cnt[w] & 1);
-        SPAN(1);
-        tc_fence_after();
-        tc_mma_pv4(tmem + col_o(w), tmem + col_s(w), sdesc(v_base, kPanelBytes, 1024), idesc_pv, e < kGroups ? 0u : 1u);
-        SPAN(2);
-        mbar_wait(&bar->p_full[w], p_cnt[w] & 1);
-        SPAN(1);
-        if (lane == 0) trace_event(a, 0, gbase + e);
-        ++p_cnt[w];
-        tc_fence_after();
-        tc_mma_pv4(tmem + col_o(w), tmem + col_s(w) + 32, sdesc(v_base + 64 * 128, kPanelBytes, 1024), idesc_pv, 1u);
-        tc_commit_w(&bar->v_empty[stage]);
-        if (e + 1 == len) tc_commit_w(&bar->o_full);
-        if (lane == 0) trace_event(a, 1, gbase + e);
-        SPAN(3);
-        ++v_it;
-        if (e + kGroups < len) issue_qk(e + kGroups, len);
+#pragma unroll
+        for (int w = 0; w < kGroups; ++w) {
+          if (pend[w]) {
+            // A = P [128 q x 128 kv] in TMEM (64 columns over S_w); B = V [128 kv x 128 d] MN-major SW128.
+            // Keys 0..63 go as soon as the group wrote them, keys 64..127 after the rest.
+            static_assert(kBN == 128, "two 64-key PV halves");
+            if (first[w]) mbar_wait(&bar->o_free[w], (o_no[w] & 1) ^ 1);  // the previous epilogue read O_w
+            mbar_wait(&bar->p_half[w], p_cnt[w] & 1);
+            SPAN(1);
+            tc_fence_after();
+            tc_mma_pv4(tmem + col_o(w), tmem + col_s(w), sdesc(v_base, kPanelBytes, 1024), idesc_pv,
+                       first[w] ? 0u : 1u);
+            SPAN(2);
+            mbar_wait(&bar->p_full[w], p_cnt[w] & 1);
+            SPAN(1);
+            ++p_cnt[w];
+            tc_fence_after();
+            tc_mma_pv4(tmem + col_o(w), tmem + col_s(w) + 32, sdesc(v_base + 64 * 128, kPanelBytes, 1024), idesc_pv,
+                       1u);
+            SPAN(3);
+            first[w] = false;
+            pend[w] = false;
+          }
+          if (cls[w]) {
+            if (!k_seen) {
+              mbar_wait(&bar->k_full[ks], (k_it / kKStages) & 1);
+              SPAN(5);
+              k_seen = true;
+            }
+            tc_fence_after();
+            static_assert(kD == 128 && kPanelBytes == 1024 * 16, "tc_mma_qk8 descriptor steps");
+            tc_mma_qk8(tmem + col_s(w), sdesc(q_base + w * kTileBytes, 16, 1024), sdesc(k_base, 16, 1024),
+                       idesc_qk);
+            tc_commit_w(&bar->s_full[w]);
+            SPAN(6);
+            pend[w] = true;
+          }
+        }
+        if (u > 0) {
+          tc_commit_w(&bar->v_empty[v_it % kVStages]);
+          ++v_it;
+        }
+        if (u < vis.len) {
+          tc_commit_w(&bar->k_empty[ks]);
+          ++k_it;
+          SPAN_COUNT(4);
+        }
+        if (u + 1 == vis.len)  // every QK^T of the item issued: Q_0, Q_1 are free once they complete
+          for (int w = 0; w < kGroups; ++w) tc_commit_w(&bar->q_empty[w]);
       }
-      gbase += len;
-      ++o_no;
+      for (int w = 0; w < kGroups; ++w)
+        if (!first[w]) {
+          tc_commit_w(&bar->o_full[w]);
+          ++o_no[w];
+        }
+      SPAN(3);
     }
     // nothing may still write TMEM when it is released
     tc_commit_w(&bar->drained);
@@ -859,38 +766,41 @@ __global__ void __launch_bounds__(kThreads, 1)
    }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-    // ===================== softmax: group w takes the item's blocks e = w, w+2, ...
-    // One thread per query row (TMEM lane) and all 128 keys of the block, with the
-    // group's own running max m, sum l and accumulator O_w.  O_w is stable when
-    // S_w is ready: the group's previous PV was issued before that QK^T, whose
+    // ===================== softmax: group w owns query tile w of the item ==========
+    // One thread per query row (TMEM lane) and all 128 keys of each visited block,
+    // with the row's running max m, sum l and accumulator O_w.  O_w is stable when
+    // S_w is ready: the tile's previous PV was issued before this QK^T, whose
     // commit covers it, so the lazy rescale needs no wait.
-    const int w = (warp - 4) >> 2;     // softmax group
+    const int w = (warp - 4) >> 2;     // softmax group = query tile
     const int quad = warp & 3;         // TMEM lane quadrant of this warp
     const int row = quad * 32 + lane;  // query row within the tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t tS = tmem + lane_off + col_s(w);
     const uint32_t tO = tmem + lane_off + col_o(w);
     int* ko = reinterpret_cast<int*>(smem + SmemLayout::korig) + w * 128;
-    float* xch = reinterpret_cast<float*>(smem + SmemLayout::xch);  // [2 items][kGroups][2][128]
     const float sc = a.scale_log2;
     const bool any_mask = a.causal || a.q_orig || a.k_orig;
-    uint32_t s_cnt = 0, o_cnt = 0, gbase = 0;  // gbase: blocks of earlier items (trace numbering)
-    const bool tr = (row == 0);
+    uint32_t s_cnt = 0, o_cnt = 0;
     SPAN_DECL
     ItemStream items;
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
       Visit vis = visit_begin(a, it);
-      const int64_t i = it.qb * kBM + row;
-      const bool valid = i < a.n;
+      const int64_t qb = 2 * it.p + w;
+      const int64_t i = qb * kBM + row;
+      const bool valid = qb < a.t && i < a.n;
       const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
-      float m = -INFINITY;  // this group's running max (log2 domain)
-      float l = 0.0f;       // this group's running sum
-      for (int e = w; e < vis.len; e += kGroups) {
+      float m = -INFINITY;  // running max (log2 domain)
+      float l = 0.0f;       // running sum
+      bool any = false;
+      for (int e = 0; e < vis.len; ++e) {
         int64_t kb;
-        int cls;
-        visit_get(a, it, vis, e, lane, kb, cls);
-        if (cls == 1) {  // original positions of the block's keys, for this group
+        int c0, c1;
+        visit_get(a, it, vis, e, lane, kb, c0, c1);
+        const int cls = w ? c1 : c0;
+        if (cls == 0) continue;  // warp-uniform: a block's class is the tile's
+        any = true;
+        if (cls == 1) {  // original positions of the block's keys, for this tile
           const int64_t j = kb * kBN + row;
           int v = 0x7fffffff;
           if (j < a.n) v = a.k_orig ? a.k_orig[(int64_t)it.h * a.n + j] : (int)j;
@@ -898,12 +808,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           ko[row] = v;
           named_bar_sync(1 + w, 128);
         }
-        if (tr) trace_event(a, 7, gbase + e);
         SPAN(0);
         mbar_wait(&bar->s_full[w], s_cnt & 1);
         SPAN(1);
         SPAN_COUNT(7);
-        if (tr) trace_event(a, 4, gbase + e);
         ++s_cnt;
         tc_fence_after();
         uint32_t r[kCols];
@@ -923,9 +831,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_st();
           named_bar_sync(1 + w, 128);  // ko may be refilled after this
         }
-        const float hmax = load_scores<false>(tS, ko, qo, r);
+        const float hmax = load_scores(tS, r);
         SPAN(2);
-        if (tr) trace_event(a, 5, gbase + e);
         // online softmax (absorb, attention.hpp:96-126) in the log2 domain with
         // lazy rescaling: O_w is rescaled only when the max grows by more than 8
         const float m_new = fmaxf(m, hmax * sc);
@@ -957,65 +864,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         l = l * factor + rs;
         tmem_wait_st();
         tc_fence_before();
-        if (tr) trace_event(a, 6, gbase + e);
         mbar_arrive(&bar->p_full[w]);
         SPAN(4);
       }
-      gbase += vis.len;
-      // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138): merge
-      // the two groups' (m, l, O), O / l -> out[out_rows[i]] (the fused
-      // un-permute, pipeline.hpp:178); group w writes output columns [64 w, 64 w + 64)
-      if (vis.len == 0) {
-        if (valid && a.status && w == 0) {
+      // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138):
+      // O_w / l -> out[out_rows[i]] (the fused un-permute, pipeline.hpp:178)
+      if (!any) {  // the tile visits no block: no PV ran, O_w is not ours to read
+        if (valid && a.status) {
           a.status[0] = 1;
-          atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
+          atomicMin(&a.status[1], (int)(it.h * a.t + qb));
         }
         continue;
       }
-      float* xb = xch + (o_cnt & 1) * kGroups * 2 * 128;  // by item parity: the next item's writes cannot race
-      xb[(w * 2 + 0) * 128 + row] = m;
-      xb[(w * 2 + 1) * 128 + row] = l;
-      named_bar_sync(3, kSoftmaxThreads);
-      const float m0 = xb[row], l0 = xb[128 + row], m1 = xb[256 + row], l1 = xb[384 + row];
-      mbar_wait(&bar->o_full, o_cnt & 1);  // the item's last PV
+      mbar_wait(&bar->o_full[w], o_cnt & 1);  // the tile's last PV
       ++o_cnt;
       tc_fence_after();
-      const float mt = fmaxf(m0, m1);
-      const float f0 = (m0 == -INFINITY) ? 0.0f : ex2(m0 - mt);
-      const float f1 = (m1 == -INFINITY) ? 0.0f : ex2(m1 - mt);
-      const float lt = l0 * f0 + l1 * f1;
-      if (valid && !(lt > 0.0f) && a.status && w == 0) {
+      if (valid && !(l > 0.0f) && a.status) {
         a.status[0] = 1;
-        atomicMin(&a.status[1], (int)(it.h * a.t + it.qb));
+        atomicMin(&a.status[1], (int)(it.h * a.t + qb));
       }
       const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
-      if (a.lse && valid && w == 0)  // natural-log LSE: l = sum 2^(s c - m), c = scale log2(e)
-        a.lse[(int64_t)it.h * a.n + orow] = (lt > 0.0f) ? (mt + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
-      const float inv = (lt > 0.0f) ? 1.0f / lt : 0.0f;
-      const float g0 = f0 * inv, g1 = f1 * inv;
-      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD + w * (kD / kGroups);
+      if (a.lse && valid)  // natural-log LSE: l = sum 2^(s c - m), c = scale log2(e)
+        a.lse[(int64_t)it.h * a.n + orow] = (l > 0.0f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      const float inv = (l > 0.0f) ? 1.0f / l : 0.0f;
+      __nv_bfloat16* dst = a.out + ((int64_t)it.h * a.n + orow) * kD;
 #pragma unroll 1
-      for (int c = 0; c < kD / kGroups / 32; ++c) {
-        const uint32_t col = w * (kD / kGroups) + c * 32;
-        uint32_t o0[32], o1[32];
-        TMEM_LD32(tmem + lane_off + col_o(0) + col, o0);
-        TMEM_LD32(tmem + lane_off + col_o(1) + col, o1);
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t o[32];
+        TMEM_LD32(tO + c * 32, o);
         tmem_wait_ld();
-        if (valid && lt > 0.0f) {
+        if (valid && l > 0.0f) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             uint32_t pk[4];
 #pragma unroll
             for (int w2 = 0; w2 < 4; ++w2) {
               const int j = u * 8 + 2 * w2;
-              // a group without blocks in this item has m = -inf and a stale O: select, never multiply
-              float v0 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j]) * g0;
-              float v1 = (m0 == -INFINITY) ? 0.0f : __uint_as_float(o0[j + 1]) * g0;
-              if (m1 != -INFINITY) {
-                v0 = fmaf(__uint_as_float(o1[j]), g1, v0);
-                v1 = fmaf(__uint_as_float(o1[j + 1]), g1, v1);
-              }
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
               pk[w2] = *reinterpret_cast<uint32_t*>(&b2);
             }
             *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -1023,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&bar->o_free);
+      mbar_arrive(&bar->o_free[w]);
       SPAN(5);
     }
     SPAN(6);
@@ -1037,31 +922,66 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// per (head, query block): the compacted list of visited key blocks with their
-// class (AdmissibilityIndex::classify), one warp per item
-__global__ void visit_kernel(KernelArgs a, int32_t* __restrict__ vis, int32_t* __restrict__ nvis) {
-  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (g >= (int64_t)a.hq * a.t) return;
-  Item it;
-  it.h = (int)(g / a.t);
-  it.qb = g % a.t;
-  const int len = list_len(a, it);
-  int32_t* out = vis + g * a.t;
-  int cnt = 0;
-  for (int e0 = 0; e0 < len; e0 += 32) {
-    const int e = e0 + lane;
-    int64_t kb = 0;
-    int cls = 0;
-    if (e < len) {
-      kb = list_at(a, it, e);
-      cls = block_class(a, it, kb);
+// per item (head, pair of query blocks): the ascending union of the two tiles'
+// selected key blocks, each with both tiles' classes (AdmissibilityIndex::
+// classify; blocks of class none for both tiles dropped).  One warp per item:
+// the two lists become bitmaps in shared memory, then each lane walks 32 words.
+constexpr int kVisitWarps = 4;
+__global__ void visit_pair_kernel(KernelArgs a, int words, int32_t* __restrict__ vis, int32_t* __restrict__ nvis) {
+  extern __shared__ uint32_t bm_smem[];
+  const int wip = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kVisitWarps + wip;
+  if (g >= (int64_t)a.hq * a.npairs) return;
+  uint32_t* bm0 = bm_smem + (size_t)wip * 2 * words;
+  uint32_t* bm1 = bm0 + words;
+  for (int x = lane; x < 2 * words; x += 32) bm0[x] = 0u;
+  __syncwarp();
+  const int h = (int)(g / a.npairs);
+  const int64_t p = g % a.npairs;
+  const int64_t qb0 = 2 * p, qb1 = qb0 + 1;
+  for (int w = 0; w < kGroups; ++w) {
+    const int64_t qb = qb0 + w;
+    if (qb >= a.t) break;
+    const int cnt = a.kv_cnt[(int64_t)h * a.t + qb];
+    const int32_t* list = a.kv_idx + ((int64_t)h * a.t + qb) * a.t;
+    uint32_t* bm = w ? bm1 : bm0;
+    for (int e = lane; e < cnt; e += 32) {
+      const int kb = list[e];
+      atomicOr(&bm[kb >> 5], 1u << (kb & 31));
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, cls != 0);
-    if (cls != 0) out[cnt + __popc(bal & ((1u << lane) - 1))] = (int32_t)(kb | ((int64_t)cls << 30));
-    cnt += __popc(bal);
   }
-  if (lane == 0) nvis[g] = cnt;
+  __syncwarp();
+  int32_t* out = vis + g * a.t;
+  int total = 0;
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int wi = w0 + lane;
+    const uint32_t m0 = wi < words ? bm0[wi] : 0u, m1 = wi < words ? bm1[wi] : 0u;
+    uint32_t keep = 0u;
+    for (uint32_t u = m0 | m1; u; u &= u - 1) {
+      const int bit = __ffs(u) - 1;
+      const int64_t kb = (int64_t)wi * 32 + bit;
+      const int c0 = ((m0 >> bit) & 1u) ? block_class(a, h, qb0, kb) : 0;
+      const int c1 = ((m1 >> bit) & 1u) ? block_class(a, h, qb1, kb) : 0;
+      if (c0 | c1) keep |= 1u << bit;
+    }
+    const int cnt = __popc(keep);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = total + incl - cnt;
+    for (uint32_t u = keep; u; u &= u - 1) {
+      const int bit = __ffs(u) - 1;
+      const int64_t kb = (int64_t)wi * 32 + bit;
+      const int c0 = ((m0 >> bit) & 1u) ? block_class(a, h, qb0, kb) : 0;
+      const int c1 = ((m1 >> bit) & 1u) ? block_class(a, h, qb1, kb) : 0;
+      out[pos++] = (int32_t)((uint32_t)kb | ((uint32_t)c0 << kKbBits) | ((uint32_t)c1 << (kKbBits + 2)));
+    }
+    total += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) nvis[g] = total;
 }
 
 // per-block [min, max] of an original-position map (AdmissibilityIndex::build)
@@ -1212,7 +1132,8 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   a.causal = p.causal;
   a.dense = p.kv_idx == nullptr;
   if (a.dense && !p.causal) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention without a block list must be causal");
-  a.items = (int64_t)p.hq * t;
+  a.npairs = ceil_div(t, 2);
+  a.items = (int64_t)p.hq * a.npairs;
   // scratch: block min/max of the original positions + visit lists
   if (!sched_ws) {
     sched_ws = stream_scratch(st, a.dense ? 256 : attention_sm100_workspace_bytes(p.hq, p.n, p.block));
@@ -1237,9 +1158,20 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   }
   if (!a.dense) {
     int32_t* vis = static_cast<int32_t*>(sched_ws) + (2 * (size_t)p.hq * t * sizeof(int2)) / sizeof(int32_t);
-    int32_t* nvis = vis + (size_t)p.hq * t * t;
-    visit_kernel<<<(unsigned)ceil_div((int64_t)p.hq * t, 8), 256, 0, st>>>(a, vis, nvis);
-    PBS_LAUNCH_CHECK("visit_kernel");
+    int32_t* nvis = vis + (size_t)p.hq * a.npairs * t;
+    const int words = (int)ceil_div(t, 32);
+    const size_t smem = (size_t)kVisitWarps * 2 * words * sizeof(uint32_t);
+    if (smem > 48 * 1024) {
+      static DeviceOnce vis_once;
+      if (int rc = once_per_device(vis_once, [] {
+            PBS_CUDA_CHECK(cudaFuncSetAttribute(visit_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                200 * 1024));
+            return (int)PBS_OK;
+          }))
+        return rc;
+    }
+    visit_pair_kernel<<<(unsigned)ceil_div(a.items, kVisitWarps), kVisitWarps * 32, smem, st>>>(a, words, vis, nvis);
+    PBS_LAUNCH_CHECK("visit_pair_kernel");
     a.vis = vis;
     a.nvis = nvis;
   }
@@ -1252,15 +1184,17 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
     return rc;
   int grid = (int)min64(a.items, num_sms());
   if (const char* e = getenv("PBS_ATTN_GRID")) grid = (int)min64(grid, atoi(e) > 0 ? atoi(e) : grid);  // debug
+  // debug (-DPBS_ATTN_SPANS builds): per-phase cycle sums of every CTA, dumped to $PBS_ATTN_TRACE
   const char* trace_path = getenv("PBS_ATTN_TRACE");
+  constexpr int kSpanWords = 32;
   if (trace_path) {
-    PBS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), 16 * kTraceEvents * 8, st));
-    PBS_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, 16 * kTraceEvents * 8, st));
+    PBS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), kSpanWords * 8, st));
+    PBS_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, kSpanWords * 8, st));
   }
   attn_sm100_kernel<<<grid, kThreads, SmemLayout::total, st>>>(mq, mk, mv, a);
   PBS_LAUNCH_CHECK("attn_sm100_kernel");
-  if (trace_path) {  // debug only: synchronous dump of CTA 0's timeline
-    std::vector<unsigned long long> h(16 * kTraceEvents);
+  if (trace_path) {  // debug only: synchronous dump
+    std::vector<unsigned long long> h(kSpanWords);
     PBS_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
     PBS_CUDA_CHECK(cudaStreamSynchronize(st));
     PBS_CUDA_CHECK(cudaFree(a.trace));
