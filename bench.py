@@ -181,45 +181,114 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU reference
-def cpu_reference_sample(n_s, threads, seed=99):
-    """The reference's own CPU pbs_attention (oracle/_ref: the unmodified
-    headers compiled with their build flags) over `threads` query heads at
-    sequence length n_s, one head per std::thread like pbs_main.cpp:99-122.
-    Returns (wall seconds, report)."""
+def _stages_heads(ref, q, k, v, cfg, threads):
+    """pbsref_pbs_stages_heads_f32: stages 1-3 of the reference pipeline per head
+    (estimate + key permutation, apply_rows, pooled scores + selection) on
+    `threads` std::threads; returns (summed stage us [3], selected blocks)."""
+    import ctypes as C
+
+    fn = ref.lib.pbsref_pbs_stages_heads_f32
+    us = np.zeros(3, dtype=np.float64)
+    sel = C.c_int64(0)
+    rc = fn(q.ctypes.data_as(C.c_void_p), k.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p),
+            C.c_int(q.shape[0]), C.c_int(k.shape[0]), C.c_size_t(q.shape[1]), C.c_size_t(q.shape[2]), C.byref(cfg),
+            C.c_int(threads), us.ctypes.data_as(C.c_void_p), C.byref(sel))
+    if rc != 0:
+        raise RuntimeError(ref.lib.pbsref_last_error().decode() if hasattr(ref.lib, "pbsref_last_error") else rc)
+    return us, sel.value
+
+
+_CPU_INPUTS: dict = {}
+
+
+def cpu_reference(n_full, threads, exec_blocks_full=None, n_attn=8192, seed=99):
+    """The reference's own CPU path on the box's host cores:
+    oracle/_ref (the unmodified reference headers compiled with their build
+    flags), one query head per std::thread like pbs_main.cpp:99-122.
+
+      * stages 1-3 (estimate + permutation, apply_rows, pooled scores +
+        selection) MEASURED at full length on `heads` query heads (whole GQA
+        groups, one per thread), wall time scaled by HQ / heads;
+      * attention (stage 4) EXTRAPOLATED: the reference's attention_us
+        (StageTimings, pipeline.hpp:51-61) on the same heads at n_attn gives
+        its executed FLOP rate per thread; the full attention is the full
+        problem's executed FLOPs (4 B^2 d per selected block pair; the
+        device run's count when given -- the selection is bit-exact -- else the
+        measured heads' count scaled by HQ / heads) at that rate on `threads`.
+    Returns a dict of the measured and extrapolated parts (ms)."""
     import torch
 
     import oracle
 
-    ref = oracle.Oracle("ref") if oracle.Oracle.available("ref") else None
-    kind = "reference"
-    if ref is None:  # reference never built on this machine: time the C restatement instead
-        ref = oracle.Oracle("oracle")
-        kind = "port"
-    # whole GQA groups only (the reference maps query head h to KV head h / group)
-    hkv = max(1, min(HKV, threads // (HQ // HKV)))
-    q, k, v = make_inputs(torch, n_s, 0, hkv * (HQ // HKV), list(range(hkv)), "cpu", seed)
-    q = q.float().numpy()
-    k = k.float().numpy()
-    v = v.float().numpy()
+    kind = "reference" if oracle.Oracle.available("ref") else "port"
+    if kind != "reference":
+        return None  # the stage timer lives in the reference shim only
+    ref = oracle.Oracle("ref")
+    g = HQ // HKV
+    hkv_s = max(1, min(HKV, threads // g))
+    heads = hkv_s * g
     cfg = oracle.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy=STRATEGY)
+
+    def inputs(n):  # generated once per length (outside the timed calls)
+        key = (n, heads, hkv_s, seed)
+        if key not in _CPU_INPUTS:
+            if len(_CPU_INPUTS) >= 2:  # keep the full-length and the sample inputs of the current config only
+                _CPU_INPUTS.clear()
+            _CPU_INPUTS[key] = tuple(x.float().numpy() for x in make_inputs(torch, n, 0, heads, list(range(hkv_s)),
+                                                                             "cpu", seed))
+        return _CPU_INPUTS[key]
+
+    q, k, v = inputs(n_full)
     t0 = time.perf_counter()
-    if kind == "reference":
-        _, rep = ref.pbs_attention_heads(q, k, v, cfg, threads)
-    else:
-        rep = None
-        for h in range(q.shape[0]):
-            rep = ref.pbs_attention(q[h], k[h // (HQ // HKV)], v[h // (HQ // HKV)], cfg).report
-    wall = time.perf_counter() - t0
-    return wall, rep, kind, q.shape[0]
+    stage_us, sel_full = _stages_heads(ref, q, k, v, cfg, threads)
+    wall_stages = time.perf_counter() - t0
+    qa, ka, va = inputs(n_attn)
+    t0 = time.perf_counter()
+    _, rep = ref.pbs_attention_heads(qa, ka, va, cfg, threads)
+    wall_attn_sample = time.perf_counter() - t0
+    flop_per_block = 4.0 * BLOCK * BLOCK * D
+    rate_thread = flop_per_block * rep["selected_blocks"] / (rep["attention_us"] * 1e-6)  # FLOP/s per thread
+    exec_blocks = exec_blocks_full if exec_blocks_full is not None else sel_full * HQ / heads
+    attn_ms = exec_blocks * flop_per_block / (rate_thread * threads) * 1e3
+    stages_ms = wall_stages * 1e3 * HQ / heads
+    return {"value": stages_ms + attn_ms, "kind": kind, "cores": threads, "heads": heads,
+            "measured_stages_ms": stages_ms, "extrapolated_attention_ms": attn_ms,
+            "stage_thread_ms": {"estimate": stage_us[0] / 1e3 / heads, "permute": stage_us[1] / 1e3 / heads,
+                                "select": stage_us[2] / 1e3 / heads},
+            "attention_gflops_per_thread": rate_thread / 1e9,
+            "sample": (f"stages 1-3 of the reference pipeline measured at full length ({n_full} tokens) on {heads} "
+                       f"query heads, one per std::thread ({wall_stages:.1f} s wall), scaled by {HQ}/{heads}; "
+                       f"attention extrapolated from the reference's attention_us at {n_attn} tokens on the same "
+                       f"heads ({rate_thread / 1e9:.2f} GFLOP/s per thread, {wall_attn_sample:.1f} s wall) to "
+                       f"{exec_blocks:.0f} executed block pairs x 4 B^2 d on {threads} threads"
+                       + (" (device-counted)" if exec_blocks_full is not None else " (scaled from the measured heads)"))}
 
 
-def extrapolate_cpu_ms(wall_s, heads_s, n_s, n_full=None, heads_full=None):
-    """Scale a sampled CPU run to the full workload.  The sampled run is
-    dominated (>85%) by block-sparse attention, whose work grows as N^2 at a
-    fixed selected fraction; heads scale linearly (one head per thread)."""
-    n_full = N if n_full is None else n_full
-    heads_full = HQ if heads_full is None else heads_full
-    return wall_s * 1e3 * (n_full / n_s) ** 2 * (heads_full / heads_s)
+def sdpa_dense_ms(torch, q, k, v, warmup, steps, barrier):
+    """torch's own dense causal attention on the same [H, N, d] bf16 shapes, as
+    an outside anchor for the dense comparator: the first SDPA backend that runs
+    (cuDNN, then flash, then memory-efficient), GQA through enable_gqa."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    F = torch.nn.functional
+    qq, kk, vv = q[None], k[None], v[None]
+    for backend in (SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION):
+        try:
+            with sdpa_kernel([backend]):
+                for _ in range(max(1, warmup)):
+                    F.scaled_dot_product_attention(qq, kk, vv, is_causal=True, enable_gqa=True)
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(steps):
+                    F.scaled_dot_product_attention(qq, kk, vv, is_causal=True, enable_gqa=True)
+                e1.record()
+                barrier()
+            return {"ms": e0.elapsed_time(e1) / steps, "backend": backend.name}
+        except Exception:  # backend unavailable for these shapes / this build: try the next
+            torch.cuda.synchronize()
+            continue
+    return None
 
 
 # ------------------------------------------------------------------ main
@@ -229,17 +298,17 @@ def run_reference(args):
         return 0
     threads = os.cpu_count() or 1
     ms = []
-    kind = "reference"
-    rep = None
-    heads = threads
+    res = None
     for i in range(args.warmup + args.steps):
-        wall, rep, kind, heads = cpu_reference_sample(args.cpu_seq, threads)
-        if i >= args.warmup:
-            ms.append(extrapolate_cpu_ms(wall, heads, args.cpu_seq, args.seq))
+        if i < args.warmup:  # warm-up: a short sample (page-in, thread start-up)
+            cpu_reference(min(args.seq, 8192), threads, n_attn=2048)
+            continue
+        res = cpu_reference(args.seq, threads, n_attn=args.cpu_seq)
+        if res is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpbsref.so was not built"}))
+            return 0
+        ms.append(res["value"])
     value = float(np.median(ms))
-    sample = (f"{heads} query heads x {args.cpu_seq} tokens ({args.model} GQA shapes, same synthetic workload), full "
-              f"reference pbs_attention per head on {threads} std::threads; wall time scaled by "
-              f"(N/{args.cpu_seq})^2 x ({HQ}/{heads}) to {HQ} heads x {args.seq} tokens (extrapolated)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
@@ -247,9 +316,10 @@ def run_reference(args):
         "config": {"workload": f"{PREFIX}_{args.seq // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
                    "seq_len": args.seq, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
                    "strategy": STRATEGY, "parallelism": "cpu threads"},
-        "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": res["kind"], "sample": res["sample"],
+                         "measured_stages_ms": res["measured_stages_ms"],
+                         "extrapolated_attention_ms": res["extrapolated_attention_ms"]},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "sample_density": rep["block_density"] if rep else None,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -367,6 +437,15 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dense_ms = t.item()
 
+    # anchor: torch SDPA dense causal attention (cuDNN or flash backend) on the same shapes
+    sdpa = None
+    if not args.no_dense:
+        sdpa = sdpa_dense_ms(torch, q, k, v, args.warmup, min(args.steps, 5), barrier)
+        if sdpa and world > 1:
+            t = torch.tensor([sdpa["ms"]], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sdpa["ms"] = t.item()
+
     # FLOP accounting: executed = 4 B^2 d per selected block pair (band
     # tiles in full); dense-causal = 4 d N(N+1)/2 per head
     sel_local = rep["selected_blocks"]
@@ -384,19 +463,23 @@ def main():
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
     peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "fallback"
     achieved = exec_flops / world / (att_ms * 1e-3) / 1e12 if att_ms > 0 else None
+    # DRAM bytes per attention launch from an ncu capture of THIS workload (profiles/attn_traffic.json,
+    # keyed by config.workload; null when no capture of this config exists)
+    workload = f"{PREFIX}_{n // 1024}k_pbs" + (f"_{STRATEGY}" if STRATEGY != "key_permute" else "") + \
+        (f"_top{args.top_k}" if args.top_k else "")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+    if os.path.exists(tpath) and world == 1:
+        traffic = (json.load(open(tpath)).get(workload) or {}).get("dram_bytes_per_launch")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        wall, crep, kind, heads = cpu_reference_sample(args.cpu_seq, threads)
-        cpu_ms = extrapolate_cpu_ms(wall, heads, args.cpu_seq, n)
-        cpu = {"value": cpu_ms, "unit": "ms", "cores": threads, "kind": kind,
-               "sample": f"{heads} heads x {args.cpu_seq} tokens, reference pbs_attention on {threads} threads "
-                         f"({wall:.1f} s wall), scaled by (N/{args.cpu_seq})^2 x ({HQ}/{heads}) (extrapolated)"}
+        res_cpu = cpu_reference(n, os.cpu_count() or 1, exec_blocks_full=sel, n_attn=args.cpu_seq)
+        if res_cpu is not None:
+            cpu = {"value": res_cpu["value"], "unit": "ms", "cores": res_cpu["cores"], "kind": res_cpu["kind"],
+                   "sample": res_cpu["sample"], "measured_stages_ms": res_cpu["measured_stages_ms"],
+                   "extrapolated_attention_ms": res_cpu["extrapolated_attention_ms"],
+                   "stage_thread_ms": res_cpu["stage_thread_ms"]}
 
     if rank == 0:
         line = {
@@ -405,12 +488,13 @@ def main():
             "vs_baseline": None, "dtype": "bf16",
             "data": ("synthetic (vertical-lines Q/K/V, seeded; selection by the real tau=0.9 algorithm)" if not args.top_k
                      else f"synthetic (vertical-lines Q/K/V, seeded; top-{args.top_k} selection, an extension)"),
-            "config": {"workload": f"{PREFIX}_{n // 1024}k_pbs", "q_heads": HQ, "kv_heads": HKV,
+            "config": {"workload": workload, "q_heads": HQ, "kv_heads": HKV,
                        "seq_len": n, "head_dim": D, "block": BLOCK, "segment": SEGMENT, "tau": TAU,
                        "strategy": STRATEGY, "top_k": args.top_k or None, "parallelism": f"heads{world}",
                        "l2": "inputs (1.5 GiB) > L2 (126 MB); no flush"},
             "speedup_vs_dense_fa": (dense_ms / ms) if dense_ms else None,
             "dense_fa_ms": dense_ms,
+            "sdpa_dense_causal": sdpa,
             "effective_tflops": dense_flops / (ms * 1e-3) / 1e12,
             "executed_tflops_attention": achieved,
             "block_density": rep["block_density"],

@@ -9,7 +9,9 @@
 // "reference"), fanning heads over std::thread like pbs_main.cpp:99-122.
 //
 // Signatures match oracle/pbs_oracle.h with the prefix pbsref_.
+#include <array>
 #include <cstring>
+#include <mutex>
 #include <exception>
 #include <string>
 #include <thread>
@@ -343,6 +345,81 @@ int pbsref_pbs_attention_heads_f32(const float* q, const float* k, const float* 
       rep_sum->attention_us += reps[h].attention_us;
       rep_sum->unpermute_us += reps[h].unpermute_us;
     }
+  }
+  return 0;
+}
+
+// Stages 1-3 of pbs_attention (pipeline.hpp:129-171) under key_permute, per
+// head over `threads` workers, each stage timed like StageClock (pipeline.hpp:
+// 86-99): estimate_key_importance + build_key_permutation (estimate),
+// apply_rows of K and V (permute), meanpool_block_scores + select_blocks
+// (select).  The CPU baseline times these at full length and extrapolates only
+// the attention.  stage_us[3] and the selected-block count are
+// summed over heads.
+int pbsref_pbs_stages_heads_f32(const float* q, const float* k, const float* v, int hq, int hkv, size_t n,
+                                size_t d, const pbs_pipeline_config* c, int threads, double* stage_us,
+                                int64_t* selected) {
+  if (hkv <= 0 || hq <= 0 || hq % hkv != 0 || c->strategy != PBS_STRATEGY_KEY_PERMUTE) {
+    g_err = "E_CONFIG: stage timing covers key_permute over whole GQA groups";
+    return PBS_ERR_CONFIG;
+  }
+  const int g = hq / hkv;
+  std::vector<std::array<double, 3>> us(hq);
+  std::vector<int64_t> sel(hq, 0);
+  std::vector<int> rcs(hq, 0);
+  std::vector<std::string> errs(hq);
+  int next = 0;
+  std::mutex mu;
+  const pbs::PipelineConfig cfg = to_cfg(c, pbs::Precision::f32);
+  auto worker = [&]() {
+    for (;;) {
+      int h;
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (next >= hq) return;
+        h = next++;
+      }
+      try {
+        const auto qm = to_mat(q + (size_t)h * n * d, n, d);
+        const auto km = to_mat(k + (size_t)(h / g) * n * d, n, d);
+        const auto vm = to_mat(v + (size_t)(h / g) * n * d, n, d);
+        const auto acfg = pbs::AttentionConfig::make(cfg.block_size, d, false, cfg.scale);
+        pbs::detail::StageClock clock;
+        const auto imp = pbs::estimate_key_importance(qm, km, acfg);
+        const pbs::Permutation pi = pbs::build_key_permutation(imp, cfg.segment_size).flatten();
+        us[h][0] = clock.lap_us();
+        const auto qp = pbs::apply_rows(pbs::Permutation::identity(n), qm);  // sigma = identity
+        const auto kp = pbs::apply_rows(pi, km);
+        const auto vp = pbs::apply_rows(pi, vm);
+        us[h][1] = clock.lap_us();
+        const std::size_t t = (n + cfg.block_size - 1) / cfg.block_size;
+        const auto causal = pbs::build_block_causal_mask<float>(t, t, cfg.block_size, cfg.segment_size);
+        const auto bsm = pbs::meanpool_block_scores(qp, kp, cfg.block_size, cfg.segment_size, causal, cfg.scale);
+        const auto mask = pbs::select_blocks(bsm, cfg.tau, cfg.forced);
+        us[h][2] = clock.lap_us();
+        sel[h] = (int64_t)mask.selected_count();
+        (void)vp;
+      } catch (const pbs::Error& e) {
+        rcs[h] = fail(e);
+        errs[h] = g_err;
+      } catch (const std::exception& e) {
+        rcs[h] = fail_other(e);
+        errs[h] = g_err;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < (threads < 1 ? 1 : threads); ++t) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+  for (int i = 0; i < 3; ++i) stage_us[i] = 0.0;
+  *selected = 0;
+  for (int h = 0; h < hq; ++h) {
+    if (rcs[h]) {
+      g_err = errs[h];
+      return rcs[h];
+    }
+    for (int i = 0; i < 3; ++i) stage_us[i] += us[h][i];
+    *selected += sel[h];
   }
   return 0;
 }

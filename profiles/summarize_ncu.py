@@ -2,7 +2,11 @@
 roofline claims rest on, and (with --traffic) write profiles/attn_traffic.json,
 which bench.py reads for roofline.traffic (DRAM bytes per launch).
 
-    python profiles/summarize_ncu.py gpurun_out/prof.ncu-rep [--traffic] > profiles/rNN_ncu_<kernel>.txt
+    python profiles/summarize_ncu.py gpurun_out/prof.ncu-rep [--traffic WORKLOAD] > profiles/rNN_ncu_<kernel>.txt
+
+--traffic WORKLOAD records the capture under the bench's config.workload key
+(e.g. llama31_8b_attn_128k_pbs); bench.py reports roofline.traffic only for
+the workload a capture was taken on, else null.
 """
 import csv
 import io
@@ -34,7 +38,7 @@ KEYS = [
 STALL = "smsp__average_warps_issue_stalled_"
 
 
-def main(path, traffic=False):
+def main(path, traffic=None):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
@@ -55,11 +59,13 @@ def main(path, traffic=False):
             rd = float(rec["dram__bytes_read.sum"].replace(',', '')) * scale[unit["dram__bytes_read.sum"]]
             wr = float(rec["dram__bytes_write.sum"].replace(',', '')) * scale[unit["dram__bytes_write.sum"]]
             dst = os.path.join(os.path.dirname(os.path.abspath(__file__)), "attn_traffic.json")
-            json.dump({"kernel": rec.get("Kernel Name", "")[:60], "dram_bytes_per_launch": rd + wr,
-                       "dram_read": rd, "dram_write": wr, "source": os.path.basename(path),
-                       "note": "ncu --set full --clock-control none, one launch of the C3 (128K) bench step"},
-                      open(dst, "w"), indent=1)
-
+            doc = json.load(open(dst)) if os.path.exists(dst) else {}
+            if "dram_bytes_per_launch" in doc:  # the round-1 single-capture form
+                doc = {}
+            doc[traffic] = {"kernel": rec.get("Kernel Name", "")[:60], "dram_bytes_per_launch": rd + wr,
+                            "dram_read": rd, "dram_write": wr, "source": os.path.basename(path),
+                            "note": "ncu --set full --clock-control none, one attention launch of the bench step"}
+            json.dump(doc, open(dst, "w"), indent=1)
 
 if __name__ == "__main__":
-    main(sys.argv[1], "--traffic" in sys.argv)
+    main(sys.argv[1], sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None)
