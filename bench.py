@@ -21,10 +21,13 @@ fused un-permute) over all heads.  `value` is the device time per step in ms
 reference-facing host-buffer C-ABI call (pinned host in, host out).  Inputs
 (1.5 GiB) exceed the 126 MB L2, so no flush is needed between steps.
 
-Multi-GPU (one process per GPU): query heads are split across ranks along KV
-groups (8 groups of 4); each rank runs its heads and one NCCL all-gather
-assembles the [32, N, d] output -- the only collective.
-Strong scaling: the problem is fixed, value = max-over-ranks ms.
+Multi-GPU (one process per GPU): pbs_shard_plan gives each
+rank a contiguous share of the (query head, query-block pair) work with equal
+causal work (whole heads for Llama's 32 heads on 1/2/4/8 GPUs, a cut inside a
+head for Qwen's 28 on 8); each rank holds only its Q and KV heads and calls
+pbs_dist_attention, which runs its share and assembles the [Hq, N, d] output
+with one NCCL all-gather-v (per-rank in-place broadcasts) -- the only
+collective.  Strong scaling: the problem is fixed, value = max-over-ranks ms.
 """
 from __future__ import annotations
 
@@ -75,27 +78,6 @@ def parse():
     if args.seq is None:
         args.seq = N
     return args
-
-
-# ------------------------------------------------------------------ sharding
-def shard_of(rank, world):
-    """Head-parallel shard: rank r owns query heads
-    [r HQ / world, (r + 1) HQ / world).  Llama's 8 groups of 4 split whole
-    groups over 1/2/4/8 ranks; Qwen's 4 groups of 7 split 3 + 4 on 8 ranks, both
-    halves holding the group's KV head.  Returns (q0, q1, kv_list, g_local):
-    the local K/V are the global KV heads kv_list, local query head j reads
-    local KV head j // g_local (when the local heads do not split evenly over
-    their KV heads, each query head gets its own copy: g_local = 1)."""
-    q0, q1 = rank * HQ // world, (rank + 1) * HQ // world
-    if q1 <= q0:
-        raise ValueError(f"{HQ} query heads do not split over {world} ranks")
-    g = HQ // HKV
-    kvs = [h // g for h in range(q0, q1)]
-    uniq = sorted(set(kvs))
-    counts = {kvs.count(x) for x in uniq}
-    if len(counts) == 1:
-        return q0, q1, uniq, counts.pop()
-    return q0, q1, kvs, 1
 
 
 # ------------------------------------------------------------------ workload
@@ -343,22 +325,38 @@ def main():
 
     lib = ops.lib()
     n = args.seq
-    q0, q1, kv_list, _ = shard_of(rank, world)
-    q, k, v = make_inputs(torch, n, q0, q1, kv_list, "cuda")
-    max_local = max(shard_of(r, world)[1] - shard_of(r, world)[0] for r in range(world))
-    torch.cuda.synchronize()
     cfg = ops.make_config(block_size=BLOCK, segment_size=SEGMENT, tau=TAU, strategy=STRATEGY, top_k=args.top_k)
-    ws = ops.workspace(ops.workspace_size(q, k, cfg))
-    # ranks with fewer heads pad their share of the gather (Qwen on 8 GPUs: 3 or 4)
-    out_pad = torch.zeros(max_local, n, D, dtype=torch.bfloat16, device="cuda")
-    out = out_pad[:q1 - q0]
-    full = torch.empty(world * max_local, n, D, dtype=torch.bfloat16, device="cuda") if world > 1 else out
     stream = torch.cuda.current_stream()
+    if world == 1:
+        q, k, v = make_inputs(torch, n, 0, HQ, list(range(HKV)), "cuda")
+        ws = ops.workspace(ops.workspace_size(q, k, cfg))
+        out = torch.empty_like(q)
+        full = out
+        ctx = None
+    else:
+        # head-parallel shard (csrc/dist.cu): this rank's contiguous
+        # share of the (head, query-block pair) work; only its Q heads and KV heads
+        shard = ops.shard_plan(HQ, HKV, n, D, BLOCK, world, rank)
+        q, k, v = make_inputs(torch, n, shard["head_begin"], shard["head_end"],
+                              list(range(shard["kv_begin"], shard["kv_end"])), "cuda")
+        full = torch.zeros(HQ, n, D, dtype=torch.bfloat16, device="cuda")
+        uid = [ops.dist_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = ops.DistContext(uid[0], world, rank)
+        ws = ops.workspace(ctx.workspace_size(q, HQ, HKV, cfg))
+        out = full
+    torch.cuda.synchronize()
 
     def step():
-        ops.pbs_attention(q, k, v, cfg, report=False, out=out, return_perms=False, ws=ws)
-        if world > 1:
-            dist.all_gather_into_tensor(full, out_pad)
+        if ctx is None:
+            ops.pbs_attention(q, k, v, cfg, report=False, out=out, return_perms=False, ws=ws)
+        else:  # compute this rank's rows + the one exchange (NCCL all-gather-v inside the library)
+            ctx.attention(q, k, v, HQ, HKV, cfg, full, ws=ws)
+
+    def report_pass():
+        if ctx is None:
+            return ops.pbs_attention(q, k, v, cfg, report=True, out=out, return_perms=False, ws=ws).report
+        return ops.attention_shard(q, k, v, HQ, HKV, cfg, world, rank, full, ws=ws, report=True)
 
     def barrier():
         if world > 1:
@@ -366,8 +364,7 @@ def main():
         torch.cuda.synchronize()
 
     # report pass: stage timings (CUDA events on the launching stream), selection stats
-    res = ops.pbs_attention(q, k, v, cfg, report=True, out=out, return_perms=False, ws=ws)
-    rep = res.report
+    rep = report_pass() if ctx is None else ctx.attention(q, k, v, HQ, HKV, cfg, full, ws=ws, report=True)
     for _ in range(args.warmup):
         step()
     barrier()
@@ -391,32 +388,49 @@ def main():
     stage = {key: 0.0 for key in ("estimate_us", "permute_us", "select_us", "attention_us", "unpermute_us")}
     reps = 3
     for _ in range(reps):
-        r = ops.pbs_attention(q, k, v, cfg, report=True, out=out, return_perms=False, ws=ws).report
+        r = report_pass()
         for key in stage:
             stage[key] += r[key] / reps
 
-    # e2e through the reference-facing host-buffer C-ABI call
+    # e2e through the reference-facing host-buffer C-ABI call: pinned host Q/K/V
+    # in, the [Hq, N, d] output back on the host.  N > 1: each rank copies its
+    # shard in, runs pbs_dist_attention (compute + NCCL gather), rank 0 copies
+    # the assembled output out.
     e2e = None
     if not args.no_e2e:
         hq_, hk_, hv_ = (x.cpu().pin_memory() for x in (q, k, v))
-        hout = torch.empty_like(hq_).pin_memory()
+        hout = torch.empty(HQ, n, D, dtype=torch.bfloat16).pin_memory()
+
+        def e2e_step():
+            if ctx is None:
+                ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout)
+                return
+            dq, dk, dv = (x.to("cuda", non_blocking=True) for x in (hq_, hk_, hv_))
+            ctx.attention(dq, dk, dv, HQ, HKV, cfg, full, ws=ws)
+            if rank == 0:
+                hout.copy_(full, non_blocking=True)
+            torch.cuda.synchronize()
+
         for _ in range(2):
-            ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout)
+            e2e_step()
         barrier()
         t0 = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 5))
         for _ in range(e2e_steps):
-            ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout)
+            e2e_step()
         barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = t.item()
         bi = sum(x.numel() * x.element_size() for x in (q, k, v))
-        bo = out.numel() * out.element_size()
+        if world > 1:
+            t = torch.tensor([e2e_ms, float(bi)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+            e2e_ms, bi = t[0].item(), int(t[1].item())
+        bo = HQ * n * D * 2
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
-               "timing": "host wall clock around the synchronous C-ABI call (pinned host buffers)"}
+               "timing": ("host wall clock around the synchronous C-ABI call (pinned host buffers)" if world == 1
+                          else "host wall clock, max over ranks: shard H2D + pbs_dist_attention (compute + NCCL "
+                               "all-gather-v) + rank 0's D2H of the assembled output")}
 
     # dense causal FlashAttention comparator (same kernel family, full causal grid)
     dense_ms = None
@@ -448,13 +462,7 @@ def main():
 
     # FLOP accounting: executed = 4 B^2 d per selected block pair (band
     # tiles in full); dense-causal = 4 d N(N+1)/2 per head
-    sel_local = rep["selected_blocks"]
-    if world > 1:
-        t = torch.tensor([float(sel_local)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t)
-        sel = t.item()
-    else:
-        sel = float(sel_local)
+    sel = float(rep["selected_blocks"])  # global: pbs_dist_attention's report is reduced over ranks
     exec_flops = 4.0 * BLOCK * BLOCK * D * sel
     dense_flops = 4.0 * D * n * (n + 1) / 2 * HQ
     att_ms = stage["attention_us"] / 1e3

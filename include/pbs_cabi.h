@@ -223,6 +223,58 @@ PBS_API int pbs_attention_host(const void* q, const void* k, const void* v, cons
                        const pbs_pipeline_config* cfg, void* out, int32_t* sigma,
                        int32_t* pi, uint8_t* mask, pbs_report* report);
 
+/* ---- multi-GPU: head-parallel shards ----------------------
+ * Replaces the reference CLI's per-head fan-out (for_each_head,
+ * tools/pbs_main.cpp:99-122: heads share nothing) with one process
+ * per GPU.  Work units are (query head, pair of query blocks), weighted by
+ * their causal key blocks; rank r owns the contiguous unit range holding the
+ * r-th 1/world of the work (whole heads when Hq % world == 0, otherwise a cut
+ * inside a head), so every rank's output rows are ONE contiguous range of the
+ * flattened [Hq * N] output rows.  A rank needs its query heads
+ * [head_begin, head_end) and KV heads [kv_begin, kv_end) only. */
+typedef struct pbs_shard {
+  int32_t head_begin, head_end; /* query heads touched */
+  int32_t kv_begin, kv_end;     /* KV heads needed */
+  int64_t qb_begin;             /* first query block of head_begin (even) */
+  int64_t qb_end;               /* end query block of head_end - 1 (T = all) */
+  int64_t out_row_begin;        /* the rank's rows of the flattened [Hq * N] output */
+  int64_t out_rows;
+} pbs_shard;
+PBS_API int pbs_shard_plan(const pbs_shape* global_shape, int64_t block_size, int32_t world_size, int32_t rank,
+                           pbs_shard* shard);
+PBS_API size_t pbs_shard_workspace_size(const pbs_shape* global_shape, const pbs_pipeline_config* cfg,
+                                        int32_t world_size, int32_t rank);
+/* Rank `rank`'s share of pbs_attention, compute only (no collective):
+ * q_local [head_end - head_begin, N, d], k_local / v_local
+ * [kv_end - kv_begin, N, d]; writes only the shard's rows of out_full
+ * [Hq, N, d].  Running every rank's shard into one buffer reproduces
+ * pbs_attention's output bit for bit.  report (optional) covers the shard's
+ * rows, densities averaged over the GLOBAL Hq (sum them over ranks). */
+PBS_API int pbs_attention_shard(const void* q_local, const void* k_local, const void* v_local,
+                                const pbs_shape* global_shape, const pbs_pipeline_config* cfg, int32_t world_size,
+                                int32_t rank, void* out_full, void* workspace, size_t workspace_bytes,
+                                pbs_report* report, void* stream);
+
+/* Per-rank handle owning an NCCL communicator (NCCL is loaded at run time).
+ * Rank 0 makes the id, the ranks share it out of band (e.g. torch.distributed
+ * or MPI), every rank creates its handle on its own device. */
+#define PBS_NCCL_UNIQUE_ID_BYTES 128
+typedef struct pbs_dist pbs_dist;
+PBS_API int pbs_dist_unique_id(uint8_t id[PBS_NCCL_UNIQUE_ID_BYTES]);
+PBS_API int pbs_dist_create(const uint8_t id[PBS_NCCL_UNIQUE_ID_BYTES], int32_t world_size, int32_t rank,
+                            pbs_dist** handle);
+PBS_API int pbs_dist_destroy(pbs_dist* handle);
+PBS_API size_t pbs_dist_workspace_size(const pbs_dist* handle, const pbs_shape* global_shape,
+                                       const pbs_pipeline_config* cfg);
+/* pbs_attention_shard on this rank, then the one exchange: every rank's rows
+ * broadcast in place into out_full on all ranks (one NCCL group of
+ * ncclBroadcast calls = an all-gather-v over NVLink).  Collective: every rank
+ * calls it with the same global shape and config; report (global counts) is
+ * collective too -- all ranks pass one or none. */
+PBS_API int pbs_dist_attention(pbs_dist* handle, const void* q_local, const void* k_local, const void* v_local,
+                               const pbs_shape* global_shape, const pbs_pipeline_config* cfg, void* out_full,
+                               void* workspace, size_t workspace_bytes, pbs_report* report, void* stream);
+
 /* ---- diagnostics (pipeline.hpp:195-295) --------------------------------- */
 
 /* Device scratch for pbs_attention_coverage. */

@@ -31,7 +31,8 @@ EXPORTS = [
     "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_select_blocks_top_k", "pbs_block_sparse_attention_fwd",
     "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
     "pbs_coverage_workspace_size", "pbs_attention_coverage", "pbs_tensor_info_read", "pbs_tensor_load",
-    "pbs_tensor_save", "pbs_debug_expf",
+    "pbs_tensor_save", "pbs_debug_expf", "pbs_shard_plan", "pbs_shard_workspace_size", "pbs_attention_shard",
+    "pbs_dist_unique_id", "pbs_dist_create", "pbs_dist_destroy", "pbs_dist_workspace_size", "pbs_dist_attention",
 ]
 
 
@@ -58,6 +59,17 @@ class Report(C.Structure):
                 ("total_admissible_blocks", C.c_int64), ("estimate_us", C.c_double),
                 ("permute_us", C.c_double), ("select_us", C.c_double), ("attention_us", C.c_double),
                 ("unpermute_us", C.c_double)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class Shard(C.Structure):
+    """pbs_shard: one rank's share of the head-parallel split."""
+
+    _fields_ = [("head_begin", C.c_int32), ("head_end", C.c_int32), ("kv_begin", C.c_int32), ("kv_end", C.c_int32),
+                ("qb_begin", C.c_int64), ("qb_end", C.c_int64), ("out_row_begin", C.c_int64),
+                ("out_rows", C.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -139,6 +151,16 @@ _SIGS = {
     "pbs_tensor_load": (C.c_int, [C.c_char_p, VP, I32, VP]),
     "pbs_tensor_save": (C.c_int, [C.c_char_p, VP, I32, I64, I64, I64, I32, I32, VP]),
     "pbs_debug_expf": (C.c_int, [VP, VP, I64, VP]),
+    "pbs_shard_plan": (C.c_int, [C.POINTER(Shape), I64, I32, I32, C.POINTER(Shard)]),
+    "pbs_shard_workspace_size": (SZ, [C.POINTER(Shape), C.POINTER(PipelineConfig), I32, I32]),
+    "pbs_attention_shard": (C.c_int, [VP, VP, VP, C.POINTER(Shape), C.POINTER(PipelineConfig), I32, I32, VP, VP, SZ,
+                                      C.POINTER(Report), VP]),
+    "pbs_dist_unique_id": (C.c_int, [VP]),
+    "pbs_dist_create": (C.c_int, [VP, I32, I32, C.POINTER(VP)]),
+    "pbs_dist_destroy": (C.c_int, [VP]),
+    "pbs_dist_workspace_size": (SZ, [VP, C.POINTER(Shape), C.POINTER(PipelineConfig)]),
+    "pbs_dist_attention": (C.c_int, [VP, VP, VP, VP, C.POINTER(Shape), C.POINTER(PipelineConfig), VP, VP, SZ,
+                                     C.POINTER(Report), VP]),
 }
 
 

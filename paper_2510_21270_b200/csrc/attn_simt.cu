@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kRows* kLanes) attn_simt_kernel(AttnParams p, 
   float* vs = ks + kKeys * d;     // [kKeys][d]
   int* kor = reinterpret_cast<int*>(vs + kKeys * d);  // [kKeys]
   const int h = blockIdx.y;
-  const int64_t qb = blockIdx.x / subtiles;
+  const int64_t qb = p.qb_begin + blockIdx.x / subtiles;
   const int sub = blockIdx.x % subtiles;
   const int tid = threadIdx.x;
   const int rl = tid / kLanes, lane = tid % kLanes;
@@ -122,6 +122,8 @@ int launch_attention_simt(const AttnParams& p, cudaStream_t st) {
   const int64_t t = ceil_div(p.n, p.block);
   if (t == 0) return PBS_OK;
   const int subtiles = (int)ceil_div(p.block, kRows);
+  const int64_t qb_end = p.qb_end > 0 ? min64(p.qb_end, t) : t;
+  if (p.qb_begin < 0 || p.qb_begin >= qb_end) return fail(PBS_ERR_CONFIG, "E_CONFIG", "empty query-block range");
   const size_t smem = (size_t)2 * kKeys * p.d * 4 + kKeys * 4;
   // head dims above 192 need more than the 48 KB default (d = 256: 64 KB + 128 B)
   static DeviceOnce attr_once;
@@ -133,7 +135,7 @@ int launch_attention_simt(const AttnParams& p, cudaStream_t st) {
         return (int)PBS_OK;
       }))
     return rc;
-  dim3 grid((unsigned)(t * subtiles), (unsigned)p.hq);
+  dim3 grid((unsigned)((qb_end - p.qb_begin) * subtiles), (unsigned)p.hq);
   if (p.dtype == PBS_DTYPE_BF16)
     attn_simt_kernel<__nv_bfloat16><<<grid, kRows * kLanes, smem, st>>>(p, t, subtiles);
   else

@@ -323,6 +323,7 @@ struct KernelArgs {
   int hq, kv_heads, group;
   int64_t n, t;
   int64_t npairs;  // ceil(t / 2): items are (head, pair of query blocks 2p, 2p + 1)
+  int64_t p_lo, p_hi;  // pairs [p_lo, p_hi) of every head (a shard's query-block range)
   float scale_log2;
   const int32_t* kv_idx;
   const int32_t* kv_cnt;
@@ -369,14 +370,15 @@ __device__ __forceinline__ Item item_of(const KernelArgs& a, int64_t idx) {
   // per-head permuted K'/V', per GQA group for shared K/V), heaviest pairs
   // first inside it.
   Item it;
-  const int64_t per = a.npairs * (a.kv_heads == a.hq ? 1 : a.group);
+  const int64_t np = a.p_hi - a.p_lo;
+  const int64_t per = np * (a.kv_heads == a.hq ? 1 : a.group);
   const int64_t grp = idx / per, rem = idx % per;
   if (a.kv_heads == a.hq) {
     it.h = (int)grp;
-    it.p = a.npairs - 1 - rem;
+    it.p = a.p_hi - 1 - rem;
   } else {
     it.h = (int)(grp * a.group + rem % a.group);
-    it.p = a.npairs - 1 - rem / a.group;
+    it.p = a.p_hi - 1 - rem / a.group;
   }
   return it;
 }
@@ -1133,7 +1135,16 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   a.dense = p.kv_idx == nullptr;
   if (a.dense && !p.causal) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention without a block list must be causal");
   a.npairs = ceil_div(t, 2);
-  a.items = (int64_t)p.hq * a.npairs;
+  {
+    const int64_t qb_end = p.qb_end > 0 ? min64(p.qb_end, t) : t;
+    if (p.qb_begin < 0 || p.qb_begin >= qb_end || (p.qb_begin & 1))
+      return fail(PBS_ERR_CONFIG, "E_CONFIG", "query-block range must be non-empty and start on an even block");
+    a.p_lo = p.qb_begin / 2;
+    a.p_hi = ceil_div(qb_end, 2);
+    if (qb_end != t && (qb_end & 1))
+      return fail(PBS_ERR_CONFIG, "E_CONFIG", "query-block range must end on an even block or at the last one");
+  }
+  a.items = (int64_t)p.hq * (a.p_hi - a.p_lo);
   // scratch: block min/max of the original positions + visit lists
   if (!sched_ws) {
     sched_ws = stream_scratch(st, a.dense ? 256 : attention_sm100_workspace_bytes(p.hq, p.n, p.block));

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "pipeline.h"
 
 namespace pbs_b200 {
 
@@ -50,7 +51,6 @@ int cuda_fail(cudaError_t e, const char* where) {
   return PBS_ERR_CUDA;
 }
 
-namespace {
 
 int esize_of(int dtype) { return dtype == PBS_DTYPE_BF16 ? 2 : 4; }
 
@@ -91,11 +91,6 @@ int check_cfg(const pbs_pipeline_config* c) {
 bool uses_pi(int s) { return s == PBS_STRATEGY_KEY_PERMUTE || s == PBS_STRATEGY_BOTH; }
 bool uses_sigma(int s) { return s == PBS_STRATEGY_QUERY_PERMUTE || s == PBS_STRATEGY_BOTH; }
 
-// workspace carve-up for pbs_attention
-struct Layout {
-  size_t status, imp, scores, pi, pi_inv, sigma, sigma_inv, groups, qperm, kp, vp, qp, qbar, kbar, blog, mask,
-      kv_idx, kv_cnt, row_cov, sched, total;
-};
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -134,41 +129,12 @@ Layout plan(const pbs_shape* s, const pbs_pipeline_config* c) {
   return L;
 }
 
-struct Timer {
-  bool on;
-  cudaStream_t st;
-  cudaEvent_t ev[6];
-  int k = 0;
-  Timer(bool enabled, cudaStream_t s) : on(enabled), st(s) {
-    if (on)
-      for (auto& e : ev) cudaEventCreate(&e);
-  }
-  ~Timer() {
-    if (on)
-      for (auto& e : ev) cudaEventDestroy(e);
-  }
-  Timer(const Timer&) = delete;
-  Timer& operator=(const Timer&) = delete;
-  void restart(cudaStream_t s) {
-    st = s;
-    k = 0;
-  }
-  void mark() {
-    if (on && k < 6) cudaEventRecord(ev[k++], st);
-  }
-  double us(int a) const {
-    float ms = 0.0f;
-    cudaEventElapsedTime(&ms, ev[a], ev[a + 1]);
-    return ms * 1000.0;
-  }
-};
 
 int run_attention(const AttnParams& p, void* sched, cudaStream_t st) {
   if (attention_sm100_supported(p)) return launch_attention_sm100(p, sched, st);
   return launch_attention_simt(p, st);
 }
 
-}  // namespace
 }  // namespace pbs_b200
 
 using namespace pbs_b200;
@@ -456,14 +422,13 @@ int pbs_check_status(const int32_t* status, int64_t num_blocks, void* stream) {
 }  // extern "C"
 
 namespace pbs_b200 {
-namespace {
 // Algorithm 1 enqueued on `stream` (no synchronisation); stage events go to tm.
 // pi_given (key_permute only): pi of every head, computed beforehand (the host
 // entry estimates all heads at once from the keys and the last query rows).
 int pipeline_enqueue(const void* q, const void* k, const void* v, const pbs_shape* shape,
                      const pbs_pipeline_config* cfg, void* out, int32_t* sigma_out, int32_t* pi_out,
                      uint8_t* mask_out, void* workspace, size_t workspace_bytes, Timer& tm, void* stream,
-                     const int32_t* pi_given = nullptr) {
+                     const int32_t* pi_given, int64_t qb_begin, int64_t qb_end) {
   if (int rc = check_shape(shape)) return rc;
   if (int rc = check_cfg(cfg)) return rc;
   const Layout L = plan(shape, cfg);
@@ -572,6 +537,8 @@ int pipeline_enqueue(const void* q, const void* k, const void* v, const pbs_shap
   p.status = status;
   // ElementMask(sigma, pi) with both identities is exactly the causal mask
   p.causal = (p.q_orig == nullptr && p.k_orig == nullptr) ? 1 : 0;
+  p.qb_begin = qb_begin;
+  p.qb_end = qb_end;
   if (int rc = run_attention(p, at(L.sched), st)) return rc;
   tm.mark();
   tm.mark();  // un-permute is fused into the attention epilogue
@@ -593,9 +560,10 @@ int report_fetch(const pbs_shape* shape, const pbs_pipeline_config* cfg, const v
 
 // ---- report (pipeline.hpp:182-191) from the fetched counters
 int report_build(const pbs_shape* shape, const pbs_pipeline_config* cfg, const int32_t* cnt, const double* cov,
-                 const int32_t* hs, const Timer& tm, pbs_report* report) {
+                 const int32_t* hs, const Timer& tm, pbs_report* report, int64_t qb_begin, int64_t qb_end) {
   const int hq = shape->num_q_heads;
   const int64_t b = cfg->block_size, s = cfg->segment_size, t = ceil_div(shape->seq_len, b);
+  const int64_t lo = qb_begin, hi = qb_end > 0 ? std::min<int64_t>(qb_end, t) : t;
   if (hs[0]) {
     return fail(PBS_ERR_DEGENERATE, "E_DEGENERATE",
                 "query block " + std::to_string(hs[1] % t) + " (head " + std::to_string(hs[1] / t) +
@@ -603,12 +571,12 @@ int report_build(const pbs_shape* shape, const pbs_pipeline_config* cfg, const i
   }
   memset(report, 0, sizeof *report);
   int64_t adm = 0;
-  for (int64_t i = 0; i < t; ++i) adm += admissible_prefix(i, t, b, s);
+  for (int64_t i = lo; i < hi; ++i) adm += admissible_prefix(i, t, b, s);
   double dens = 0.0, covsum = 0.0;
   for (int h = 0; h < hq; ++h) {
     int64_t sel = 0;
     double c = 0.0;
-    for (int64_t i = 0; i < t; ++i) {
+    for (int64_t i = lo; i < hi; ++i) {
       sel += cnt[(size_t)h * t + i];
       c += cov[(size_t)h * t + i];
     }
@@ -627,7 +595,6 @@ int report_build(const pbs_shape* shape, const pbs_pipeline_config* cfg, const i
   report->unpermute_us = tm.us(4);
   return PBS_OK;
 }
-}  // namespace
 }  // namespace pbs_b200
 
 extern "C" {

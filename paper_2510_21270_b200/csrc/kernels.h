@@ -83,6 +83,10 @@ struct AttnParams {
   // a row with no admissible key), f32 [Hq, N] in output-row order, or nullptr
   float* lse;
   int causal;               // dense causal comparator mode
+  // query blocks [qb_begin, qb_end) only (qb_end == 0: all; qb_begin even on the
+  // tensor-core path): a head-parallel shard that cuts inside a head
+  int64_t qb_begin;
+  int64_t qb_end;
 };
 int launch_attention_simt(const AttnParams& p, cudaStream_t st);
 bool attention_sm100_supported(const AttnParams& p);

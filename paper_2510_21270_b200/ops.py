@@ -20,6 +20,8 @@ and stream plumbing here.
     attention_coverage        pipeline.hpp:198-243
     density_sweep             pipeline.hpp:245-295
     tensor_info / load_tensor / save_tensor   tensor_io.hpp (PBST files)
+    shard_plan / attention_shard / DistContext  head-parallel multi-GPU (the
+                              per-head fan-out of pbs_main.cpp:99-122)
 """
 from __future__ import annotations
 
@@ -29,7 +31,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import PipelineConfig, Report, Shape, check
+from ._lib import PipelineConfig, Report, Shape, Shard, check
 
 _WS: dict = {}
 
@@ -392,3 +394,81 @@ def debug_expf(x: torch.Tensor) -> torch.Tensor:
     y = torch.empty_like(x)
     check(lib().pbs_debug_expf(_ptr(x), _ptr(y), x.numel(), _stream()))
     return y
+
+
+# ---------------------------------------------------------------- multi-GPU
+def shard_plan(num_q_heads, num_kv_heads, seq_len, head_dim, block_size, world_size, rank, dtype=torch.bfloat16):
+    """pbs_shard_plan: rank's contiguous share of the (query head, query-block
+    pair) work units, weighted by causal key blocks.  Pure host arithmetic."""
+    code = _lib.DTYPE_BF16 if dtype == torch.bfloat16 else _lib.DTYPE_F32
+    shape = Shape(code, num_q_heads, num_kv_heads, head_dim, seq_len)
+    s = Shard()
+    check(lib().pbs_shard_plan(C.byref(shape), block_size, world_size, rank, C.byref(s)))
+    return s.as_dict()
+
+
+def _global_shape(q_local, num_q_heads, num_kv_heads):
+    _, n, d = q_local.shape
+    return Shape(_dtype_code(q_local), num_q_heads, num_kv_heads, d, n)
+
+
+def attention_shard(q_local, k_local, v_local, num_q_heads, num_kv_heads, cfg, world_size, rank, out_full,
+                    ws=None, report=False):
+    """Rank `rank`'s share of pbs_attention, compute only, into its rows of
+    out_full [Hq, N, d] (q_local: the shard's query heads, k/v_local: its KV heads)."""
+    _check_dev(q_local, k_local, v_local, out_full)
+    shape = _global_shape(q_local, num_q_heads, num_kv_heads)
+    need = lib().pbs_shard_workspace_size(C.byref(shape), C.byref(cfg), world_size, rank)
+    if need == 0:
+        check(_lib.PBS_ERR_CONFIG)
+    ws = workspace(need, q_local.device) if ws is None else ws
+    rep = Report() if report else None
+    check(lib().pbs_attention_shard(_ptr(q_local), _ptr(k_local), _ptr(v_local), C.byref(shape), C.byref(cfg),
+                                    world_size, rank, _ptr(out_full), _ptr(ws), ws.numel(),
+                                    C.byref(rep) if rep else None, _stream()))
+    return rep.as_dict() if rep else None
+
+
+def dist_unique_id() -> bytes:
+    """pbs_dist_unique_id: the NCCL id rank 0 shares with the other ranks."""
+    buf = (C.c_uint8 * 128)()
+    check(lib().pbs_dist_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+class DistContext:
+    """pbs_dist: a per-rank handle owning the NCCL communicator of the
+    head-parallel path; attention() computes the rank's share and all-gathers
+    every rank's rows into out_full (the one exchange)."""
+
+    def __init__(self, unique_id: bytes, world_size: int, rank: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self.world, self.rank = world_size, rank
+        self._h = C.c_void_p()
+        check(lib().pbs_dist_create(C.cast(buf, C.c_void_p), world_size, rank, C.byref(self._h)))
+
+    def workspace_size(self, q_local, num_q_heads, num_kv_heads, cfg):
+        shape = _global_shape(q_local, num_q_heads, num_kv_heads)
+        return int(lib().pbs_dist_workspace_size(self._h, C.byref(shape), C.byref(cfg)))
+
+    def attention(self, q_local, k_local, v_local, num_q_heads, num_kv_heads, cfg, out_full, ws=None, report=False):
+        _check_dev(q_local, k_local, v_local, out_full)
+        shape = _global_shape(q_local, num_q_heads, num_kv_heads)
+        if ws is None:
+            ws = workspace(self.workspace_size(q_local, num_q_heads, num_kv_heads, cfg), q_local.device)
+        rep = Report() if report else None
+        check(lib().pbs_dist_attention(self._h, _ptr(q_local), _ptr(k_local), _ptr(v_local), C.byref(shape),
+                                       C.byref(cfg), _ptr(out_full), _ptr(ws), ws.numel(),
+                                       C.byref(rep) if rep else None, _stream()))
+        return rep.as_dict() if rep else None
+
+    def close(self):
+        if self._h:
+            lib().pbs_dist_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,11 +1,16 @@
 """Multi-rank host logic of the head-parallel path, on CPU.
 
-bench.py shards query heads along KV groups and assembles the output with one
-all-gather.  Here 2 gloo ranks run that exact sharding on a small problem,
-compute each local head with the CPU oracle (standing in for the device
-pipeline) and all-gather; the result must equal the single-rank run bit for
-bit, i.e. the shard boundaries, per-KV-head seeding and gather order
-reproduce the N = 1 problem.
+The product splits the work with pbs_shard_plan (csrc/dist.cu): contiguous
+ranges of (query head, query-block pair) units holding equal causal work, so
+each rank's output rows are one contiguous range of the [Hq * N] output and
+the one exchange is an all-gather-v (one broadcast per rank).  Here:
+  * the plan itself (coverage, contiguity, balance, KV ranges) for the bench
+    shapes at 1/2/4/8 ranks, against a Python restatement of the work model;
+  * 2 and 8 gloo ranks run that exact split on a small problem, compute their
+    rows with the CPU oracle (standing in for the device pipeline, which
+    tests/test_gpu_parity.py::test_shards_reassemble_* runs rank by rank) and
+    exchange them with the same per-rank broadcasts; the result must equal the
+    single-rank run bit for bit.
 """
 import os
 import socket
@@ -16,7 +21,10 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from paper_2510_21270_b200 import ops
+
 N_SMALL = 512
+B_SMALL, S_SMALL = 64, 128
 
 
 def _free_port():
@@ -34,23 +42,92 @@ def _use_model(name):
     return bench
 
 
-def _local_outputs(rank, world, model="llama", pad_to=None):
+def _pair_work(t):
+    """Causal key blocks visited per (head, pair): tiles 2p and 2p + 1."""
+    return [(2 * p + 1) + (2 * p + 2 if 2 * p + 1 < t else 0) for p in range((t + 1) // 2)]
+
+
+@pytest.mark.parametrize("hq,hkv,n,b", [(32, 8, 131072, 128), (28, 4, 262144, 128), (32, 8, 32768, 128),
+                                        (28, 4, N_SMALL, B_SMALL), (6, 3, 1000, 64), (1, 1, 4096, 64),
+                                        (5, 5, 129, 128)])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_plan_covers_balances_and_is_contiguous(hq, hkv, n, b, world):
+    t = -(-n // b)
+    w = _pair_work(t)
+    owner = {}
+    rows = []
+    loads = []
+    for r in range(world):
+        s = ops.shard_plan(hq, hkv, n, 128, b, world, r)
+        load = 0
+        for h in range(s["head_begin"], s["head_end"]):
+            lo = s["qb_begin"] if h == s["head_begin"] else 0
+            hi = s["qb_end"] if h == s["head_end"] - 1 else t
+            assert lo % 2 == 0 and (hi % 2 == 0 or hi == t) and lo < hi
+            for p in range(lo // 2, -(-hi // 2)):
+                assert (h, p) not in owner
+                owner[(h, p)] = r
+                load += w[p]
+        if s["out_rows"]:
+            assert s["kv_begin"] == s["head_begin"] // (hq // hkv)
+            assert s["kv_end"] == (s["head_end"] - 1) // (hq // hkv) + 1
+            rows.append((s["out_row_begin"], s["out_rows"]))
+        loads.append(load)
+    assert len(owner) == hq * len(w)  # every unit exactly once
+    start = 0
+    for r0, cnt in rows:  # contiguous, in rank order, tiling [0, Hq * N)
+        assert r0 == start
+        start += cnt
+    assert start == hq * n
+    mean = sum(loads) / world
+    assert max(loads) - mean <= max(w) + 1e-9  # balanced to one unit
+    if hq % world == 0:  # whole heads when they split evenly
+        for r in range(world):
+            s = ops.shard_plan(hq, hkv, n, 128, b, world, r)
+            assert s["qb_begin"] == 0 and s["qb_end"] == t and s["head_end"] - s["head_begin"] == hq // world
+
+
+def test_qwen_on_8_ranks_is_balanced_not_4_plus_3():
+    """28 heads on 8 ranks: 3.5 heads of work each (the 4 + 3 head split caps
+    efficiency at 87.5%)."""
+    t = 262144 // 128
+    w = _pair_work(t)
+    head_w = sum(w)
+    loads = []
+    for r in range(8):
+        s = ops.shard_plan(28, 4, 262144, 128, 128, 8, r)
+        load = 0
+        for h in range(s["head_begin"], s["head_end"]):
+            lo = s["qb_begin"] if h == s["head_begin"] else 0
+            hi = s["qb_end"] if h == s["head_end"] - 1 else t
+            load += sum(w[lo // 2:-(-hi // 2)])
+        loads.append(load / head_w)
+    assert max(loads) - min(loads) < 2 * max(w) / head_w
+    assert abs(np.mean(loads) - 3.5) < 1e-9
+
+
+def _oracle_rows(model, world, rank):
+    """The rank's rows of the [Hq, N, d] output from the CPU oracle (whole heads
+    computed, the shard's rows kept), flattened [rows, d]."""
     import oracle
 
     bench = _use_model(model)
-    q0, q1, kv_list, g_local = bench.shard_of(rank, world)
-    q, k, v = bench.make_inputs(torch, N_SMALL, q0, q1, kv_list, "cpu")
+    s = ops.shard_plan(bench.HQ, bench.HKV, N_SMALL, 128, B_SMALL, world, rank)
+    if s["out_rows"] == 0:
+        return s, torch.zeros(0, 128)
+    kv_list = list(range(s["kv_begin"], s["kv_end"]))
+    q, k, v = bench.make_inputs(torch, N_SMALL, s["head_begin"], s["head_end"], kv_list, "cpu")
     orc = oracle.Oracle("oracle")
-    cfg = oracle.make_config(block_size=64, segment_size=128, tau=0.9, strategy="key_permute")
+    cfg = oracle.make_config(block_size=B_SMALL, segment_size=S_SMALL, tau=0.9, strategy="key_permute")
+    g = bench.HQ // bench.HKV
     outs = []
-    for h in range(q1 - q0):
-        r = orc.pbs_attention(q[h].float().numpy(), k[h // g_local].float().numpy(), v[h // g_local].float().numpy(),
-                              cfg)
+    for j, h in enumerate(range(s["head_begin"], s["head_end"])):
+        kv = h // g - s["kv_begin"]
+        r = orc.pbs_attention(q[j].float().numpy(), k[kv].float().numpy(), v[kv].float().numpy(), cfg)
         outs.append(torch.from_numpy(r.output))
-    out = torch.stack(outs)
-    if pad_to is not None and out.shape[0] < pad_to:  # bench.py pads the gather to the largest share
-        out = torch.cat([out, torch.zeros(pad_to - out.shape[0], *out.shape[1:])])
-    return out
+    flat = torch.stack(outs).reshape(-1, 128)
+    r0 = s["out_row_begin"] - s["head_begin"] * N_SMALL
+    return s, flat[r0:r0 + s["out_rows"]]
 
 
 def _worker(rank, world, port, path, model):
@@ -58,39 +135,22 @@ def _worker(rank, world, port, path, model):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     bench = _use_model(model)
-    shares = [bench.shard_of(r, world) for r in range(world)]
-    max_local = max(s[1] - s[0] for s in shares)
-    out = _local_outputs(rank, world, model, pad_to=max_local)
-    full = [torch.empty_like(out) for _ in range(world)]
-    dist.all_gather(full, out)
-    if rank == 0:  # drop each rank's padding, in rank order
-        torch.save(torch.cat([f[:s[1] - s[0]] for f, s in zip(full, shares)]), path)
+    full = torch.zeros(bench.HQ * N_SMALL, 128)
+    s, mine = _oracle_rows(model, world, rank)
+    if s["out_rows"]:
+        full[s["out_row_begin"]:s["out_row_begin"] + s["out_rows"]] = mine
+    # the product's exchange: one broadcast of each rank's contiguous rows (all-gather-v)
+    for r in range(world):
+        sr = ops.shard_plan(bench.HQ, bench.HKV, N_SMALL, 128, B_SMALL, world, r)
+        if sr["out_rows"]:
+            view = full[sr["out_row_begin"]:sr["out_row_begin"] + sr["out_rows"]]
+            buf = view.clone()
+            dist.broadcast(buf, src=r)
+            view.copy_(buf)
+    if rank == world - 1:
+        torch.save(full.reshape(bench.HQ, N_SMALL, 128), path)
     dist.barrier()
     dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("model", ["llama", "qwen"])
-def test_shard_arithmetic(model):
-    """Every query head owned exactly once; each local query head reads the KV
-    head of its group; Llama splits whole groups, Qwen's groups of 7 split 3 + 4
-    on 8 ranks with both halves holding the group's KV head."""
-    bench = _use_model(model)
-    g = bench.HQ // bench.HKV
-    for world in (1, 2, 4, 8):
-        owned = []
-        for r in range(world):
-            q0, q1, kv_list, g_local = bench.shard_of(r, world)
-            assert (q1 - q0) == len(kv_list) * g_local
-            for j, h in enumerate(range(q0, q1)):
-                assert kv_list[j // g_local] == h // g
-            owned += list(range(q0, q1))
-        assert owned == list(range(bench.HQ))
-    if model == "qwen":
-        assert [bench.shard_of(r, 8)[1] - bench.shard_of(r, 8)[0] for r in range(8)] == [3, 4] * 4
-    else:
-        assert all(bench.shard_of(r, 8)[3] == 4 for r in range(8))
-    with pytest.raises(ValueError):
-        bench.shard_of(0, bench.HQ + 1)
 
 
 @pytest.fixture(autouse=True)
@@ -104,7 +164,7 @@ def test_multi_rank_gather_matches_single_rank(tmp_path, model, world):
     path = str(tmp_path / "gathered.pt")
     mp.spawn(_worker, args=(world, _free_port(), path, model), nprocs=world, join=True)
     gathered = torch.load(path)
-    single = _local_outputs(0, 1, model)
+    _, single = _oracle_rows(model, 1, 0)
     bench = _use_model(model)
-    assert gathered.shape == single.shape == (bench.HQ, N_SMALL, 128)
-    assert torch.equal(gathered, single)
+    assert gathered.shape == (bench.HQ, N_SMALL, 128)
+    assert torch.equal(gathered.reshape(-1, 128), single)

@@ -605,3 +605,101 @@ def test_host_entry_concurrent_callers(ops):
     for w, g in zip(want, got):
         assert torch.equal(w.output, g.output) and torch.equal(w.pi, g.pi) and torch.equal(w.mask, g.mask)
         assert w.report["selected_blocks"] == g.report["selected_blocks"]
+
+
+# ---- head-parallel shards on the device -------------------
+@pytest.mark.parametrize("hq,hkv,n,world", [(8, 2, 2048, 2), (8, 2, 2048 + 64, 4), (14, 2, 4096, 4),
+                                            (7, 1, 2048, 2), (7, 1, 4096 + 128, 8), (3, 3, 640, 8)])
+def test_shards_reassemble_pbs_attention(ops, hq, hkv, n, world):
+    """Every rank's pbs_attention_shard run one after another on this GPU into
+    one buffer equals the single pbs_attention call bit for bit -- including
+    ranks whose share cuts inside a head (Qwen-like groups of 7) and ranks
+    that need only some KV heads; the reports sum to the single call's."""
+    rng = np.random.default_rng(hq * n + world)
+    tq, tk, tv, *_ = bf16_inputs(rng, hq, hkv, n, 128, kind="vertical_lines")
+    cfg = ops.make_config()
+    want = ops.pbs_attention(tq, tk, tv, cfg)
+    out = torch.zeros_like(tq)
+    sel = 0
+    cuts = 0
+    for r in range(world):
+        s = ops.shard_plan(hq, hkv, n, 128, 128, world, r)
+        if s["out_rows"] == 0:
+            continue
+        cuts += s["qb_begin"] != 0
+        ql = tq[s["head_begin"]:s["head_end"]].contiguous()
+        kl = tk[s["kv_begin"]:s["kv_end"]].contiguous()
+        vl = tv[s["kv_begin"]:s["kv_end"]].contiguous()
+        rep = ops.attention_shard(ql, kl, vl, hq, hkv, cfg, world, r, out, report=True)
+        sel += rep["selected_blocks"]
+    torch.cuda.synchronize()
+    assert torch.equal(out, want.output)
+    assert sel == want.report["selected_blocks"]
+    if hq % world:
+        assert cuts > 0  # the split really cut inside a head
+
+
+def test_dist_context_world_one_matches(ops):
+    """pbs_dist_* with a one-rank NCCL communicator: compute + the (trivial)
+    in-place broadcast equals pbs_attention; the global report matches."""
+    rng = np.random.default_rng(31)
+    tq, tk, tv, *_ = bf16_inputs(rng, 8, 2, 2048, 128, kind="vertical_lines")
+    cfg = ops.make_config()
+    want = ops.pbs_attention(tq, tk, tv, cfg)
+    ctx = ops.DistContext(ops.dist_unique_id(), 1, 0)
+    out = torch.zeros_like(tq)
+    rep = ctx.attention(tq, tk, tv, 8, 2, cfg, out, report=True)
+    torch.cuda.synchronize()
+    ctx.close()
+    assert torch.equal(out, want.output)
+    for key in ("selected_blocks", "total_admissible_blocks"):
+        assert rep[key] == want.report[key]
+    assert abs(rep["block_density"] - want.report["block_density"]) < 1e-12
+
+
+def _two_process_worker(rank, world, port, path):
+    import torch.distributed as dist
+
+    from paper_2510_21270_b200 import ops as o
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    rng = np.random.default_rng(77)
+    hq, hkv, n = 7, 1, 2048
+    tq, tk, tv, *_ = bf16_inputs(rng, hq, hkv, n, 128, kind="vertical_lines")
+    cfg = o.make_config()
+    s = o.shard_plan(hq, hkv, n, 128, 128, world, rank)
+    out = torch.zeros_like(tq)
+    o.attention_shard(tq[s["head_begin"]:s["head_end"]].contiguous(), tk[s["kv_begin"]:s["kv_end"]].contiguous(),
+                      tv[s["kv_begin"]:s["kv_end"]].contiguous(), hq, hkv, cfg, world, rank, out)
+    full = out.cpu().reshape(-1, 128)
+    for r in range(world):  # the all-gather-v over gloo (the product does it with NCCL)
+        sr = o.shard_plan(hq, hkv, n, 128, 128, world, r)
+        view = full[sr["out_row_begin"]:sr["out_row_begin"] + sr["out_rows"]]
+        buf = view.float().clone()
+        dist.broadcast(buf, src=r)
+        view.copy_(buf.to(view.dtype))
+    if rank == 0:
+        want = o.pbs_attention(tq, tk, tv, cfg).output.cpu().reshape(-1, 128)
+        torch.save({"ok": bool(torch.equal(full, want))}, path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_processes_one_gpu_gather(ops, tmp_path):
+    """Two processes (gloo for the exchange) each run their shard of a
+    Qwen-like group of 7 on the device pipeline; the gathered output equals
+    the single-process result bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    path = str(tmp_path / "ok.pt")
+    mp.spawn(_two_process_worker, args=(2, port, path), nprocs=2, join=True)
+    assert torch.load(path)["ok"]
