@@ -182,7 +182,9 @@ PBS_API int pbs_select_blocks_top_k(const float* scores, int32_t num_heads, int6
 
 /* attention_block_sparse (attention.hpp:259-310) with the original-position
  * ElementMask (attention.hpp:41-73): permuted query row i may see permuted key
- * j iff k_orig[j] <= q_orig[i].  q_orig = sigma, k_orig = pi (NULL = identity).
+ * j iff k_orig[j] <= q_orig[i].  q_orig = sigma, k_orig = pi; one of them NULL
+ * = identity on that side; both NULL = no element mask (em == nullptr with
+ * cfg.causal false, attention.hpp:262: every key of a selected block).
  * kv_idx/kv_cnt from pbs_select_blocks (block-level skip, attention.hpp:284-286).
  * kp/vp hold kv_heads heads (kv_heads == Hq for per-q-head permuted K'/V',
  * == Hkv for unpermuted shared K/V).  out_rows (optional) scatters output row
@@ -316,6 +318,16 @@ PBS_API int pbs_tensor_load(const char* path, void* dst, int32_t dst_dtype, void
  * as_stack = 0 writes a 2-D file (heads must be 1). */
 PBS_API int pbs_tensor_save(const char* path, const void* src, int32_t src_dtype, int64_t heads, int64_t rows,
                             int64_t cols, int32_t file_dtype, int32_t as_stack, void* stream);
+
+/* ---- device memory (for FFI callers without the CUDA runtime) ------------ */
+#define PBS_COPY_H2D 0
+#define PBS_COPY_D2H 1
+#define PBS_COPY_D2D 2
+PBS_API int pbs_malloc(size_t bytes, void** ptr);
+PBS_API int pbs_free(void* ptr);
+/* stream-ordered copy; kind = PBS_COPY_*; host memory should be pinned for overlap */
+PBS_API int pbs_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream);
+PBS_API int pbs_stream_synchronize(void* stream);
 
 /* ---- test hooks ---------------------------------------------------------- */
 /* y[i] = the device port of glibc expf (the reference's std::exp(float)). */

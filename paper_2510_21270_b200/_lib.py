@@ -33,6 +33,7 @@ EXPORTS = [
     "pbs_coverage_workspace_size", "pbs_attention_coverage", "pbs_tensor_info_read", "pbs_tensor_load",
     "pbs_tensor_save", "pbs_debug_expf", "pbs_shard_plan", "pbs_shard_workspace_size", "pbs_attention_shard",
     "pbs_dist_unique_id", "pbs_dist_create", "pbs_dist_destroy", "pbs_dist_workspace_size", "pbs_dist_attention",
+    "pbs_malloc", "pbs_free", "pbs_memcpy", "pbs_stream_synchronize",
 ]
 
 
@@ -151,6 +152,10 @@ _SIGS = {
     "pbs_tensor_load": (C.c_int, [C.c_char_p, VP, I32, VP]),
     "pbs_tensor_save": (C.c_int, [C.c_char_p, VP, I32, I64, I64, I64, I32, I32, VP]),
     "pbs_debug_expf": (C.c_int, [VP, VP, I64, VP]),
+    "pbs_malloc": (C.c_int, [SZ, C.POINTER(VP)]),
+    "pbs_free": (C.c_int, [VP]),
+    "pbs_memcpy": (C.c_int, [VP, VP, SZ, I32, VP]),
+    "pbs_stream_synchronize": (C.c_int, [VP]),
     "pbs_shard_plan": (C.c_int, [C.POINTER(Shape), I64, I32, I32, C.POINTER(Shard)]),
     "pbs_shard_workspace_size": (SZ, [C.POINTER(Shape), C.POINTER(PipelineConfig), I32, I32]),
     "pbs_attention_shard": (C.c_int, [VP, VP, VP, C.POINTER(Shape), C.POINTER(PipelineConfig), I32, I32, VP, VP, SZ,

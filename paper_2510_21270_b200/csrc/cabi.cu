@@ -761,8 +761,13 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   const char* hk_ = static_cast<const char*>(k);
   const char* hv_ = static_cast<const char*>(v);
   char* k_all = nullptr;
+  char* q_tail = nullptr;
+  char* imp = nullptr;
+  float* scores = nullptr;
   int32_t* pi_all = nullptr;
+  int32_t* pi_inv = nullptr;
   Timer est_tm(report != nullptr, s_run);
+  const float sc = effective_scale(cfg->scale, (int)d);
   if (est_first) {
     char* p = static_cast<char*>(A.ptr) + (size_t)nslots * slot;
     auto take_b = [&](size_t bytes) {
@@ -771,42 +776,40 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
       return r;
     };
     k_all = take_b(kall_b);
-    char* q_tail = take_b(qtail_b);
-    char* imp = take_b(imp_b);
-    float* scores = reinterpret_cast<float*>(take_b((size_t)hq * n * 4));
+    q_tail = take_b(qtail_b);
+    imp = take_b(imp_b);
+    scores = reinterpret_cast<float*>(take_b((size_t)hq * n * 4));
     pi_all = reinterpret_cast<int32_t*>(take_b((size_t)hq * n * 4));
-    int32_t* pi_inv = reinterpret_cast<int32_t*>(take_b((size_t)hq * n * 4));
-    // the last `take` rows of every query head, then K one KV head at a time:
-    // each head's logits start as soon as its keys have landed, so the copy of
-    // K overlaps the estimate's GEMM
+    pi_inv = reinterpret_cast<int32_t*>(take_b((size_t)hq * n * 4));
     while (A.ev_k.size() < (size_t)hkv) {
       cudaEvent_t e;
       PBS_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       A.ev_k.push_back(e);
     }
-    PBS_CUDA_CHECK(cudaMemcpy2DAsync(q_tail, (size_t)take * d * es, hq_ + (size_t)(n - take) * d * es,
-                                     (size_t)n * d * es, (size_t)take * d * es, (size_t)hq, cudaMemcpyHostToDevice,
-                                     s_in));
-    for (int64_t c = 0; c < hkv; ++c) {
-      PBS_CUDA_CHECK(cudaMemcpyAsync(k_all + (size_t)c * kvb, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
-      PBS_CUDA_CHECK(cudaEventRecord(A.ev_k[c], s_in));
-    }
-    const float sc = effective_scale(cfg->scale, (int)d);
-    for (int64_t c = 0; c < hkv; ++c) {
+  }
+  // estimate of the query heads of KV groups [c0, c1) (stage 1 reads only K and
+  // the last `take` query rows): logits per group as its keys land, then the
+  // exps / denominators / scores and the segmented sort for those heads
+  auto estimate_groups = [&](int64_t c0, int64_t c1) -> int {
+    for (int64_t c = c0; c < c1; ++c) {
       PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_k[c], 0));
-      if (c == 0) est_tm.mark();
+      if (c == c0) est_tm.mark();
       if (int rc = launch_importance_logits(q_tail, k_all, shape->dtype, (int)hq, (int)hkv, (int)(c * g), (int)g, n,
                                             (int)d, cfg->block_size, sc, imp, imp_b, s_run, take))
         return rc;
     }
-    if (int rc = launch_importance_finish((int)hq, n, cfg->block_size, scores, imp, imp_b, s_run)) return rc;
-    if (int rc = launch_segmented_sort(scores, 0, (int)hq, n, cfg->segment_size, pi_all, pi_inv, s_run)) return rc;
+    const int h0 = (int)(c0 * g), nh = (int)((c1 - c0) * g);
+    if (int rc = launch_importance_finish((int)hq, h0, nh, n, cfg->block_size, scores, imp, imp_b, s_run)) return rc;
+    if (int rc = launch_segmented_sort(scores + (size_t)h0 * n, 0, nh, n, cfg->segment_size, pi_all + (size_t)h0 * n,
+                                       pi_inv + (size_t)h0 * n, s_run))
+      return rc;
     est_tm.mark();
-  }
+    return PBS_OK;
+  };
   char* ho_ = static_cast<char*>(out);
   pbs_report total{};
   double dens = 0.0, cov = 0.0;
-  // pinned report counters per slot: kv_cnt (int32), row_cov (double), status
+  // pinned report counters per chunk parity: kv_cnt (int32), row_cov (double), status
   const size_t rep_bytes = al((size_t)g * t * 4) + al((size_t)g * t * 8) + 256;
   if (report && A.pinned_bytes < rep_bytes * 2) {
     if (A.pinned) cudaFreeHost(A.pinned);
@@ -820,14 +823,29 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   auto rep_hs = [&](int i) {
     return reinterpret_cast<int32_t*>(A.pinned + i * rep_bytes + al((size_t)g * t * 4) + al((size_t)g * t * 8));
   };
-  // fold the report of group c (its counters were fetched on s_run) into the total
-  auto fold = [&](int64_t c) -> int {
-    const int i = (int)(c % nslots);
+  // Work chunks: one per KV group, except that the LAST group (key_permute, pi
+  // precomputed) runs in up to 4 head slices, so the output of one slice goes
+  // back to the host while the next computes and the drain after the last
+  // kernel is one slice, not one group.
+  struct Chunk {
+    int64_t c, a, b;  // KV group c, its query heads [a, b) (local to the group)
+  };
+  std::vector<Chunk> chunks;
+  for (int64_t c = 0; c < hkv; ++c) {
+    const int64_t parts = (est_first && c == hkv - 1) ? std::min<int64_t>(g, 4) : 1;
+    for (int64_t j = 0; j < parts; ++j) chunks.push_back(Chunk{c, j * g / parts, (j + 1) * g / parts});
+  }
+  // fold the report of chunk kk (its counters were fetched on s_run) into the total
+  auto fold = [&](size_t kk) -> int {
+    const int i = (int)(kk % 2);
+    const Chunk& ch = chunks[kk];
+    pbs_shape cs2 = cs;
+    cs2.num_q_heads = (int32_t)(ch.b - ch.a);
     PBS_CUDA_CHECK(cudaEventSynchronize(A.ev_rep[i]));
     pbs_report r{};
-    if (int rc = report_build(&cs, cfg, rep_cnt(i), rep_cov(i), rep_hs(i), *A.timer[i], &r)) {
+    if (int rc = report_build(&cs2, cfg, rep_cnt(i), rep_cov(i), rep_hs(i), *A.timer[i], &r)) {
       if (rc == PBS_ERR_DEGENERATE) {  // name the head in the whole problem
-        const int32_t hfull = (int32_t)(c * g + rep_hs(i)[1] / t);
+        const int32_t hfull = (int32_t)(ch.c * g + ch.a + rep_hs(i)[1] / t);
         return fail(PBS_ERR_DEGENERATE, "E_DEGENERATE",
                     "query block " + std::to_string(rep_hs(i)[1] % t) + " (head " + std::to_string(hfull) +
                         ") has an empty softmax denominator (all keys masked)");
@@ -836,8 +854,8 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     }
     total.selected_blocks += r.selected_blocks;
     total.total_admissible_blocks += r.total_admissible_blocks;
-    dens += r.block_density;
-    cov += r.pooled_score_coverage;
+    dens += r.block_density * (double)(ch.b - ch.a);
+    cov += r.pooled_score_coverage * (double)(ch.b - ch.a);
     total.causal_density_baseline = r.causal_density_baseline;
     total.estimate_us += r.estimate_us;
     total.permute_us += r.permute_us;
@@ -855,49 +873,119 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     PBS_CUDA_CHECK(cudaEventRecord(A.ev_in[c % nslots], s_in));
     return PBS_OK;
   };
-  if (int rc = copy_in(0)) return rc;
-  for (int64_t c = 0; c < hkv; ++c) {
+  if (est_first) {
+    // Fill order: the last `take` rows of every query head, K of group 0, then
+    // group 0's Q and V, then the other groups' K.  Group 0 is estimated alone
+    // and starts as soon as its own inputs are in; the other groups' estimate
+    // runs after it, while their K (and group 1's Q, V) stream in.
+    PBS_CUDA_CHECK(cudaMemcpy2DAsync(q_tail, (size_t)take * d * es, hq_ + (size_t)(n - take) * d * es,
+                                     (size_t)n * d * es, (size_t)take * d * es, (size_t)hq, cudaMemcpyHostToDevice,
+                                     s_in));
+    PBS_CUDA_CHECK(cudaMemcpyAsync(k_all, hk_, kvb, cudaMemcpyHostToDevice, s_in));
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_k[0], s_in));
+    if (int rc = copy_in(0)) return rc;
+    for (int64_t c = 1; c < hkv; ++c) {
+      PBS_CUDA_CHECK(cudaMemcpyAsync(k_all + (size_t)c * kvb, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
+      PBS_CUDA_CHECK(cudaEventRecord(A.ev_k[c], s_in));
+    }
+    if (int rc = estimate_groups(0, 1)) return rc;
+  } else {
+    if (int rc = copy_in(0)) return rc;
+  }
+  for (size_t kk = 0; kk < chunks.size(); ++kk) {
+    const Chunk& ch = chunks[kk];
+    const int64_t c = ch.c;
     const int i = (int)(c % nslots);
+    const int ri = (int)(kk % 2);
     Slot& S = sl[i];
-    if (c + 1 < hkv && nslots > 1)
-      if (int rc = copy_in(c + 1)) return rc;
-    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_in[i], 0));
-    Timer& tm = *A.timer[i];
+    const bool first_of_group = ch.a == 0;
+    if (first_of_group) {
+      if (c + 1 < hkv && nslots > 1)
+        if (int rc = copy_in(c + 1)) return rc;
+      if (est_first && c == 1)
+        if (int rc = estimate_groups(1, hkv)) return rc;
+      PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_in[i], 0));
+    }
+    pbs_shape cs2 = cs;
+    cs2.num_q_heads = (int32_t)(ch.b - ch.a);
+    const size_t qoff = (size_t)ch.a * n * d * es, poff = (size_t)ch.a * n, moff = (size_t)ch.a * t * t;
+    const size_t qbytes = (size_t)(ch.b - ch.a) * n * d * es, pbytes = (size_t)(ch.b - ch.a) * n * 4,
+                 mbytes = (size_t)(ch.b - ch.a) * t * t;
+    Timer& tm = *A.timer[ri];
     tm.restart(s_run);
     tm.on = report != nullptr;
-    const int32_t* pi_c = est_first ? pi_all + (size_t)c * g * n : nullptr;
-    if (int rc = pipeline_enqueue(S.q, est_first ? k_all + (size_t)c * kvb : S.k, S.v, &cs, cfg, S.out,
-                                  sigma ? S.sig : nullptr, (pi && !est_first) ? S.pi : nullptr,
-                                  mask ? S.mask : nullptr, S.ws, ws, tm, s_run, pi_c))
+    const int32_t* pi_c = est_first ? pi_all + (size_t)c * g * n + poff : nullptr;
+    if (int rc = pipeline_enqueue(S.q + qoff, est_first ? k_all + (size_t)c * kvb : S.k, S.v, &cs2, cfg, S.out + qoff,
+                                  sigma ? S.sig + poff : nullptr, (pi && !est_first) ? S.pi + poff : nullptr,
+                                  mask ? S.mask + moff : nullptr, S.ws, ws, tm, s_run, pi_c))
       return rc;
     if (report) {
-      if (int rc = report_fetch(&cs, cfg, S.ws, rep_cnt(i), rep_cov(i), rep_hs(i), s_run)) return rc;
-      PBS_CUDA_CHECK(cudaEventRecord(A.ev_rep[i], s_run));
+      if (int rc = report_fetch(&cs2, cfg, S.ws, rep_cnt(ri), rep_cov(ri), rep_hs(ri), s_run)) return rc;
+      PBS_CUDA_CHECK(cudaEventRecord(A.ev_rep[ri], s_run));
     }
-    PBS_CUDA_CHECK(cudaEventRecord(A.ev_done[i], s_run));
-    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_out, A.ev_done[i], 0));
-    PBS_CUDA_CHECK(cudaMemcpyAsync(ho_ + (size_t)c * qb, S.out, qb, cudaMemcpyDeviceToHost, s_out));
-    if (sigma) PBS_CUDA_CHECK(cudaMemcpyAsync(sigma + (size_t)c * g * n, S.sig, pb, cudaMemcpyDeviceToHost, s_out));
+    PBS_CUDA_CHECK(cudaEventRecord(A.ev_done[ri], s_run));
+    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_out, A.ev_done[ri], 0));
+    const size_t hoff = (size_t)c * g + ch.a;  // first query head of the chunk
+    PBS_CUDA_CHECK(cudaMemcpyAsync(ho_ + hoff * n * d * es, S.out + qoff, qbytes, cudaMemcpyDeviceToHost, s_out));
+    if (sigma)
+      PBS_CUDA_CHECK(cudaMemcpyAsync(sigma + hoff * n, S.sig + poff, pbytes, cudaMemcpyDeviceToHost, s_out));
     if (pi)
-      PBS_CUDA_CHECK(cudaMemcpyAsync(pi + (size_t)c * g * n, est_first ? pi_c : S.pi, pb, cudaMemcpyDeviceToHost, s_out));
-    if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask + (size_t)c * mb, S.mask, mb, cudaMemcpyDeviceToHost, s_out));
+      PBS_CUDA_CHECK(cudaMemcpyAsync(pi + hoff * n, est_first ? pi_c : S.pi + poff, pbytes, cudaMemcpyDeviceToHost,
+                                     s_out));
+    if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask + hoff * t * t, S.mask + moff, mbytes, cudaMemcpyDeviceToHost, s_out));
     PBS_CUDA_CHECK(cudaEventRecord(A.ev_out[i], s_out));
-    // the previous group's report, while this one computes (its slot's
-    // counters are overwritten only two groups later, after this fold)
-    if (report && c > 0)
-      if (int rc = fold(c - 1)) return rc;
-    if (nslots == 1 && c + 1 < hkv) {
+    // the previous chunk's report, while this one computes (its counters are
+    // overwritten only two chunks later, after this fold)
+    if (report && kk > 0)
+      if (int rc = fold(kk - 1)) return rc;
+    const bool last_of_group = ch.b == g;
+    if (nslots == 1 && last_of_group && c + 1 < hkv) {
       PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
       if (int rc = copy_in(c + 1)) return rc;
     }
   }
-  if (report && hkv > 0)
-    if (int rc = fold(hkv - 1)) return rc;
-  if (report && est_first) total.estimate_us += est_tm.us(0);  // events complete: every fold synchronised later work
+  if (report && !chunks.empty())
+    if (int rc = fold(chunks.size() - 1)) return rc;
+  if (report && est_first) {  // events complete: every fold synchronised later work
+    total.estimate_us += est_tm.us(0);
+    if (hkv > 1) total.estimate_us += est_tm.us(2);
+  }
   PBS_CUDA_CHECK(cudaStreamSynchronize(s_out));
-  total.block_density = dens / (double)hkv;
-  total.pooled_score_coverage = cov / (double)hkv;
+  total.block_density = dens / (double)hq;
+  total.pooled_score_coverage = cov / (double)hq;
   if (report) *report = total;
+  return PBS_OK;
+}
+
+// ---- device memory for C-ABI callers without the CUDA runtime (FFI bindings,
+// the pbs:: drop-in header); the hot calls themselves never allocate
+int pbs_malloc(size_t bytes, void** ptr) {
+  if (!ptr) return fail(PBS_ERR_CONFIG, "E_CONFIG", "null pointer");
+  *ptr = nullptr;
+  if (bytes == 0) return PBS_OK;
+  const cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaErrorMemoryAllocation)
+    return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "device allocation of " + std::to_string(bytes) + " bytes failed");
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  return PBS_OK;
+}
+
+int pbs_free(void* ptr) {
+  if (ptr) PBS_CUDA_CHECK(cudaFree(ptr));
+  return PBS_OK;
+}
+
+int pbs_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream) {
+  if (bytes == 0) return PBS_OK;
+  const cudaMemcpyKind k = kind == PBS_COPY_H2D ? cudaMemcpyHostToDevice
+                           : kind == PBS_COPY_D2H ? cudaMemcpyDeviceToHost
+                                                  : cudaMemcpyDeviceToDevice;
+  PBS_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, k, as_stream(stream)));
+  return PBS_OK;
+}
+
+int pbs_stream_synchronize(void* stream) {
+  PBS_CUDA_CHECK(cudaStreamSynchronize(as_stream(stream)));
   return PBS_OK;
 }
 

@@ -21,8 +21,9 @@ int launch_importance(const void* q, const void* k, int dtype, int hq, int hkv, 
 int launch_importance_logits(const void* q, const void* k, int dtype, int hq, int hkv, int h0, int nh, int64_t n,
                              int d, int64_t block, float scale, void* ws, size_t ws_bytes, cudaStream_t st,
                              int64_t q_rows = 0);
-int launch_importance_finish(int hq, int64_t n, int64_t block, float* scores, void* ws, size_t ws_bytes,
-                             cudaStream_t st);
+// exps, denominators and scores of heads [h0, h0 + nh) of an hq-head workspace
+int launch_importance_finish(int hq, int h0, int nh, int64_t n, int64_t block, float* scores, void* ws,
+                             size_t ws_bytes, cudaStream_t st);
 // per segment stable sort; primary_keys: 0 = descending f32 scores, 1 = ascending u32 groups
 int launch_segmented_sort(const void* keys, int key_kind, int heads, int64_t n, int64_t segment,
                           int32_t* perm, int32_t* inv, cudaStream_t st);

@@ -14,11 +14,15 @@ output PBST in the manifest's precision and the report document
 {"aggregate": ..., "heads": [...]} with report_to_json's fixed fields
 (manifest.hpp:174-186) and aggregate_reports' rules (pbs_main.cpp:124-144).
 
-Differences, by design: the device computes in bf16 whatever `precision`
-says (precision picks the output file's dtype); there is no N^2 limit on the
-coverage (pbs_main.cpp:202-207 refuses N^2 > 2^26 on the CPU); `workload`
-manifests (the reference's synthetic generator) are refused -- generate the
-tensors with the reference and pass them as `inputs`.
+Precision: `f32` manifests run the device's f32 path (the reference's f32
+arithmetic: permutations and masks bit-exact, outputs within 1e-4).  The device
+has no f64 path, so an `f64` manifest (the reference default, pipeline.hpp:35)
+is refused with E_CONFIG unless the caller opts into a lower device precision
+(`--device-precision f32|bf16`, or run_manifest(device_precision=...)); the
+output file keeps the manifest's dtype.  Other differences, by design: there is
+no N^2 limit on the coverage (pbs_main.cpp:202-207 refuses N^2 > 2^26 on the
+CPU); `workload` manifests (the reference's synthetic generator) are refused --
+generate the tensors with the reference and pass them as `inputs`.
 """
 from __future__ import annotations
 
@@ -159,7 +163,21 @@ def aggregate_reports(heads: list) -> dict:
     return agg
 
 
-def run_manifest(m: RunManifest, base_dir=".") -> dict:
+def device_dtype(m: RunManifest, device_precision=None):
+    """The device element type for a manifest: its own precision when the device
+    has it (f32), else the caller's explicit choice; f64 alone is refused."""
+    import torch
+
+    choice = device_precision or m.precision
+    if choice == "f32":
+        return torch.float32
+    if choice == "bf16":
+        return torch.bfloat16
+    raise _config_error("precision f64 is not supported by the B200 device path (pass --device-precision f32 or "
+                        "bf16 to run an f64 manifest at lower precision)")
+
+
+def run_manifest(m: RunManifest, base_dir=".", device_precision=None) -> dict:
     """The CLI's `run` (pbs_main.cpp:197-232) on the GPU; returns the report document."""
     import torch
 
@@ -180,7 +198,8 @@ def run_manifest(m: RunManifest, base_dir=".") -> dict:
         raise _config_error(f"pipeline expects self-attention: N == M, got {qr} vs {kr}")
     if qc != kc or kr != vr or vc != kc:
         raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: pipeline inputs have inconsistent shapes")
-    q, k, v = (ops.load_tensor(resolve(x), dtype=torch.bfloat16) for x in (m.q, m.k, m.v))
+    dt = device_dtype(m, device_precision)
+    q, k, v = (ops.load_tensor(resolve(x), dtype=dt) for x in (m.q, m.k, m.v))
     from_stack = any(i["ndim"] == 3 for i in infos)
     q, k, v = (x if x.dim() == 3 else x.unsqueeze(0) for x in (q, k, v))
     cfg = m.config()
@@ -217,17 +236,17 @@ def format_sweep_csv(rows) -> str:
     return "".join(out)
 
 
-def sweep_manifest(m: RunManifest, base_dir=".", taus=(), segments=(), strategies=(), out_path="") -> str:
+def sweep_manifest(m: RunManifest, base_dir=".", taus=(), segments=(), strategies=(), out_path="",
+                   device_precision=None) -> str:
     """The CLI's `sweep` (pbs_main.cpp:248-267): density_sweep of head 0 for every
     strategy (sorted, unique), defaults from the manifest's pipeline."""
-    import torch
-
     from . import ops
 
     def resolve(p):
         return p if os.path.isabs(p) else os.path.join(base_dir, p)
 
-    q, k, v = (ops.load_tensor(resolve(x), dtype=torch.bfloat16) for x in (m.q, m.k, m.v))
+    dt = device_dtype(m, device_precision)
+    q, k, v = (ops.load_tensor(resolve(x), dtype=dt) for x in (m.q, m.k, m.v))
     q, k, v = (x[:1] if x.dim() == 3 else x.unsqueeze(0) for x in (q, k, v))
     taus = list(taus) or [m.tau]
     segments = list(segments) or [m.segment_size]
@@ -252,22 +271,26 @@ def main(argv=None) -> int:
     sub = ap.add_subparsers(dest="cmd", required=True)
     r = sub.add_parser("run", help="Run the pipeline per head and write reports")
     r.add_argument("--manifest", required=True)
+    r.add_argument("--device-precision", choices=["f32", "bf16"], default=None,
+                   help="device element type (default: the manifest's precision; f64 needs this)")
     sw = sub.add_parser("sweep", help="Density/coverage/error sweep as CSV")
     sw.add_argument("--manifest", required=True)
     sw.add_argument("--tau-list", default="")
     sw.add_argument("--segment-list", default="")
     sw.add_argument("--strategies", default="")
     sw.add_argument("--out", default="")
+    sw.add_argument("--device-precision", choices=["f32", "bf16"], default=None)
     args = ap.parse_args(argv)
     try:
         m = load_manifest(args.manifest)
         base = os.path.dirname(os.path.abspath(args.manifest))
         if args.cmd == "run":
-            run_manifest(m, base)
+            run_manifest(m, base, args.device_precision)
         else:
             split = lambda s: [x for x in s.split(",") if x]  # noqa: E731
             sweep_manifest(m, base, [float(x) for x in split(args.tau_list)],
-                           [int(x) for x in split(args.segment_list)], split(args.strategies), args.out)
+                           [int(x) for x in split(args.segment_list)], split(args.strategies), args.out,
+                           args.device_precision)
     except _lib.PbsError as e:  # the CLI's stderr line and exit code (pbs_main.cpp:467-480)
         sys.stderr.write(str(e) + "\n")
         return e.code

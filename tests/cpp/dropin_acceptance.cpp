@@ -1,0 +1,339 @@
+// dropin_acceptance.cpp -- the reference's own acceptance / pipeline criteria
+// run through the pbs:: drop-in (include/pbs_dropin.hpp) on the device,
+// compiled against the UNMODIFIED reference headers and its test utilities.
+// TEST INFRASTRUCTURE: the reference's pbs::* functions are the checker here.
+//
+// One "[PASS] name" / "[FAIL] name: detail" line per criterion; the exit code
+// is the failure count (the acceptance suite's convention,
+// tests/acceptance/acceptance_main.cpp:505-523).  f32 instances throughout: the
+// device has no f64 path (the drop-in refuses T = double, checked below).
+//
+//   criteria re-expressed (reference file:line):
+//   P1  pbs_attention parity: sigma, pi, mask, counts equal to pbs::pbs_attention<float>,
+//       outputs within 1e-4 (pipeline.hpp:107-193), four strategies, three workloads
+//   C3  kernel equivalence, square shapes: full-mask block-sparse == oracle within
+//       kernel_tol<float> (acceptance_main.cpp:123-156)
+//   C4  tau = 1 exactness across strategies and segment sizes (acceptance_main.cpp:165-199;
+//       pipeline_test.cpp:27-55 at n = 96, d = 8, b = 16)
+//   C5  bitwise causality under key permutation (acceptance_main.cpp:201-229)
+//   G   GoldenRun256's workload and config (pipeline_test.cpp:79-103): density and
+//       permutations equal to the reference's f32 run
+//   OPS estimate / key permutation / block scores / selection bit-exact
+//   COV attention_coverage within 1e-5 of the reference (pipeline.hpp:198-243)
+//   DEG degenerate row -> DegenerateRowError(1) (attention_test.cpp:261-282)
+//   F64 T = double refused with pbs::ConfigError
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "pbs/attention.hpp"
+#include "pbs/block_selection.hpp"
+#include "pbs/matrix.hpp"
+#include "pbs/permutation.hpp"
+#include "pbs/pipeline.hpp"
+#include "pbs/rng.hpp"
+#include "pbs/workload.hpp"
+#include "pbs_dropin.hpp"
+#include "testutil.hpp"
+
+using pbs::AttentionConfig;
+using pbs::Matrix;
+
+namespace {
+
+struct Check {
+  bool ok = true;
+  std::string detail;
+  void require(bool cond, const std::string& msg) {
+    if (!cond && ok) {
+      ok = false;
+      detail = msg;
+    }
+  }
+};
+
+const pbs::PermutationStrategy kStrategies[] = {pbs::PermutationStrategy::none, pbs::PermutationStrategy::key_permute,
+                                                pbs::PermutationStrategy::query_permute,
+                                                pbs::PermutationStrategy::both};
+
+void parity_case(Check& c, const Matrix<float>& q, const Matrix<float>& k, const Matrix<float>& v,
+                 const pbs::PipelineConfig& cfg, const std::string& tag) {
+  const auto want = pbs::pbs_attention(q, k, v, cfg);
+  const auto got = pbs::b200::pbs_attention(q, k, v, cfg);
+  c.require(got.sigma.map() == want.sigma.map(), tag + ": sigma differs");
+  c.require(got.pi.map() == want.pi.map(), tag + ": pi differs");
+  c.require(got.mask == want.mask, tag + ": mask differs");
+  c.require(got.report.selected_blocks == want.report.selected_blocks, tag + ": selected_blocks differs");
+  c.require(got.report.total_admissible_blocks == want.report.total_admissible_blocks, tag + ": admissible differs");
+  c.require(got.report.block_density == want.report.block_density, tag + ": density differs");
+  const double err = pbs::max_abs_diff(got.output, want.output);
+  c.require(err <= 1e-4, tag + ": output max err " + std::to_string(err));
+}
+
+Check p1_parity() {
+  Check c;
+  pbs::Rng rng(2001);
+  for (const auto kind : {pbs::WorkloadKind::vertical_lines, pbs::WorkloadKind::mixed, pbs::WorkloadKind::gaussian}) {
+    pbs::WorkloadSpec spec;
+    spec.kind = kind;
+    spec.n = 1024 + 77;
+    spec.d = 64;
+    spec.seed = 7;
+    spec.line_count = 16;
+    const auto w = pbs::generate_workload<float>(spec, 64, 256);
+    for (const auto st : kStrategies) {
+      pbs::PipelineConfig cfg;
+      cfg.block_size = 64;
+      cfg.segment_size = st == pbs::PermutationStrategy::none ? 0 : 256;
+      cfg.tau = 0.9;
+      cfg.strategy = st;
+      cfg.precision = pbs::Precision::f32;
+      parity_case(c, w.q[0], w.k[0], w.v[0], cfg,
+                  std::string(pbs::workload_kind_name(kind)) + "/" + pbs::strategy_name(st));
+      if (!c.ok) return c;
+    }
+  }
+  // the reference's own defaults (B = 128, S = 256) at the tensor-core shape d = 128
+  const auto q = testutil::random_matrix<float>(2048, 128, rng);
+  const auto k = testutil::random_matrix<float>(2048, 128, rng);
+  const auto v = testutil::random_matrix<float>(2048, 128, rng);
+  pbs::PipelineConfig cfg;
+  cfg.precision = pbs::Precision::f32;
+  parity_case(c, q, k, v, cfg, "defaults d128");
+  return c;
+}
+
+Check c3_kernel_equivalence() {
+  Check c;
+  pbs::Rng rng(1003);
+  struct Case {
+    std::size_t n, d, b;
+  };
+  for (const Case cs : {Case{7, 4, 16}, Case{33, 16, 16}, Case{257, 64, 32}, Case{1024, 64, 128}}) {
+    for (const bool causal : {false, true}) {
+      const auto q = testutil::random_matrix<float>(cs.n, cs.d, rng);
+      const auto k = testutil::random_matrix<float>(cs.n, cs.d, rng);
+      const auto v = testutil::random_matrix<float>(cs.n, cs.d, rng);
+      const auto cfg = AttentionConfig::make(cs.b, cs.d, causal);
+      const auto oracle = pbs::attention_oracle(q, k, v, cfg);
+      const std::size_t t = (cs.n + cs.b - 1) / cs.b;
+      const auto sparse = pbs::b200::attention_block_sparse(q, k, v, cfg, pbs::BlockMask::full(t, t, cs.b));
+      const double diff = pbs::max_abs_diff(sparse, oracle);
+      c.require(diff <= testutil::kernel_tol<float>(),
+                "full-mask sparse vs oracle diff " + std::to_string(diff) + " at n=" + std::to_string(cs.n) +
+                    " b=" + std::to_string(cs.b) + (causal ? " causal" : ""));
+      if (!c.ok) return c;
+    }
+  }
+  return c;
+}
+
+void tau_one(Check& c, std::size_t n, std::size_t d, std::size_t b, pbs::Rng& rng) {
+  const auto q = testutil::random_matrix<float>(n, d, rng);
+  const auto k = testutil::random_matrix<float>(n, d, rng);
+  const auto v = testutil::random_matrix<float>(n, d, rng);
+  const auto oracle = pbs::attention_oracle(q, k, v, AttentionConfig::make(b, d, true));
+  std::vector<Matrix<float>> outs;
+  for (const auto st : kStrategies)
+    for (const std::size_t s : {b, 2 * b, 4 * b}) {
+      pbs::PipelineConfig cfg;
+      cfg.block_size = b;
+      cfg.segment_size = s;
+      cfg.tau = 1.0;
+      cfg.strategy = st;
+      const auto res = pbs::b200::pbs_attention(q, k, v, cfg);
+      const double diff = pbs::max_abs_diff(res.output, oracle);
+      c.require(diff <= testutil::kernel_tol<float>(), std::string("strategy ") + pbs::strategy_name(st) + " S=" +
+                                                           std::to_string(s) + " n=" + std::to_string(n) + " diff " +
+                                                           std::to_string(diff));
+      outs.push_back(res.output);
+      if (!c.ok) return;
+    }
+  for (const auto& a : outs)
+    for (const auto& b2 : outs)
+      c.require(pbs::max_abs_diff(a, b2) <= 2 * testutil::kernel_tol<float>(), "strategies disagree");
+}
+
+Check c4_tau_one() {
+  Check c;
+  pbs::Rng rng(1004);
+  tau_one(c, 512, 32, 64, rng);
+  pbs::Rng rng2(51);
+  if (c.ok) tau_one(c, 96, 8, 16, rng2);
+  return c;
+}
+
+Check c5_causality() {
+  Check c;
+  pbs::Rng rng(1005);
+  for (int it = 0; it < 50 && c.ok; ++it) {
+    const std::size_t b = 8 + 8 * rng.index(2);
+    const std::size_t n = b * (4 + rng.index(8));
+    const std::size_t d = 4 + 4 * rng.index(2);
+    pbs::PipelineConfig cfg;
+    cfg.block_size = b;
+    cfg.segment_size = 2 * b;
+    cfg.tau = 0.5 + 0.5 * rng.uniform();
+    cfg.strategy = pbs::PermutationStrategy::key_permute;
+    const auto q = testutil::random_matrix<float>(n, d, rng);
+    const auto k = testutil::random_matrix<float>(n, d, rng);
+    auto v = testutil::random_matrix<float>(n, d, rng);
+    const auto base = pbs::b200::pbs_attention(q, k, v, cfg);
+    const std::size_t j = 1 + rng.index(n - 1);
+    for (std::size_t col = 0; col < d; ++col) v(j, col) = -v(j, col) + 50.0f;
+    const auto pert = pbs::b200::pbs_attention(q, k, v, cfg);
+    for (std::size_t i = 0; i < j && c.ok; ++i)
+      for (std::size_t col = 0; col < d; ++col)
+        c.require(base.output(i, col) == pert.output(i, col),
+                  "row " + std::to_string(i) + " changed after perturbing value row " + std::to_string(j));
+  }
+  return c;
+}
+
+Check golden256() {
+  Check c;
+  pbs::WorkloadSpec spec;
+  spec.kind = pbs::WorkloadKind::gaussian;
+  spec.n = 256;
+  spec.d = 16;
+  spec.seed = 13;
+  const auto w = pbs::generate_workload<float>(spec, 32, 64);
+  pbs::PipelineConfig cfg;
+  cfg.block_size = 32;
+  cfg.segment_size = 64;
+  cfg.tau = 0.9;
+  cfg.strategy = pbs::PermutationStrategy::key_permute;
+  parity_case(c, w.q[0], w.k[0], w.v[0], cfg, "golden256");
+  const auto got = pbs::b200::pbs_attention(w.q[0], w.k[0], w.v[0], cfg);
+  const auto oracle = pbs::attention_oracle(w.q[0], w.k[0], w.v[0], AttentionConfig::make(32, 16, true));
+  const double err = pbs::max_abs_diff(got.output, oracle);
+  c.require(err <= 1e-5, "golden256 max err vs causal oracle " + std::to_string(err));
+  c.detail = " (density " + std::to_string(got.report.block_density) + ")";
+  return c;
+}
+
+Check ops_bitexact() {
+  Check c;
+  pbs::WorkloadSpec spec;
+  spec.kind = pbs::WorkloadKind::vertical_lines;
+  spec.n = 2048;
+  spec.d = 64;
+  spec.seed = 3;
+  spec.line_count = 12;
+  const auto w = pbs::generate_workload<float>(spec, 64, 128);
+  const auto& q = w.q[0];
+  const auto& k = w.k[0];
+  const auto acfg = AttentionConfig::make(64, 64);
+  const auto want = pbs::estimate_key_importance(q, k, acfg);
+  const auto got = pbs::b200::estimate_key_importance(q, k, acfg);
+  c.require(got.scores == want.scores, "importance scores differ");
+  c.require(got.source_query_block == want.source_query_block, "source query block differs");
+  const auto pw = pbs::build_key_permutation(want, 128).flatten();
+  const auto pg = pbs::b200::build_key_permutation(got, 128).flatten();
+  c.require(pw.map() == pg.map(), "key permutation differs");
+  const auto kp = pbs::apply_rows(pw, k);
+  const std::size_t t = 2048 / 64;
+  const auto causal = pbs::build_block_causal_mask<float>(t, t, 64, 128);
+  const auto bw = pbs::meanpool_block_scores(q, kp, 64, 128, causal);
+  const auto bg = pbs::b200::meanpool_block_scores(q, kp, 64, 128, causal);
+  c.require(bw.scores == bg.scores, "block scores differ");
+  for (const double tau : {0.0, 0.5, 0.9, 1.0}) {
+    c.require(pbs::select_blocks(bw, tau) == pbs::b200::select_blocks(bg, tau),
+              "selection differs at tau " + std::to_string(tau));
+  }
+  return c;
+}
+
+Check coverage() {
+  Check c;
+  pbs::Rng rng(77);
+  const auto q = testutil::random_matrix<float>(1024, 64, rng);
+  const auto k = testutil::random_matrix<float>(1024, 64, rng);
+  const auto v = testutil::random_matrix<float>(1024, 64, rng);
+  pbs::PipelineConfig cfg;
+  cfg.block_size = 64;
+  cfg.segment_size = 128;
+  cfg.tau = 0.7;
+  const auto res = pbs::pbs_attention(q, k, v, cfg);
+  const double want = pbs::attention_coverage(q, k, res.mask, res.sigma, res.pi);
+  const double got = pbs::b200::attention_coverage(q, k, res.mask, res.sigma, res.pi);
+  c.require(std::fabs(got - want) <= 1e-5, "coverage " + std::to_string(got) + " vs " + std::to_string(want));
+  return c;
+}
+
+Check degenerate() {
+  Check c;
+  pbs::Rng rng(30);
+  const std::size_t n = 8, d = 2, b = 2;
+  const auto q = testutil::random_matrix<float>(n, d, rng);
+  const auto k = testutil::random_matrix<float>(n, d, rng);
+  const auto v = testutil::random_matrix<float>(n, d, rng);
+  const auto cfg = AttentionConfig::make(b, d);
+  const auto em = pbs::ElementMask::identity(n, n);
+  pbs::BlockMask mask(4, 4, b, 0);
+  for (std::size_t i = 0; i < 4; ++i)
+    for (std::size_t j = 0; j <= i; ++j) mask.set(i, j, true);
+  mask.set(1, 0, false);
+  mask.set(1, 1, false);
+  mask.set(1, 3, true);
+  try {
+    pbs::b200::attention_block_sparse(q, k, v, cfg, mask, &em);
+    c.require(false, "expected DegenerateRowError");
+  } catch (const pbs::DegenerateRowError& e) {
+    c.require(e.query_block() == 1u, "query block " + std::to_string(e.query_block()));
+  }
+  return c;
+}
+
+Check f64_refused() {
+  Check c;
+  pbs::Rng rng(5);
+  const auto q = testutil::random_matrix<double>(64, 8, rng);
+  try {
+    pbs::b200::pbs_attention(q, q, q, pbs::PipelineConfig{});
+    c.require(false, "f64 was not refused");
+  } catch (const pbs::ConfigError& e) {
+    c.require(std::string(e.what()).find("f64") != std::string::npos, e.what());
+  }
+  return c;
+}
+
+}  // namespace
+
+int main() {
+  struct Entry {
+    const char* name;
+    std::function<Check()> fn;
+  };
+  const Entry entries[] = {
+      {"P1 pbs_attention parity with the reference (f32)", p1_parity},
+      {"C3 kernel equivalence (full-mask sparse == oracle)", c3_kernel_equivalence},
+      {"C4 exactness at tau=1 across strategies and segment sizes", c4_tau_one},
+      {"C5 bitwise causality under key permutation", c5_causality},
+      {"G  GoldenRun256 workload through the drop-in", golden256},
+      {"OPS estimate / key permutation / block scores / selection bit-exact", ops_bitexact},
+      {"COV attention_coverage", coverage},
+      {"DEG degenerate row raises DegenerateRowError", degenerate},
+      {"F64 double precision refused with ConfigError", f64_refused},
+  };
+  int failures = 0;
+  for (const auto& e : entries) {
+    Check c;
+    try {
+      c = e.fn();
+    } catch (const std::exception& ex) {
+      c.ok = false;
+      c.detail = std::string("exception: ") + ex.what();
+    }
+    if (c.ok) std::printf("[PASS] %s%s\n", e.name, c.detail.c_str());
+    else {
+      std::printf("[FAIL] %s: %s\n", e.name, c.detail.c_str());
+      ++failures;
+    }
+    std::fflush(stdout);
+  }
+  if (failures) std::printf("%d criterion(s) failed\n", failures);
+  return failures;
+}
