@@ -1181,7 +1181,9 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
           }))
         return rc;
     }
-    visit_pair_kernel<<<(unsigned)ceil_div(a.items, kVisitWarps), kVisitWarps * 32, smem, st>>>(a, words, vis, nvis);
+    // every pair of every head (the items may be a query-block range of them)
+    visit_pair_kernel<<<(unsigned)ceil_div((int64_t)p.hq * a.npairs, kVisitWarps), kVisitWarps * 32, smem, st>>>(
+        a, words, vis, nvis);
     PBS_LAUNCH_CHECK("visit_pair_kernel");
     a.vis = vis;
     a.nvis = nvis;

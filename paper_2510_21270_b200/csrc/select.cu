@@ -313,6 +313,264 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
   }
 }
 
+// ---- warp-per-row selection ---------------------------------------------------
+// One warp per (head, query block) row, 4 rows per CTA, no CTA barriers:
+//  * mode 0: the softmax of the block-logit row (matrix.hpp:127-142): warp max,
+//    exps spread over the lanes, the sequential denominator in one lane (values
+//    read 8 ahead from shared memory), the IEEE division spread again;
+//  * the threshold rule (block_selection.hpp:171-206) needs only the sorted
+//    PREFIX whose double cumulative sum reaches tau.  A bisection over the
+//    float bit patterns finds the largest theta with sum_{v >= theta} v >=
+//    tau + 1e-9 (summed in any order: the reference's sequential double sum
+//    over the same elements differs by < a * 2^-52, far below the 1e-9
+//    margin), so the prefix lies inside C = {v >= theta}; only C is sorted
+//    (unique composite keys: descending score, ties by ascending index =
+//    std::stable_sort's order) and walked by the exact one-lane double chain.
+//    Rows whose total mass cannot clear the margin (tau ~ 1), or with negative
+//    or non-finite scores, sort every admissible block instead.  top-k: the
+//    largest theta keeping >= k candidates;
+//  * forced blocks, the mask row, the ascending kv list and the pooled-score
+//    coverage (ascending double sum, pipeline.hpp:186-191) from a bitmap.
+constexpr int kSelWarps = 4;
+
+struct SelWarpLayout {
+  int tpad, pow2, words;
+  __host__ __device__ size_t per_warp() const {
+    return ((size_t)tpad * 4 + (size_t)pow2 * 8 + (size_t)words * 4 + 15) & ~(size_t)15;
+  }
+};
+
+__host__ __device__ inline SelWarpLayout sel_layout(int64_t t) {
+  SelWarpLayout L;
+  L.tpad = (int)((t + 3) & ~3);
+  int p = 32;
+  while (p < t) p <<= 1;
+  L.pow2 = p;
+  L.words = (int)((t + 31) / 32);
+  return L;
+}
+
+// warp-synchronous bitonic sort of n (power of two, >= 32) ascending 64-bit keys
+__device__ __forceinline__ void warp_bitonic(unsigned long long* keys, int n, int lane) {
+  for (int size = 2; size <= n; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int x = lane; x < n / 2; x += 32) {
+        const int lo = 2 * x - (x & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const unsigned long long p = keys[lo], q = keys[hi];
+        if ((p > q) == up) {
+          keys[lo] = q;
+          keys[hi] = p;
+        }
+      }
+      __syncwarp();
+    }
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kSelWarps * 32) select_warp_kernel(
+    int mode, const float* __restrict__ rows_in, int hq, int64_t t, int64_t block, int64_t segment, double tau,
+    int top_k, int forced_first, int forced_band, int select, float* __restrict__ scores_out,
+    uint8_t* __restrict__ mask, int32_t* __restrict__ kv_idx, int32_t* __restrict__ kv_cnt,
+    double* __restrict__ row_cov) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint64_t tab[32];
+  load_exp2f_table(tab);
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kSelWarps + w;
+  if (g >= (int64_t)hq * t) return;
+  const int64_t h = g / t, i = g % t;
+  const int a = (int)admissible_prefix(i, t, block, segment);
+  const SelWarpLayout L = sel_layout(t);
+  unsigned char* base = smem + (size_t)w * L.per_warp();
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(base);            // [pow2]
+  float* sv = reinterpret_cast<float*>(base + (size_t)L.pow2 * 8);                   // [tpad]
+  uint32_t* bits = reinterpret_cast<uint32_t*>(base + (size_t)L.pow2 * 8 + (size_t)L.tpad * 4);  // [words]
+  const float* in = rows_in + (h * t + i) * t;
+  for (int j = lane; j < a; j += 32) sv[j] = in[j];
+  __syncwarp();
+  if (mode == 0) {
+    float mx = -INFINITY;
+    for (int j = lane; j < a; j += 32) mx = fmaxf(mx, sv[j]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int j = lane; j < a; j += 32) sv[j] = expf_glibc(__fsub_rn(sv[j], mx), tab);
+    __syncwarp();
+    float denom = 0.0f;
+    if (lane == 0) {
+      int j = 0;
+      for (; j + 8 <= a; j += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = sv[j + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) denom = __fadd_rn(denom, v[u]);
+      }
+      for (; j < a; ++j) denom = __fadd_rn(denom, sv[j]);
+    }
+    denom = __shfl_sync(0xffffffffu, denom, 0);
+    for (int j = lane; j < a; j += 32) sv[j] = __fdiv_rn(sv[j], denom);
+    __syncwarp();
+    if (scores_out) {
+      float* so = scores_out + (h * t + i) * t;
+      for (int64_t j = lane; j < t; j += 32) so[j] = j < a ? sv[j] : 0.0f;
+    }
+  }
+  if (!select) return;
+
+  // ---- candidate set C = {j < a : v_j >= theta}
+  const int k_top = top_k > 0 ? min(top_k, a) : 0;
+  bool all = false;
+  {
+    bool bad = false;  // negative / non-finite scores: no threshold argument, sort everything
+    for (int j = lane; j < a; j += 32) bad |= !(sv[j] >= 0.0f) || !(sv[j] <= 3.0e38f);
+    all = __any_sync(0xffffffffu, bad);
+  }
+  uint32_t theta = 0;
+  if (!all) {
+    auto crit = [&](uint32_t th) {
+      if (k_top > 0) {
+        int c = 0;
+        for (int j = lane; j < a; j += 32) c += __float_as_uint(sv[j]) >= th;
+        return warp_sum_i(c) >= k_top;
+      }
+      double s = 0.0;
+      for (int j = lane; j < a; j += 32)
+        if (__float_as_uint(sv[j]) >= th) s += (double)sv[j];
+      return warp_sum_d(s) >= tau + 1e-9;
+    };
+    if (!crit(0u)) {
+      all = true;
+    } else {
+      uint32_t lo = 0u, hi = 0x7f800001u;  // crit(lo) holds, crit(hi) fails (no finite v >= +inf bits + 1)
+      while (hi - lo > 1u) {
+        const uint32_t mid = lo + (hi - lo) / 2u;
+        if (crit(mid)) lo = mid;
+        else hi = mid;
+      }
+      theta = lo;
+    }
+  }
+  int take = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    int nc = 0;
+    for (int j0 = 0; j0 < a; j0 += 32) {
+      const int j = j0 + lane;
+      const bool in_c = j < a && (all || __float_as_uint(sv[j]) >= theta);
+      const unsigned bal = __ballot_sync(0xffffffffu, in_c);
+      if (in_c)
+        keys[nc + __popc(bal & ((1u << lane) - 1))] =
+            ((unsigned long long)(~float_order_key(sv[j])) << 32) | (unsigned)j;
+      nc += __popc(bal);
+    }
+    int n2 = 32;
+    while (n2 < nc) n2 <<= 1;
+    for (int k = nc + lane; k < n2; k += 32) keys[k] = ~0ull;
+    __syncwarp();
+    warp_bitonic(keys, n2, lane);
+    if (k_top > 0) {
+      take = min(k_top, nc);
+      break;
+    }
+    // the reference's chain (line 187-196): double cumulative sum in sorted order
+    int tk = -1;
+    if (lane == 0) {
+      double cum = 0.0;
+      for (int k0 = 0; k0 < nc && tk < 0; k0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (k0 + u < nc) ? sv[keys[k0 + u] & 0xffffffffu] : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (k0 + u >= nc || tk >= 0) break;
+          cum += (double)v[u];
+          if (cum >= tau) tk = k0 + u + 1;
+        }
+      }
+    }
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    if (tk >= 0) {
+      take = tk;
+      break;
+    }
+    if (all) {  // fallback (line 188): every admissible block
+      take = a;
+      break;
+    }
+    all = true;  // cannot happen past the 1e-9 margin; stay exact regardless
+    __syncwarp();
+  }
+  // ---- the mask row as a bitmap: the taken prefix, then the forced blocks
+  for (int x = lane; x < L.words; x += 32) bits[x] = 0u;
+  __syncwarp();
+  for (int k = lane; k < take; k += 32) {
+    const unsigned j = (unsigned)(keys[k] & 0xffffffffu);
+    atomicOr(&bits[j >> 5], 1u << (j & 31));
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (forced_first && t > 0) bits[0] |= 1u;
+    if (forced_band) {
+      int64_t lo, hi;
+      if (segment == 0) {
+        lo = i;
+        hi = i + 1;
+      } else {
+        const int64_t per = segment / block;
+        lo = (i / per) * per;
+        hi = min64(lo + per, t);
+      }
+      for (int64_t j = lo; j < hi; ++j) bits[j >> 5] |= 1u << (j & 31);
+    }
+  }
+  __syncwarp();
+  if (mask) {
+    uint8_t* mo = mask + (h * t + i) * t;
+    if ((t & 3) == 0) {
+      uint32_t* mo4 = reinterpret_cast<uint32_t*>(mo);
+      for (int64_t q4 = lane; q4 < t / 4; q4 += 32) {
+        const uint32_t nib = (bits[q4 >> 3] >> ((q4 & 7) * 4)) & 0xfu;
+        mo4[q4] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+      }
+    } else {
+      for (int64_t j = lane; j < t; j += 32) mo[j] = (uint8_t)((bits[j >> 5] >> (j & 31)) & 1u);
+    }
+  }
+  // ascending compaction of the selected blocks + coverage partial (double, j ascending)
+  int cnt = 0;
+  double cov = 0.0;
+  int32_t* out = kv_idx ? kv_idx + (h * t + i) * t : nullptr;
+  for (int64_t j0 = 0; j0 < t; j0 += 32) {
+    const unsigned word = bits[j0 >> 5];
+    const int64_t j = j0 + lane;
+    const bool sel = j < t && ((word >> lane) & 1u);
+    if (sel && out) out[cnt + __popc(word & ((1u << lane) - 1))] = (int32_t)j;
+    cnt += __popc(word);
+    if (mode == 0 && j0 < a) {
+      const double val = (sel && j < a) ? (double)sv[j] : 0.0;
+      unsigned b = word & (j0 + 32 <= a ? 0xffffffffu : ((1u << (a - j0)) - 1));
+      while (b) {
+        const int kk = __ffs(b) - 1;
+        b &= b - 1;
+        cov += __shfl_sync(0xffffffffu, val, kk);
+      }
+    }
+  }
+  if (lane == 0) {
+    if (kv_cnt) kv_cnt[h * t + i] = cnt;
+    if (row_cov) row_cov[h * t + i] = cov;
+  }
+}
+
 inline size_t select_smem(int64_t t) {
   int64_t pow2 = 1;
   while (pow2 < t) pow2 <<= 1;
@@ -355,14 +613,30 @@ static int launch_select_common(int mode, const float* rows_in, int hq, int64_t 
                                 cudaStream_t st) {
   if (t == 0 || hq == 0) return PBS_OK;
   if (t > 16384) return fail(PBS_ERR_RESOURCE, "E_RESOURCE", "block grid wider than 16384 blocks");
-  const size_t smem = select_smem(t);
-  static DeviceOnce attr_once;
-  if (int rc = once_per_device(attr_once, [] {
+  const size_t smem = sel_layout(t).per_warp() * kSelWarps;
+  if (smem <= 200 * 1024) {
+    static DeviceOnce attr_once;
+    if (int rc = once_per_device(attr_once, [] {
+          PBS_CUDA_CHECK(
+              cudaFuncSetAttribute(select_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          return (int)PBS_OK;
+        }))
+      return rc;
+    select_warp_kernel<<<(unsigned)ceil_div((int64_t)hq * t, kSelWarps), kSelWarps * 32, smem, st>>>(
+        mode, rows_in, hq, t, block, segment, tau, top_k, forced_first, forced_band, select, scores_out, mask, kv_idx,
+        kv_cnt, row_cov);
+    PBS_LAUNCH_CHECK("select_warp_kernel");
+    return PBS_OK;
+  }
+  // very wide grids (t > ~4000 blocks): one CTA per row with the shared-memory bitonic sort
+  const size_t smem1 = select_smem(t);
+  static DeviceOnce attr_once1;
+  if (int rc = once_per_device(attr_once1, [] {
         PBS_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         return (int)PBS_OK;
       }))
     return rc;
-  select_kernel<<<dim3((unsigned)t, (unsigned)hq), kSelThreads, smem, st>>>(
+  select_kernel<<<dim3((unsigned)t, (unsigned)hq), kSelThreads, smem1, st>>>(
       mode, rows_in, t, block, segment, tau, top_k, forced_first, forced_band, select, scores_out, mask, kv_idx,
       kv_cnt, row_cov);
   PBS_LAUNCH_CHECK("select_kernel");
