@@ -107,19 +107,86 @@ __global__ void __launch_bounds__(xgemm::kThreads, 2) importance_logits_kernel(
   }
 }
 
-// K1b + K1c: denom_i = sequential fp32 sum of E[j][i] = expf(L[j][i] - mx_i)
-// over j = 0..N-1 (permutation.hpp:171-172), then w_i = 1 / (denom * take)
-// (line 174).  One CTA per (head, 32 rows): warp 1 streams 256-key x 32-row
-// tiles of L into a shared-memory ring, one 2-D TMA copy per tile (the whole
-// ring in flight); kExpWarps warps turn each tile into E in place (the glibc
-// expf port, every element once); warp 0 is the adder, one dependent chain of
-// N adds per lane.  E never goes back to HBM: the score pass recomputes it
-// from L (K1d).  Shapes whose row groups are not whole 16-byte pieces
-// (take % 32 != 0 or a partial row group) take 4-byte cp.async copies.
-constexpr int kJT = 256;     // keys per ring tile (one barrier round trip per 256 adds)
-constexpr int kRing = 4;     // 4 tiles = 128 KB in flight
-constexpr int kExpWarps = 8; // 8192 exps per tile against the adder's 256 x 4 cycles
-constexpr int kDenThreads = 64 + 32 * kExpWarps;
+// K1b: E[j][i] = expf(L[j][i] - mx_i) in place (permutation.hpp:171), every
+// element once, on the whole GPU (the sequential passes below only stream E).
+// CTA = kExpKeys keys of one head; the row maxima are decoded into smem.
+constexpr int kExpKeys = 128;
+__global__ void __launch_bounds__(256) importance_exp_kernel(float* __restrict__ L, const unsigned* __restrict__ rowmax,
+                                                             int take, int64_t n, int h0) {
+  __shared__ float mx[1024];
+  __shared__ uint64_t tab[32];
+  load_exp2f_table(tab);
+  const int h = h0 + blockIdx.y;
+  for (int i = threadIdx.x; i < take && i < 1024; i += blockDim.x) mx[i] = decode_order_key(rowmax[(int64_t)h * take + i]);
+  __syncthreads();
+  const int64_t j0 = (int64_t)blockIdx.x * kExpKeys;
+  const int64_t cnt = min64(kExpKeys, n - j0) * take;
+  float* base = L + ((int64_t)h * n + j0) * take;
+  if (take % 4 == 0 && take <= 1024) {
+    // four 16-byte loads in flight per thread before any exp.  When take
+    // divides 4 x blockDim (take = B = 128), a thread's row offset i never
+    // changes (the CTA starts on a key boundary): its four maxima are hoisted.
+    float4* b4 = reinterpret_cast<float4*>(base);
+    const int64_t n4 = cnt / 4;
+    if ((4 * (int)blockDim.x) % take == 0) {
+      const int i = (4 * (int)threadIdx.x) % take;
+      const float m0 = mx[i], m1 = mx[i + 1], m2 = mx[i + 2], m3 = mx[i + 3];
+      for (int64_t e0 = threadIdx.x; e0 < n4; e0 += 4 * (int64_t)blockDim.x) {
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t e = e0 + (int64_t)u * blockDim.x;
+          if (e < n4) x[u] = b4[e];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t e = e0 + (int64_t)u * blockDim.x;
+          if (e >= n4) break;
+          x[u].x = expf_glibc(__fsub_rn(x[u].x, m0), tab);
+          x[u].y = expf_glibc(__fsub_rn(x[u].y, m1), tab);
+          x[u].z = expf_glibc(__fsub_rn(x[u].z, m2), tab);
+          x[u].w = expf_glibc(__fsub_rn(x[u].w, m3), tab);
+          b4[e] = x[u];
+        }
+      }
+      return;
+    }
+    for (int64_t e0 = threadIdx.x; e0 < n4; e0 += 4 * (int64_t)blockDim.x) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + (int64_t)u * blockDim.x;
+        if (e < n4) x[u] = b4[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + (int64_t)u * blockDim.x;
+        if (e >= n4) break;
+        const int i = (int)((e * 4) % take);
+        x[u].x = expf_glibc(__fsub_rn(x[u].x, mx[i]), tab);
+        x[u].y = expf_glibc(__fsub_rn(x[u].y, mx[i + 1]), tab);
+        x[u].z = expf_glibc(__fsub_rn(x[u].z, mx[i + 2]), tab);
+        x[u].w = expf_glibc(__fsub_rn(x[u].w, mx[i + 3]), tab);
+        b4[e] = x[u];
+      }
+    }
+  } else {
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int i = (int)(e % take);
+      const float m = i < 1024 ? mx[i] : decode_order_key(rowmax[(int64_t)h * take + i]);
+      base[e] = expf_glibc(__fsub_rn(base[e], m), tab);
+    }
+  }
+}
+
+// K1c: denom_i = sequential fp32 sum of E[j][i] over j = 0..N-1 (line 172), then
+// w_i = 1 / (denom * take) (line 174).  One CTA per (head, 32 rows): warp 1
+// streams 128-key x 32-row tiles of E into a shared-memory ring, one 2-D TMA
+// copy per tile (the whole ring in flight), warp 0 is the adder, one dependent
+// chain of N adds per lane.  Shapes whose row groups are not whole 16-byte
+// pieces (take % 4 != 0 or a partial row group) take 4-byte cp.async copies.
+constexpr int kJT = 256;    // keys per ring tile (one barrier round trip per 256 adds)
+constexpr int kRing = 4;    // 4 tiles = 128 KB in flight
 
 __device__ __forceinline__ void tma_load_3d_f32(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                 int c2) {
@@ -130,135 +197,104 @@ __device__ __forceinline__ void tma_load_3d_f32(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
-struct DenomSmem {
-  float ring[kRing][kJT][32];
-  uint64_t full[kRing], conv[kRing], empty[kRing];
-  uint64_t tab[32];
-  float mx[32];
-};
-
-__global__ void __launch_bounds__(kDenThreads, 1) importance_denom_kernel(const __grid_constant__ CUtensorMap tm_l,
-                                                                       bool tma, const float* __restrict__ L,
-                                                                       const unsigned* __restrict__ rowmax, int take,
-                                                                       int64_t n, int h0, float* __restrict__ w) {
+__global__ void __launch_bounds__(64, 1) importance_denom_kernel(const __grid_constant__ CUtensorMap tm_e, bool tma,
+                                                              const float* __restrict__ E, int take, int64_t n,
+                                                              int h0, float* __restrict__ w) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  DenomSmem& S = *reinterpret_cast<DenomSmem*>(dsm);
+  float (*ring)[kJT][32] = reinterpret_cast<float (*)[kJT][32]>(dsm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + sizeof(float) * kRing * kJT * 32);
+  uint64_t* empty = full + kRing;
   const int h = h0 + blockIdx.y;
   const int i0 = blockIdx.x * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows = min(32, take - i0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
-      ptx::mbar_init(&S.full[s], tma ? 1 : 32);
-      ptx::mbar_init(&S.conv[s], kExpWarps);
-      ptx::mbar_init(&S.empty[s], 1);
+      ptx::mbar_init(&full[s], tma ? 1 : 32);
+      ptx::mbar_init(&empty[s], 1);
     }
     ptx::fence_mbar_init();
   }
-  load_exp2f_table(S.tab);
-  if (threadIdx.x < 32)
-    S.mx[threadIdx.x] = threadIdx.x < rows ? decode_order_key(rowmax[(int64_t)h * take + i0 + threadIdx.x]) : 0.0f;
   __syncthreads();
   const int64_t ntiles = (n + kJT - 1) / kJT;
-  const float* Lh = L + (int64_t)h * n * take;
+  const float* Eh = E + (int64_t)h * n * take;
   if (warp == 1) {
     for (int64_t t = 0; t < ntiles; ++t) {
       const int slot = (int)(t % kRing);
-      ptx::mbar_wait(&S.empty[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
+      ptx::mbar_wait(&empty[slot], (uint32_t)(((t / kRing) & 1) ^ 1));
       const int64_t jb = t * kJT;
       const int cnt = (int)min64(kJT, n - jb);
       if (tma) {
-        // keys past N are zero-filled by the TMA unit; the box is always 32 KB
+        // keys past N are zero-filled by the TMA unit; the box is always 4 KB
         if (lane == 0) {
-          ptx::mbar_expect_tx(&S.full[slot], kJT * 32 * 4);
-          tma_load_3d_f32(&S.ring[slot][0][0], &tm_l, &S.full[slot], i0, (int)jb, h);
+          ptx::mbar_expect_tx(&full[slot], kJT * 32 * 4);
+          tma_load_3d_f32(&ring[slot][0][0], &tm_e, &full[slot], i0, (int)jb, h);
         }
       } else {
         for (int jj = 0; jj < cnt; ++jj)
-          if (lane < rows) cp_async4(&S.ring[slot][jj][lane], Lh + (jb + jj) * take + i0 + lane);
+          if (lane < rows) cp_async4(&ring[slot][jj][lane], Eh + (jb + jj) * take + i0 + lane);
         cp_async_wait_all();
-        ptx::mbar_arrive(&S.full[slot]);
+        ptx::mbar_arrive(&full[slot]);
       }
-    }
-  } else if (warp >= 2) {
-    // E = expf(L - mx_i) in place (permutation.hpp:171), row i = lane of the tile
-    const int te = threadIdx.x - 64;
-    const float m = S.mx[lane];
-    for (int64_t t = 0; t < ntiles; ++t) {
-      const int slot = (int)(t % kRing);
-      ptx::mbar_wait(&S.full[slot], (uint32_t)((t / kRing) & 1));
-      const int cnt = (int)min64(kJT, n - t * kJT);
-      float* tile = &S.ring[slot][0][0];
-#pragma unroll 8
-      for (int e = te; e < kJT * 32; e += 32 * kExpWarps)
-        if ((e >> 5) < cnt) tile[e] = expf_glibc(__fsub_rn(tile[e], m), S.tab);
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&S.conv[slot]);
     }
   } else {
     float denom = 0.0f;
     for (int64_t t = 0; t < ntiles; ++t) {
       const int slot = (int)(t % kRing);
-      ptx::mbar_wait(&S.conv[slot], (uint32_t)((t / kRing) & 1));
+      ptx::mbar_wait(&full[slot], (uint32_t)((t / kRing) & 1));
       const int cnt = (int)min64(kJT, n - t * kJT);
       if (cnt == kJT) {
 #pragma unroll
         for (int j0 = 0; j0 < kJT; j0 += 128) {
           float v[128];
 #pragma unroll
-          for (int jj = 0; jj < 128; ++jj) v[jj] = S.ring[slot][j0 + jj][lane];
+          for (int jj = 0; jj < 128; ++jj) v[jj] = ring[slot][j0 + jj][lane];
 #pragma unroll
           for (int jj = 0; jj < 128; ++jj) denom = __fadd_rn(denom, v[jj]);
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[slot]);
       } else {
-        for (int jj = 0; jj < cnt; ++jj) denom = __fadd_rn(denom, S.ring[slot][jj][lane]);
+        for (int jj = 0; jj < cnt; ++jj) denom = __fadd_rn(denom, ring[slot][jj][lane]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[slot]);
       }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&S.empty[slot]);
     }
     if (lane < rows) w[(int64_t)h * take + i0 + lane] = __fdiv_rn(1.0f, __fmul_rn(denom, (float)take));
   }
 }
 
 // K1d: s[j] = sum_i E[j][i] * w_i in order i = 0..take-1 (line 175), the product
-// rounded before the add, E = expf(L - mx_i) recomputed from L (the denominator
-// pass never stores it).  CTA = 128 keys, one per thread; 32-row chunks of the
-// keys' L rows double-buffered through smem (16-byte cp.async, rows padded to
-// 36 floats so each thread's 16-byte reads are bank-conflict free).
+// rounded before the add.  CTA = 128 keys, one per thread; 32-row chunks of the
+// keys' E rows double-buffered through smem (16-byte cp.async, rows padded to 36
+// floats so each thread's 16-byte reads are bank-conflict free).
 constexpr int kSK = 128;
 constexpr int kSPad = 36;
-__global__ void __launch_bounds__(kSK) importance_scores_kernel(const float* __restrict__ L,
-                                                                const unsigned* __restrict__ rowmax,
+__global__ void __launch_bounds__(kSK) importance_scores_kernel(const float* __restrict__ E,
                                                                 const float* __restrict__ w, int take, int64_t n,
                                                                 int h0, float* __restrict__ scores) {
   __shared__ __align__(16) float tile[2][kSK][kSPad];
   __shared__ float ws[2][32];
-  __shared__ float ms[2][32];
-  __shared__ uint64_t tab[32];
-  load_exp2f_table(tab);
   const int h = h0 + blockIdx.y;
   const int64_t j0 = (int64_t)blockIdx.x * kSK;
   const int tid = threadIdx.x;
   const int keys = (int)min64(kSK, n - j0);
-  const float* Lh = L + (int64_t)h * n * take;
+  const float* Eh = E + (int64_t)h * n * take;
   const bool vec = (take % 4 == 0);
   auto stage = [&](int buf, int i0) {
     const int ic = min(32, take - i0);
-    if (tid < 32) {
-      ws[buf][tid] = tid < ic ? w[(int64_t)h * take + i0 + tid] : 0.0f;
-      ms[buf][tid] = tid < ic ? decode_order_key(rowmax[(int64_t)h * take + i0 + tid]) : 0.0f;
-    }
+    if (tid < 32) ws[buf][tid] = tid < ic ? w[(int64_t)h * take + i0 + tid] : 0.0f;
     if (vec) {
       // ic is a multiple of 4 here: ic / 4 pieces per key
       const int pk = ic >> 2;
       for (int c = tid; c < keys * pk; c += kSK) {
         const int r = c / pk, q = c - r * pk;
-        cp_async16(&tile[buf][r][4 * q], Lh + (j0 + r) * take + i0 + 4 * q);
+        cp_async16(&tile[buf][r][4 * q], Eh + (j0 + r) * take + i0 + 4 * q);
       }
     } else {
       for (int c = tid; c < keys * ic; c += kSK) {
         const int r = c / ic, q = c - r * ic;
-        cp_async4(&tile[buf][r][q], Lh + (j0 + r) * take + i0 + q);
+        cp_async4(&tile[buf][r][q], Eh + (j0 + r) * take + i0 + q);
       }
     }
     cp_async_commit();
@@ -276,19 +312,14 @@ __global__ void __launch_bounds__(kSK) importance_scores_kernel(const float* __r
     if (ic == 32) {
 #pragma unroll
       for (int c = 0; c < 32; c += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(&tile[buf][tid][c]);
-        const float e0 = expf_glibc(__fsub_rn(l4.x, ms[buf][c]), tab);
-        const float e1 = expf_glibc(__fsub_rn(l4.y, ms[buf][c + 1]), tab);
-        const float e2 = expf_glibc(__fsub_rn(l4.z, ms[buf][c + 2]), tab);
-        const float e3 = expf_glibc(__fsub_rn(l4.w, ms[buf][c + 3]), tab);
-        s = __fadd_rn(s, __fmul_rn(e0, ws[buf][c]));
-        s = __fadd_rn(s, __fmul_rn(e1, ws[buf][c + 1]));
-        s = __fadd_rn(s, __fmul_rn(e2, ws[buf][c + 2]));
-        s = __fadd_rn(s, __fmul_rn(e3, ws[buf][c + 3]));
+        const float4 e = *reinterpret_cast<const float4*>(&tile[buf][tid][c]);
+        s = __fadd_rn(s, __fmul_rn(e.x, ws[buf][c]));
+        s = __fadd_rn(s, __fmul_rn(e.y, ws[buf][c + 1]));
+        s = __fadd_rn(s, __fmul_rn(e.z, ws[buf][c + 2]));
+        s = __fadd_rn(s, __fmul_rn(e.w, ws[buf][c + 3]));
       }
     } else {
-      for (int c = 0; c < ic; ++c)
-        s = __fadd_rn(s, __fmul_rn(expf_glibc(__fsub_rn(tile[buf][tid][c], ms[buf][c]), tab), ws[buf][c]));
+      for (int c = 0; c < ic; ++c) s = __fadd_rn(s, __fmul_rn(tile[buf][tid][c], ws[buf][c]));
     }
     __syncthreads();  // buf is refilled two chunks later
   }
@@ -539,7 +570,13 @@ int launch_importance_finish(int hq, int h0, int nh, int64_t n, int64_t block, f
   if (nh == 0) return PBS_OK;
   const ImpWs W = imp_ws(ws, hq, n, take);
   float* L = W.L;
-  const size_t smem = sizeof(DenomSmem);
+  // E = expf(L - mx) once per element on the whole GPU (the glibc port is
+  // FP64 work: computing it once and streaming E twice beats recomputing it
+  // inside the two sequential passes, measured 1.46 vs 2.6 ms at C3)
+  importance_exp_kernel<<<dim3((unsigned)ceil_div(n, kExpKeys), (unsigned)nh), 256, 0, st>>>(L, W.rowmax, take, n,
+                                                                                             h0);
+  PBS_LAUNCH_CHECK("importance_exp_kernel");
+  const size_t smem = sizeof(float) * kRing * kJT * 32 + 2 * kRing * sizeof(uint64_t);
   static DeviceOnce attr_once;
   if (int rc = once_per_device(attr_once, [&] {
         PBS_CUDA_CHECK(
@@ -547,18 +584,18 @@ int launch_importance_finish(int hq, int h0, int nh, int64_t n, int64_t block, f
         return (int)PBS_OK;
       }))
     return rc;
-  alignas(64) CUtensorMap tm_l;
-  const bool tma = (take % 32 == 0);  // every CTA's 32 rows are whole 16-byte pieces
+  alignas(64) CUtensorMap tm_e;
+  const bool tma = (take % 4 == 0) && (take % 32 == 0);  // every CTA's 32 rows are whole 16-byte pieces
   if (tma) {
-    if (int rc = make_f32_map_3d(&tm_l, L, take, n, hq, 32, kJT)) return rc;
+    if (int rc = make_f32_map_3d(&tm_e, L, take, n, hq, 32, kJT)) return rc;
   } else {
-    memset(&tm_l, 0, sizeof(tm_l));
+    memset(&tm_e, 0, sizeof(tm_e));
   }
-  importance_denom_kernel<<<dim3((unsigned)ceil_div(take, 32), (unsigned)nh), kDenThreads, smem, st>>>(
-      tm_l, tma, L, W.rowmax, take, n, h0, W.w);
+  importance_denom_kernel<<<dim3((unsigned)ceil_div(take, 32), (unsigned)nh), 64, smem, st>>>(tm_e, tma, L, take, n,
+                                                                                              h0, W.w);
   PBS_LAUNCH_CHECK("importance_denom_kernel");
-  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, kSK), (unsigned)nh), kSK, 0, st>>>(L, W.rowmax, W.w, take, n,
-                                                                                         h0, scores);
+  importance_scores_kernel<<<dim3((unsigned)ceil_div(n, kSK), (unsigned)nh), kSK, 0, st>>>(L, W.w, take, n, h0,
+                                                                                         scores);
   PBS_LAUNCH_CHECK("importance_scores_kernel");
   return PBS_OK;
 }
