@@ -637,6 +637,7 @@ struct Arena {
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   cudaEvent_t ev_rep[2] = {nullptr, nullptr};
+  cudaEvent_t ev_comp[2] = {nullptr, nullptr};  // per slot: the group's compute is done (its inputs are free)
   std::vector<cudaEvent_t> ev_k;  // per KV head: its keys are on the device (estimate-first path)
   // per slot: stage timers and pinned copies of the report counters, so a
   // group's report is built while the next group computes
@@ -691,10 +692,38 @@ int arena_streams(Arena& A) {
     PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_done[i], cudaEventDisableTiming));
     PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_out[i], cudaEventDisableTiming));
     PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_rep[i], cudaEventDisableTiming));
+    PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_comp[i], cudaEventDisableTiming));
     A.timer[i] = new Timer(true, A.st[1]);
   }
   return PBS_OK;
 }
+}  // namespace
+
+namespace {
+// debug (PBS_HOST_TRACE=1): the host entry's timeline, CUDA events on its three
+// streams, printed to stderr as ms after the first event once the call is done
+struct HostTrace {
+  bool on = getenv("PBS_HOST_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void mark(const std::string& name, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    ev.emplace_back(name, e);
+  }
+  ~HostTrace() {
+    if (!on || ev.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& x : ev) {
+      float ms = 0.0f;
+      const cudaError_t e = cudaEventElapsedTime(&ms, ev.front().second, x.second);
+      fprintf(stderr, "pbs_host_trace %8.3f ms  %s%s\n", ms, x.first.c_str(),
+              e == cudaSuccess ? "" : (std::string(" (") + cudaGetErrorString(e) + ")").c_str());
+    }
+    for (auto& x : ev) cudaEventDestroy(x.second);
+  }
+};
 }  // namespace
 
 int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_shape* shape,
@@ -757,6 +786,8 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     sl[i].ws = take(ws);
   }
   cudaStream_t s_in = A.st[0], s_run = A.st[1], s_out = A.st[2];
+  HostTrace tr;
+  tr.mark("start", s_in);
   const char* hq_ = static_cast<const char*>(q);
   const char* hk_ = static_cast<const char*>(k);
   const char* hv_ = static_cast<const char*>(v);
@@ -804,6 +835,7 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
                                        pi_inv + (size_t)h0 * n, s_run))
       return rc;
     est_tm.mark();
+    tr.mark("run: estimate groups " + std::to_string(c0) + ".." + std::to_string(c1 - 1) + " done", s_run);
     return PBS_OK;
   };
   char* ho_ = static_cast<char*>(out);
@@ -824,15 +856,16 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     return reinterpret_cast<int32_t*>(A.pinned + i * rep_bytes + al((size_t)g * t * 4) + al((size_t)g * t * 8));
   };
   // Work chunks: one per KV group, except that the LAST group (key_permute, pi
-  // precomputed) runs in up to 4 head slices, so the output of one slice goes
-  // back to the host while the next computes and the drain after the last
-  // kernel is one slice, not one group.
+  // precomputed) runs in two head halves, so the output of the first goes back
+  // to the host while the second computes and the drain after the last kernel
+  // is half a group (single-head slices cost more in per-launch tails than
+  // they save in drain: measured 1.85 ms per 1-head slice vs 1.26 per head).
   struct Chunk {
     int64_t c, a, b;  // KV group c, its query heads [a, b) (local to the group)
   };
   std::vector<Chunk> chunks;
   for (int64_t c = 0; c < hkv; ++c) {
-    const int64_t parts = (est_first && c == hkv - 1) ? std::min<int64_t>(g, 4) : 1;
+    const int64_t parts = (est_first && c == hkv - 1) ? std::min<int64_t>(g, 2) : 1;
     for (int64_t j = 0; j < parts; ++j) chunks.push_back(Chunk{c, j * g / parts, (j + 1) * g / parts});
   }
   // fold the report of chunk kk (its counters were fetched on s_run) into the total
@@ -866,11 +899,16 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   };
   auto copy_in = [&](int64_t c) -> int {
     Slot& S = sl[c % nslots];
-    if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_in, A.ev_out[c % nslots], 0));  // slot drained
+    // the slot's Q / K / V buffers are free once group c - nslots has been
+    // COMPUTED (its output buffer, written again by group c, is guarded on
+    // s_run by ev_out below), so the inputs of the next group stream in while
+    // the previous output is still being copied out
+    if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_in, A.ev_comp[c % nslots], 0));
     PBS_CUDA_CHECK(cudaMemcpyAsync(S.q, hq_ + (size_t)c * qb, qb, cudaMemcpyHostToDevice, s_in));
     if (!est_first) PBS_CUDA_CHECK(cudaMemcpyAsync(S.k, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
     PBS_CUDA_CHECK(cudaMemcpyAsync(S.v, hv_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
     PBS_CUDA_CHECK(cudaEventRecord(A.ev_in[c % nslots], s_in));
+    tr.mark("in: Q,V of group " + std::to_string(c) + " landed", s_in);
     return PBS_OK;
   };
   if (est_first) {
@@ -888,6 +926,7 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
       PBS_CUDA_CHECK(cudaMemcpyAsync(k_all + (size_t)c * kvb, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
       PBS_CUDA_CHECK(cudaEventRecord(A.ev_k[c], s_in));
     }
+    tr.mark("in: all K landed", s_in);
     if (int rc = estimate_groups(0, 1)) return rc;
   } else {
     if (int rc = copy_in(0)) return rc;
@@ -905,6 +944,7 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
       if (est_first && c == 1)
         if (int rc = estimate_groups(1, hkv)) return rc;
       PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_in[i], 0));
+      if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_out[i], 0));  // S.out copied out
     }
     pbs_shape cs2 = cs;
     cs2.num_q_heads = (int32_t)(ch.b - ch.a);
@@ -924,6 +964,10 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
       PBS_CUDA_CHECK(cudaEventRecord(A.ev_rep[ri], s_run));
     }
     PBS_CUDA_CHECK(cudaEventRecord(A.ev_done[ri], s_run));
+    if (ch.b == g) PBS_CUDA_CHECK(cudaEventRecord(A.ev_comp[i], s_run));
+    tr.mark("run: chunk " + std::to_string(kk) + " (group " + std::to_string(c) + " heads " + std::to_string(ch.a) +
+                ".." + std::to_string(ch.b - 1) + ") computed",
+            s_run);
     PBS_CUDA_CHECK(cudaStreamWaitEvent(s_out, A.ev_done[ri], 0));
     const size_t hoff = (size_t)c * g + ch.a;  // first query head of the chunk
     PBS_CUDA_CHECK(cudaMemcpyAsync(ho_ + hoff * n * d * es, S.out + qoff, qbytes, cudaMemcpyDeviceToHost, s_out));
@@ -934,6 +978,7 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
                                      s_out));
     if (mask) PBS_CUDA_CHECK(cudaMemcpyAsync(mask + hoff * t * t, S.mask + moff, mbytes, cudaMemcpyDeviceToHost, s_out));
     PBS_CUDA_CHECK(cudaEventRecord(A.ev_out[i], s_out));
+    tr.mark("out: chunk " + std::to_string(kk) + " copied out", s_out);
     // the previous chunk's report, while this one computes (its counters are
     // overwritten only two chunks later, after this fold)
     if (report && kk > 0)

@@ -21,3 +21,6 @@ r = ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout, report=True).report
 print("host-entry stage sums (ms):", {k: round(r[k] / 1e3, 2) for k in ("estimate_us", "permute_us", "select_us", "attention_us")})
 d = ops.pbs_attention(q, k, v, cfg).report
 print("device-entry stages (ms):  ", {k: round(d[k] / 1e3, 2) for k in ("estimate_us", "permute_us", "select_us", "attention_us")})
+# one traced call (PBS_HOST_TRACE: CUDA-event timeline of the three streams, on stderr)
+os.environ["PBS_HOST_TRACE"] = "1"
+ops.pbs_attention_host(hq_, hk_, hv_, cfg, out=hout, report=False)
