@@ -533,8 +533,13 @@ __device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, fl
       if ((j & 15) >= 16 - kPolyPer16) {
         exp2_poly2(y0, y1, p0, p1);
       } else {
+#ifdef PBS_EXP_FAKE  // timing experiment only (wrong results): no MUFU work
+        p0 = fmaxf(fmaf(y0, 0.001f, 1.0f), 0.0f);
+        p1 = fmaxf(fmaf(y1, 0.001f, 1.0f), 0.0f);
+#else
         p0 = ex2(y0);
         p1 = ex2(y1);
+#endif
       }
       sum2[jp & 1] = fadd2(sum2[jp & 1], pk2(p0, p1));
       __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
@@ -645,6 +650,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t* empty = kp ? &bar->k_empty[s] : &bar->v_empty[s];
           uint64_t* full = kp ? &bar->k_full[s] : &bar->v_full[s];
           mbar_wait(empty, ((it_k / nst) & 1) ^ 1);
+#ifdef PBS_NO_KV_LOAD  // timing experiment only (wrong results): K/V tiles loaded once per ring slot
+          if (it_k >= (uint32_t)nst) {
+            mbar_arrive(full);
+            ++it_k;
+            continue;
+          }
+#endif
           mbar_expect_tx(full, kTileBytes);
           unsigned char* dst = smem + (kp ? SmemLayout::k : SmemLayout::v) + s * kTileBytes;
           for (int p = 0; p < 2; ++p)
