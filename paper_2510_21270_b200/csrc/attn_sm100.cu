@@ -78,6 +78,9 @@ static_assert((168 - kRegsControl) * 128 >= (kRegsSoftmax - 168) * kSoftmaxThrea
 // keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the
 // MUFU; 0: with two groups working on different tiles the MUFU keeps up
 // (round 1 A/B on the box: 0 / 2 / 4 of 16 -> 61 / 62 / 66 ms x GHz at 128K)
+#ifndef PBS_PRODUCER_SLEEP_NS
+#define PBS_PRODUCER_SLEEP_NS 64
+#endif
 #ifndef PBS_POLY_PER16
 #define PBS_POLY_PER16 0
 #endif
@@ -134,6 +137,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Softmax -> MMA signals: one arrival per warp (the barrier counts 4 per group)
+// after the warp's lanes have fenced their TMEM accesses, instead of 128 lane
+// arrivals serialised on one shared-memory word.
+#ifdef PBS_LANE_ARRIVE
+constexpr int kGroupArrivals = 128;
+__device__ __forceinline__ void group_arrive(uint64_t* bar) { mbar_arrive(bar); }
+#else
+constexpr int kGroupArrivals = 4;
+__device__ __forceinline__ void group_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+#endif
 // Bounded wait: a deadlock becomes a trap (~10 s at 2 GHz; the launch then fails
 // with an illegal-instruction error) instead of a hung GPU.  The trap is inline:
 // a call (e.g. to printf) would make every wait site an ABI call boundary and
@@ -157,6 +173,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   while (!mbar_try(addr, parity))
     if (clock64() - t0 > 20000000000ll) asm volatile("trap;");
+}
+
+// Producer-side wait (slot free): the TMA warps run ahead of the consumers, so
+// they poll with a short sleep instead of spinning.  A spinning producer
+// re-issued its try_wait loop ~65 times per tile and took issue slots from the
+// softmax warps of its SM sub-partition (ncu source page).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try(addr, parity)) return;
+  const long long t0 = clock64();
+  do {
+    __nanosleep(PBS_PRODUCER_SLEEP_NS);
+    if (clock64() - t0 > 20000000000ll) asm volatile("trap;");
+  } while (!mbar_try(addr, parity));
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
@@ -359,6 +389,13 @@ struct KernelArgs {
 #define SPAN_COUNT(i) do { } while (0)
 #define SPAN_FLUSH(cond, base) do { } while (0)
 #endif
+// Event timeline (-DPBS_ATTN_EVENTS, debug): CTA 0's first 1024 steps, clock64
+// stamps into a.trace[32 + step * 8 + k] (MMA warp) and a.trace[8224 + ...] (softmax)
+#ifdef PBS_ATTN_EVENTS
+#define EVT(cond, idx, k) do { if ((cond) && blockIdx.x == 0 && a.trace && (idx) < 2048) a.trace[32 + (idx) * 8 + (k)] = clock64(); } while (0)
+#else
+#define EVT(cond, idx, k) do { } while (0)
+#endif
 
 struct Item {
   int h;
@@ -549,7 +586,7 @@ __device__ __forceinline__ float emit_p(const uint32_t (&r)[kCols], float sc, fl
     if (c == 1) {  // keys 0..63 are in TMEM: their half of the PV may start
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(half_bar);
+      group_arrive(half_bar);
     }
   }
   float s0, s1, s2, s3;
@@ -586,10 +623,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar->q_full[w], 1);
       mbar_init(&bar->q_empty[w], 1);
       mbar_init(&bar->s_full[w], 1);
-      mbar_init(&bar->p_half[w], 128);
-      mbar_init(&bar->p_full[w], 128);
+      mbar_init(&bar->p_half[w], kGroupArrivals);
+      mbar_init(&bar->p_full[w], kGroupArrivals);
       mbar_init(&bar->o_full[w], 1);
-      mbar_init(&bar->o_free[w], 128);
+      mbar_init(&bar->o_free[w], kGroupArrivals);
     }
     for (int s = 0; s < kKStages; ++s) {
       mbar_init(&bar->k_full[s], 1);
@@ -632,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int w = 0; w < kGroups; ++w) {
           int64_t qb = 2 * it.p + w;
           if (qb >= a.t) qb = 2 * it.p;  // a lone last tile: tile 1's buffer gets tile 0's rows (never read)
-          mbar_wait(&bar->q_empty[w], (q_it & 1) ^ 1);
+          mbar_wait_backoff(&bar->q_empty[w], (q_it & 1) ^ 1);
           mbar_expect_tx(&bar->q_full[w], kTileBytes);
           for (int p = 0; p < 2; ++p)
             tma_load_3d(smem + SmemLayout::q + w * kTileBytes + p * kPanelBytes, &tm_q, &bar->q_full[w], p * 64,
@@ -649,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = (int)(it_k % nst);
           uint64_t* empty = kp ? &bar->k_empty[s] : &bar->v_empty[s];
           uint64_t* full = kp ? &bar->k_full[s] : &bar->v_full[s];
-          mbar_wait(empty, ((it_k / nst) & 1) ^ 1);
+          mbar_wait_backoff(empty, ((it_k / nst) & 1) ^ 1);
 #ifdef PBS_NO_KV_LOAD  // timing experiment only (wrong results): K/V tiles loaded once per ring slot
           if (it_k >= (uint32_t)nst) {
             mbar_arrive(full);
@@ -676,6 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_pv = make_idesc(0, 1);  // P K-major (TMEM), V MN-major
     const uint32_t q_base = smem_u32(smem + SmemLayout::q);
     uint32_t q_it = 0, k_it = 0, v_it = 0, o_no[kGroups] = {0, 0}, p_cnt[kGroups] = {0, 0};
+    uint32_t gs = 0;  // CTA step counter (events)
     SPAN_DECL
     ItemStream items;
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
@@ -689,9 +727,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       bool pend[kGroups] = {false, false}, first[kGroups] = {true, true};
-      for (int u = 0; u <= vis.len; ++u) {
+      for (int u = 0; u <= vis.len; ++u, ++gs) {
         int64_t kb = 0;
         int cls[kGroups] = {0, 0};
+        EVT(lane == 0 && gs < 1024, gs, 0);
         if (u < vis.len) visit_get(a, it, vis, u, lane, kb, cls[0], cls[1]);
         uint32_t v_base = 0;
         if (u > 0) {
@@ -702,6 +741,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ks = k_it % kKStages;
         const uint32_t k_base = smem_u32(smem + SmemLayout::k + ks * kTileBytes);
         bool k_seen = false;
+        EVT(lane == 0 && gs < 1024, gs, 1);
+        // the tile whose PV is the last reader of V_{u-1}: the V slot is released
+        // right after it, before the following QK^T (a commit covers every
+        // earlier MMA, so a later commit would hold the slot for one more QK^T)
+        const int last_pv = pend[1] ? 1 : 0;
         SPAN(0);
 #pragma unroll
         for (int w = 0; w < kGroups; ++w) {
@@ -717,6 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        first[w] ? 0u : 1u);
             SPAN(2);
             mbar_wait(&bar->p_full[w], p_cnt[w] & 1);
+            EVT(lane == 0 && gs < 1024, gs, 2 + 2 * w);
             SPAN(1);
             ++p_cnt[w];
             tc_fence_after();
@@ -725,6 +770,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             SPAN(3);
             first[w] = false;
             pend[w] = false;
+#ifndef PBS_LATE_V_RELEASE
+            if (w == last_pv) {
+              tc_commit_w(&bar->v_empty[v_it % kVStages]);
+              ++v_it;
+            }
+#endif
           }
           if (cls[w]) {
             if (!k_seen) {
@@ -737,19 +788,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_mma_qk8(tmem + col_s(w), sdesc(q_base + w * kTileBytes, 16, 1024), sdesc(k_base, 16, 1024),
                        idesc_qk);
             tc_commit_w(&bar->s_full[w]);
+            EVT(lane == 0 && gs < 1024, gs, 3 + 2 * w);
             SPAN(6);
             pend[w] = true;
           }
         }
+#ifdef PBS_LATE_V_RELEASE
         if (u > 0) {
           tc_commit_w(&bar->v_empty[v_it % kVStages]);
           ++v_it;
         }
+#endif
         if (u < vis.len) {
           tc_commit_w(&bar->k_empty[ks]);
           ++k_it;
           SPAN_COUNT(4);
         }
+        EVT(lane == 0 && gs < 1024, gs, 6);
         if (u + 1 == vis.len)  // every QK^T of the item issued: Q_0, Q_1 are free once they complete
           for (int w = 0; w < kGroups; ++w) tc_commit_w(&bar->q_empty[w]);
       }
@@ -810,6 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = 0; e < vis.len; ++e) {
         int64_t kb;
         int c0, c1;
+        EVT(row == 0 && w == 0 && s_cnt < 1024, 1024 + s_cnt, 0);
         visit_get(a, it, vis, e, lane, kb, c0, c1);
         const int cls = w ? c1 : c0;
         if (cls == 0) continue;  // warp-uniform: a block's class is the tile's
@@ -823,11 +879,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1 + w, 128);
         }
         SPAN(0);
+        EVT(row == 0 && w == 0 && s_cnt < 1024, 1024 + s_cnt, 1);
         mbar_wait(&bar->s_full[w], s_cnt & 1);
+        EVT(row == 0 && w == 0 && s_cnt < 1024, 1024 + s_cnt, 2);
         SPAN(1);
         SPAN_COUNT(7);
         ++s_cnt;
         tc_fence_after();
+#if defined(PBS_SOFTMAX_NOP) || defined(PBS_SOFTMAX_LOADONLY)  // timing experiments only (wrong results)
+        {
+#ifdef PBS_SOFTMAX_LOADONLY
+          uint32_t r[kCols];
+          const float hm = load_scores(tS, r);
+          m = fmaxf(m, hm * sc);
+#endif
+          l = 1.0f;
+          tc_fence_before();
+          group_arrive(&bar->p_half[w]);
+          group_arrive(&bar->p_full[w]);
+          SPAN(4);
+          continue;
+        }
+#endif
         uint32_t r[kCols];
         if (cls == 1) {
           // ElementMask (attention.hpp:41-73) applied in TMEM, 32 columns at a
@@ -846,6 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1 + w, 128);  // ko may be refilled after this
         }
         const float hmax = load_scores(tS, r);
+        EVT(row == 0 && w == 0 && s_cnt <= 1024, 1023 + s_cnt, 3);
         SPAN(2);
         // online softmax (absorb, attention.hpp:96-126) in the log2 domain with
         // lazy rescaling: O_w is rescaled only when the max grows by more than 8
@@ -874,11 +948,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         SPAN(3);
+        EVT(row == 0 && w == 0 && s_cnt <= 1024, 1023 + s_cnt, 4);
         const float rs = emit_p<kPolyPer16>(r, sc, neg_m, tS, &bar->p_half[w]);
         l = l * factor + rs;
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bar->p_full[w]);
+        group_arrive(&bar->p_full[w]);
+        EVT(row == 0 && w == 0 && s_cnt <= 1024, 1023 + s_cnt, 5);
         SPAN(4);
       }
       // ---- epilogue (OnlineSoftmaxState::finalize, attention.hpp:130-138):
@@ -922,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&bar->o_free[w]);
+      group_arrive(&bar->o_free[w]);
       SPAN(5);
     }
     SPAN(6);
@@ -1211,7 +1287,7 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   if (const char* e = getenv("PBS_ATTN_GRID")) grid = (int)min64(grid, atoi(e) > 0 ? atoi(e) : grid);  // debug
   // debug (-DPBS_ATTN_SPANS builds): per-phase cycle sums of every CTA, dumped to $PBS_ATTN_TRACE
   const char* trace_path = getenv("PBS_ATTN_TRACE");
-  constexpr int kSpanWords = 32;
+  constexpr int kSpanWords = 32 + 2048 * 8;
   if (trace_path) {
     PBS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), kSpanWords * 8, st));
     PBS_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, kSpanWords * 8, st));

@@ -92,7 +92,14 @@ __global__ void bench(long long* out, int iters, volatile int* stop) {
       const uint64_t bd = sdesc(b + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
       if (kMode == 0) mma_ss(tm, sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), bd, idesc(kN), k > 0);
       else if (kMode == 1) mma_ts(tm, tm + 256 + k * 8, bd, idesc(kN), k > 0);
-      else mma_ts(tm, tm + 256 + k * 8, sdesc(b + k * 16 * 128, 16384, 1024), idesc(kN, 1), k > 0);  // B MN-major (V)
+      else if (kMode == 2) mma_ts(tm, tm + 256 + k * 8, sdesc(b + k * 16 * 128, 16384, 1024), idesc(kN, 1), k > 0);  // B MN-major (V)
+      else {  // 3: the attention step mix, QK^T (SS) into cols 0.. then PV (TS, B MN-major) into cols 384..
+        mma_ss(tm, sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), bd, idesc(kN), k > 0);
+      }
+    }
+    if (kMode == 3) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mma_ts(tm + 384, tm + 128 + k * 8, sdesc(b + k * 16 * 128, 16384, 1024), idesc(kN, 1), k > 0);
     }
     if (kCommit == 1) commit(&bar2[it & 1]);  // a commit after every 8 MMAs (nobody waits)
     if (kCommit == 2) { commit(&bar2[0]); wait(&bar2[0], it & 1); }  // and wait for it
@@ -118,8 +125,8 @@ void run(int warps) {
   cudaDeviceSynchronize();
   k<<<148, 32 * warps, 140 * 1024>>>(d, iters, nullptr);
   long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  const double per = (double)h / (iters * 8.0);
-  printf("commit %d %s%s N=%d load %d warps %d: %.1f cycles per 128x%dx16 MMA (ideal %d) %s\n", kCommit, kMode == 2 ? "TS-Bmn" : kMode ? "TS" : "SS", kRandom ? " random" : "", kN, kLoad, warps, per, kN, kN / 2,
+  const double per = (double)h / (iters * (kMode == 3 ? 16.0 : 8.0));
+  printf("commit %d %s%s N=%d load %d warps %d: %.1f cycles per 128x%dx16 MMA (ideal %d) %s\n", kCommit, kMode == 3 ? "QK+PV" : kMode == 2 ? "TS-Bmn" : kMode ? "TS" : "SS", kRandom ? " random" : "", kN, kLoad, warps, per, kN, kN / 2,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -131,5 +138,6 @@ int main() {
   run<0, 128, 1>(9); run<1, 128, 1>(9); run<1, 128, 1>(5);
   run<0, 128, 2>(9); run<1, 128, 2>(9);
   run<0, 128, 3>(9); run<1, 128, 3>(9);
+  run<3, 128, 0, true>(1); run<3, 128, 0, true, 1>(1); run<3, 128, 3, true>(9); run<3, 128, 1, true>(9); run<0, 128, 3, true>(9); run<0, 128, 3, true>(5);
   return 0;
 }
