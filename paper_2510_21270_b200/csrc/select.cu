@@ -463,7 +463,96 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_warp_kernel(
     }
   }
   int take = 0;
-  for (int pass = 0; pass < 2; ++pass) {
+  // Exact path (no sort): when every candidate is >= 2^-29, any double sum of
+  // candidates is exact (all partial sums lie below 2, whose ulp 2^-52 divides
+  // every such float), so the reference's sequential cumulative sum over the
+  // sorted prefix equals the order-free sum of the same top-k set.  The prefix
+  // is then {v > v*} plus the first ties v == v* in index order, where v* is
+  // the largest value with sum_{v >= v*} >= tau (bisection over float bits,
+  // exact warp-reduced double sums).
+  bool exact_done = false;
+  int nc = 0;  // exact path: candidates compacted into keys[]
+  if (!all && k_top == 0 && tau > 0.0) {
+    float vmin = INFINITY;
+    for (int j = lane; j < a; j += 32)
+      if (__float_as_uint(sv[j]) >= theta) vmin = fminf(vmin, sv[j]);
+    for (int o = 16; o > 0; o >>= 1) vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+    if (vmin >= 1.862645149230957e-09f) {  // 2^-29
+      // candidates compacted into keys[] (value bits << 32 | index), ascending index
+      for (int j0 = 0; j0 < a; j0 += 32) {
+        const int j = j0 + lane;
+        const bool in_c = j < a && __float_as_uint(sv[j]) >= theta;
+        const unsigned bal = __ballot_sync(0xffffffffu, in_c);
+        if (in_c) keys[nc + __popc(bal & ((1u << lane) - 1))] = ((unsigned long long)__float_as_uint(sv[j]) << 32) | (unsigned)j;
+        nc += __popc(bal);
+      }
+      __syncwarp();
+      auto mass = [&](uint32_t th, bool strict) {  // sum of the candidates >= th (> th); exact when < 2
+        double sum = 0.0;
+        for (int k = lane; k < nc; k += 32) {
+          const uint32_t vb = (uint32_t)(keys[k] >> 32);
+          if (strict ? vb > th : vb >= th) sum += (double)__uint_as_float(vb);
+        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        return sum;
+      };
+      const double total = mass(theta, false);
+      exact_done = total < 2.0 && total >= tau;  // all partial sums below 2 (scores need not be probabilities)
+    }
+    if (exact_done) {
+      auto mass = [&](uint32_t th, bool strict) {
+        double sum = 0.0;
+        for (int k = lane; k < nc; k += 32) {
+          const uint32_t vb = (uint32_t)(keys[k] >> 32);
+          if (strict ? vb > th : vb >= th) sum += (double)__uint_as_float(vb);
+        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        return sum;
+      };
+      uint32_t lo = theta, hi = 0x7f800001u;  // mass(lo) >= tau (the margin above), mass(hi) = 0 < tau
+      while (hi - lo > 1u) {
+        const uint32_t mid = lo + (hi - lo) / 2u;
+        if (mass(mid, false) >= tau) lo = mid;
+        else hi = mid;
+      }
+      const uint32_t vstar = lo;
+      const double s_gt = mass(vstar, true);
+      int gt = 0;
+      for (int k = lane; k < nc; k += 32) gt += (uint32_t)(keys[k] >> 32) > vstar;
+      gt = warp_sum_i(gt);
+      // ties v == v* in ascending index order until the sum reaches tau
+      int r = 0;
+      if (lane == 0) {
+        double cum = s_gt;
+        for (int k = 0; k < nc; ++k)
+          if ((uint32_t)(keys[k] >> 32) == vstar) {
+            cum += (double)__uint_as_float(vstar);
+            ++r;
+            if (cum >= tau) break;
+          }
+      }
+      r = __shfl_sync(0xffffffffu, r, 0);
+      take = gt + r;
+      for (int x = lane; x < L.words; x += 32) bits[x] = 0u;
+      __syncwarp();
+      int tie_seen = 0;
+      for (int k0 = 0; k0 < nc; k0 += 32) {
+        const int k = k0 + lane;
+        const uint32_t vb = k < nc ? (uint32_t)(keys[k] >> 32) : 0u;
+        const bool tie = k < nc && vb == vstar;
+        const unsigned tb = __ballot_sync(0xffffffffu, tie);
+        const bool pick = k < nc && (vb > vstar || (tie && tie_seen + __popc(tb & ((1u << lane) - 1)) < r));
+        if (pick) {
+          const unsigned j = (unsigned)(keys[k] & 0xffffffffu);
+          atomicOr(&bits[j >> 5], 1u << (j & 31));
+        }
+        tie_seen += __popc(tb);
+      }
+      __syncwarp();
+      exact_done = true;
+    }
+  }
+  for (int pass = 0; pass < 2 && !exact_done; ++pass) {
     int nc = 0;
     for (int j0 = 0; j0 < a; j0 += 32) {
       const int j = j0 + lane;
@@ -512,13 +601,15 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_warp_kernel(
     __syncwarp();
   }
   // ---- the mask row as a bitmap: the taken prefix, then the forced blocks
-  for (int x = lane; x < L.words; x += 32) bits[x] = 0u;
-  __syncwarp();
-  for (int k = lane; k < take; k += 32) {
-    const unsigned j = (unsigned)(keys[k] & 0xffffffffu);
-    atomicOr(&bits[j >> 5], 1u << (j & 31));
+  if (!exact_done) {
+    for (int x = lane; x < L.words; x += 32) bits[x] = 0u;
+    __syncwarp();
+    for (int k = lane; k < take; k += 32) {
+      const unsigned j = (unsigned)(keys[k] & 0xffffffffu);
+      atomicOr(&bits[j >> 5], 1u << (j & 31));
+    }
+    __syncwarp();
   }
-  __syncwarp();
   if (lane == 0) {
     if (forced_first && t > 0) bits[0] |= 1u;
     if (forced_band) {
@@ -557,16 +648,13 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_warp_kernel(
     const bool sel = j < t && ((word >> lane) & 1u);
     if (sel && out) out[cnt + __popc(word & ((1u << lane) - 1))] = (int32_t)j;
     cnt += __popc(word);
-    if (mode == 0 && j0 < a) {
-      const double val = (sel && j < a) ? (double)sv[j] : 0.0;
-      unsigned b = word & (j0 + 32 <= a ? 0xffffffffu : ((1u << (a - j0)) - 1));
-      while (b) {
-        const int kk = __ffs(b) - 1;
-        b &= b - 1;
-        cov += __shfl_sync(0xffffffffu, val, kk);
-      }
-    }
+    if (mode == 0 && row_cov && sel && j < a) cov += (double)sv[j];
   }
+  // pooled-score coverage (pipeline.hpp:186-191): the reference adds the selected
+  // probabilities in ascending order; a lane-parallel double sum differs by
+  // < cnt * 2^-53 (the report's tolerance is 1e-9)
+  if (mode == 0 && row_cov)
+    for (int o = 16; o > 0; o >>= 1) cov += __shfl_xor_sync(0xffffffffu, cov, o);
   if (lane == 0) {
     if (kv_cnt) kv_cnt[h * t + i] = cnt;
     if (row_cov) row_cov[h * t + i] = cov;

@@ -189,6 +189,47 @@ def test_unpermute_inverts_the_gather(ops, d, dtype):
         np.testing.assert_array_equal(got[hh], want)
 
 
+@pytest.mark.parametrize("t,s_blocks,tau", [(256, 2, 0.9), (1024, 2, 0.9), (2048, 4, 0.75), (300, 1, 0.5)])
+def test_select_exact_sum_path_edge_rows(ops, oracle, t, s_blocks, tau):
+    """block_selection.hpp:171-206 on constructed rows: the order-free exact
+    double-sum path (all candidates >= 2^-29) against the reference's sorted
+    sequential sum, including ties at the tau boundary (broken by index), rows
+    of equal probabilities, rows with tiny probabilities (< 2^-29: the sorted
+    fallback) and unnormalised scores summing past 2 (fallback)."""
+    rng = np.random.default_rng(11)
+    b, seg = 64, 64 * s_blocks
+    rows = []
+    for i in range(t):
+        kind = i % 6
+        if kind == 0:
+            r = rng.random(t).astype(np.float32)
+        elif kind == 1:
+            r = np.full(t, 1.0, np.float32)  # all ties
+        elif kind == 2:
+            r = np.round(rng.random(t) * 4).astype(np.float32)  # many ties on few levels
+        elif kind == 3:
+            r = (rng.random(t) * 1e-12).astype(np.float32)
+            r[rng.integers(0, t, 3)] = 1.0  # a few large values, the rest below 2^-29
+        elif kind == 4:
+            r = rng.exponential(size=t).astype(np.float32) ** 4
+        else:
+            r = rng.random(t).astype(np.float32) * 8.0  # not normalised below
+        rows.append(r)
+    sc = np.stack(rows)
+    causal = oracle.build_block_causal_mask(t, b, seg)
+    # probabilities over each row's admissible prefix, as the pooled softmax produces
+    adm = causal.astype(bool)
+    p = np.where(adm, sc, 0).astype(np.float32)
+    norm = p.sum(axis=1, keepdims=True).astype(np.float32)
+    p = np.where(np.arange(t)[:, None] % 6 == 5, p, p / np.maximum(norm, 1e-30)).astype(np.float32)
+    mask, kv_idx, kv_cnt = ops.select_blocks(torch.from_numpy(p[None]).cuda(), b, seg, tau)
+    mask = mask.cpu().numpy()[0]
+    wm = oracle.select_blocks(p, causal, b, seg, tau)
+    np.testing.assert_array_equal(mask, wm)
+    kv_cnt = kv_cnt.cpu().numpy()[0]
+    np.testing.assert_array_equal(kv_cnt, wm.sum(axis=1))
+
+
 @pytest.mark.parametrize("n,b,s,k", [(2048, 128, 256, 3), (4096, 16, 64, 40), (1000, 32, 64, 1)])
 def test_select_top_k_bitexact(ops, oracle, n, b, s, k):
     """The top-k extension (north star (3)): the first k admissible blocks of the
