@@ -101,6 +101,11 @@ inline void apply_rows(const int32_t* perm, const void* src, int src_heads, int 
   check(pbs_apply_rows(perm, src, src_heads, dst_heads, (int64_t)rows, cols, dtype, dst, stream));
 }
 
+/// Workspace bytes build_query_permutation needs.
+inline std::size_t query_permutation_workspace_size(const pbs_shape& s, std::size_t block) {
+  return pbs_query_permutation_workspace_size(&s, (int64_t)block);
+}
+
 /// build_query_permutation (permutation.hpp:206-275); k may be K' (strategy both).
 inline void build_query_permutation(const void* q, const void* k, int k_heads, const pbs_shape& s,
                                     std::size_t block, std::size_t segment, int32_t* perm, int32_t* inv, void* ws,

@@ -135,6 +135,10 @@ PBS_API int pbs_build_query_permutation(const void* q, const void* k, int32_t k_
                                 int64_t segment_size, int32_t* perm, int32_t* inv,
                                 void* workspace, size_t workspace_bytes, void* stream);
 
+/* Device workspace bytes pbs_build_query_permutation needs for this shape and
+ * block size (0 on a bad shape). */
+PBS_API size_t pbs_query_permutation_workspace_size(const pbs_shape* shape, int64_t block_size);
+
 /* ---- stage 2: gathers --------------------------------------------------- */
 
 /* apply_rows (permutation.hpp:79-89), batched with a GQA broadcast:

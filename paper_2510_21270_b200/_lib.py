@@ -27,7 +27,7 @@ STRATEGIES = {"none": 0, "key_permute": 1, "query_permute": 2, "both": 3}
 # every symbol include/pbs_cabi.h declares
 EXPORTS = [
     "pbs_last_error", "pbs_version", "pbs_kernel_launches", "pbs_workspace_size", "pbs_estimate_key_importance",
-    "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_apply_rows", "pbs_unpermute",
+    "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_query_permutation_workspace_size", "pbs_apply_rows", "pbs_unpermute",
     "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_select_blocks_top_k", "pbs_block_sparse_attention_fwd",
     "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
     "pbs_coverage_workspace_size", "pbs_attention_coverage", "pbs_tensor_info_read", "pbs_tensor_load",
@@ -133,6 +133,7 @@ _SIGS = {
     "pbs_estimate_key_importance": (C.c_int, [VP, VP, C.POINTER(Shape), I64, DBL, VP, VP, SZ, VP]),
     "pbs_build_key_permutation": (C.c_int, [VP, I32, I64, I64, VP, VP, VP]),
     "pbs_build_query_permutation": (C.c_int, [VP, VP, I32, C.POINTER(Shape), I64, I64, VP, VP, VP, SZ, VP]),
+    "pbs_query_permutation_workspace_size": (SZ, [C.POINTER(Shape), I64]),
     "pbs_apply_rows": (C.c_int, [VP, VP, I32, I32, I64, I32, I32, VP, VP]),
     "pbs_unpermute": (C.c_int, [VP, VP, I32, I64, I32, I32, VP, VP]),
     "pbs_meanpool_block_scores": (C.c_int, [VP, VP, C.POINTER(Shape), I64, I64, DBL, VP, VP, SZ, VP]),

@@ -193,6 +193,12 @@ int pbs_build_query_permutation(const void* q, const void* k, int32_t k_heads, c
   return launch_segmented_sort(groups, 1, shape->num_q_heads, n, segment_size, perm, inv, st);
 }
 
+size_t pbs_query_permutation_workspace_size(const pbs_shape* shape, int64_t block_size) {
+  if (!shape || check_shape(shape) || block_size <= 0) return 0;
+  return query_perm_workspace_bytes(shape->num_q_heads, shape->seq_len, shape->head_dim, block_size) +
+         al((size_t)shape->num_q_heads * shape->seq_len * 4);
+}
+
 int pbs_apply_rows(const int32_t* perm, const void* src, int32_t src_heads, int32_t dst_heads, int64_t rows,
                    int32_t cols, int32_t dtype, void* dst, void* stream) {
   if (dtype != PBS_DTYPE_BF16 && dtype != PBS_DTYPE_F32) return fail(PBS_ERR_CONFIG, "E_CONFIG", "bad dtype");

@@ -21,6 +21,9 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
+
+#include <cstdio>
 
 #include "common.cuh"
 #include "exact_gemm.cuh"
@@ -493,6 +496,302 @@ __global__ void query_group_finalize_kernel(const unsigned long long* __restrict
   groups[g] = b ? (0xffffffffu - (uint32_t)(b & 0xffffffffu)) : (uint32_t)tc;
 }
 
+// ---- K3 screen (bf16, d = 128): tensor-core cosine screen + exact re-check ----
+// The assignment only needs each query's argmax.  The centroids (f32) are split
+// into bf16 hi + lo parts, so q . (c_hi + c_lo) on the tensor cores (mma.sync
+// m16n8k16, f32 accumulation) is within 4.3e-5 |q||c| of the reference's
+// sequential f32 dot (split residual 2^-18, accumulation 256 x 2^-23, the
+// reference's own rounding 128 x 2^-24).  With delta = 1e-4 (2.3x that bound):
+//  1. screen: a row whose best screened cosine beats every other centroid by
+//     more than 2 delta has the reference's argmax; the other rows are listed
+//     per KV head with their best screened score;
+//  2. the listed rows are screened again (the same MMA sequence, so identical
+//     scores): every centroid within 2 delta of the best is a candidate;
+//  3. the candidates' cosines are computed exactly as the reference does
+//     (sequential c, rounded products, IEEE division), argmax with the first
+//     index on ties; a row with more than kScrCand candidates scans every
+//     centroid exactly.
+constexpr int kScrMT = 2;                  // 16-row MMA tiles per warp (B fragments reused across them)
+constexpr int kScrRows = 8 * 16 * kScrMT;  // queries per CTA
+constexpr int kScrChunk = 64;              // centroids per shared-memory chunk
+constexpr int kScrPad = 136;               // bf16 per padded centroid row (272 B: conflict-free fragment loads)
+constexpr int kScrCand = 16;               // candidates kept per listed row
+constexpr float kScrDelta = 1e-4f;
+
+__global__ void centroid_split_kernel(const float* __restrict__ cent, const float* __restrict__ cn, int64_t rows,
+                                      __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
+                                      float* __restrict__ rinv, float* __restrict__ pen) {
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  for (int c = threadIdx.x; c < kScrPad; c += blockDim.x) {
+    const float x = c < 128 ? cent[r * 128 + c] : 0.0f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    hi[r * kScrPad + c] = h;
+    lo[r * kScrPad + c] = __float2bfloat16_rn(x - __bfloat162float(h));
+  }
+  if (threadIdx.x == 0) {
+    const float v = cn[r];
+    rinv[r] = v > 0.0f ? 1.0f / v : 0.0f;
+    pen[r] = v > 0.0f ? 0.0f : -INFINITY;
+  }
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+struct Best2 {
+  float m, s2;  // best and second-best scaled score
+  int j;        // index of the best
+};
+__device__ __forceinline__ void best2_push(Best2& b, float v, int j) {
+  if (v > b.m) {
+    b.s2 = b.m;
+    b.m = v;
+    b.j = j;
+  } else {
+    b.s2 = fmaxf(b.s2, v);
+  }
+}
+__device__ __forceinline__ Best2 best2_merge(Best2 a, Best2 o) {
+  const bool ob = o.m > a.m || (o.m == a.m && o.j < a.j);
+  Best2 r;
+  r.m = ob ? o.m : a.m;
+  r.j = ob ? o.j : a.j;
+  r.s2 = ob ? fmaxf(o.s2, a.m) : fmaxf(a.s2, o.m);
+  return r;
+}
+
+struct ScreenLists {
+  int32_t* count;  // [k_heads] listed rows per KV head
+  int32_t* rows;   // [k_heads][k_group * n] global row index h * n + i
+  float* best;     // [k_heads][k_group * n] best screened (scaled) score of the row
+  int32_t* cand;   // [k_heads][k_group * n][kScrCand]
+  int32_t* cand_n; // [k_heads][k_group * n]
+};
+
+// kListed = false: rows blockIdx.x * kScrRows.. of head blockIdx.y (decide or list);
+// kListed = true: the rows listed for KV head blockIdx.y (emit candidates).
+template <bool kListed>
+__global__ void __launch_bounds__(256) query_group_screen_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ chi, const __nv_bfloat16* __restrict__ clo,
+    const float* __restrict__ rinv, const float* __restrict__ pen, const float* __restrict__ qn, int k_group,
+    int64_t n, int64_t tc, uint32_t* __restrict__ groups, ScreenLists L) {
+  extern __shared__ __align__(16) unsigned char scr_smem[];
+  // [2 bufs][2 (hi, lo)][kScrChunk][kScrPad] bf16, then [2 bufs][2 (rinv, pen)][kScrChunk] f32
+  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(scr_smem);
+  float* sf = reinterpret_cast<float*>(scr_smem + (size_t)2 * 2 * kScrChunk * kScrPad * 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int hk = kListed ? (int)blockIdx.y : (int)blockIdx.y / k_group;
+  const int64_t list_base = (int64_t)hk * k_group * n;
+  const int64_t nrows = kListed ? (int64_t)L.count[hk] : n;
+  if ((int64_t)blockIdx.x * kScrRows >= nrows) return;
+  const int64_t r0 = (int64_t)blockIdx.x * kScrRows + warp * 16 * kScrMT;
+  auto row_of = [&](int64_t r) -> int64_t {  // global row (h * n + i) of local row r; past the end: the last row
+    r = min64(r, nrows - 1);
+    return kListed ? (int64_t)L.rows[list_base + r] : (int64_t)blockIdx.y * n + r;
+  };
+  uint32_t af[kScrMT][8][4];
+#pragma unroll
+  for (int mt = 0; mt < kScrMT; ++mt) {
+    const uint32_t* qa = reinterpret_cast<const uint32_t*>(q + row_of(r0 + mt * 16 + g) * 128);
+    const uint32_t* qb = reinterpret_cast<const uint32_t*>(q + row_of(r0 + mt * 16 + g + 8) * 128);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      af[mt][ks][0] = __ldg(qa + ks * 8 + t4);
+      af[mt][ks][1] = __ldg(qb + ks * 8 + t4);
+      af[mt][ks][2] = __ldg(qa + ks * 8 + 4 + t4);
+      af[mt][ks][3] = __ldg(qb + ks * 8 + 4 + t4);
+    }
+  }
+  // listed mode: the candidate threshold of each of this thread's rows
+  float thr[kScrMT][2];
+  if (kListed) {
+#pragma unroll
+    for (int mt = 0; mt < kScrMT; ++mt)
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int64_t r = min64(r0 + mt * 16 + g + 8 * hr, nrows - 1);
+        thr[mt][hr] = L.best[list_base + r] - 2.0f * kScrDelta * qn[L.rows[list_base + r]];
+      }
+  }
+  const __nv_bfloat16* ghi = chi + (int64_t)hk * tc * kScrPad;
+  const __nv_bfloat16* glo = clo + (int64_t)hk * tc * kScrPad;
+  const int nchunks = (int)((tc + kScrChunk - 1) / kScrChunk);
+  constexpr int kChunkElems = kScrChunk * kScrPad;  // per part
+  auto load_chunk = [&](int c, int buf) {
+    const int64_t j0 = (int64_t)c * kScrChunk;
+    const int rows = (int)min64(kScrChunk, tc - j0);
+    for (int part = 0; part < 2; ++part) {
+      const uint4* src = reinterpret_cast<const uint4*>((part ? glo : ghi) + j0 * kScrPad);
+      uint4* dst = reinterpret_cast<uint4*>(sb + (buf * 2 + part) * kChunkElems);
+      const int vecs = rows * kScrPad / 8;
+      for (int x = threadIdx.x; x < kChunkElems / 8; x += blockDim.x) {
+        const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(dst + x);
+        if (x < vecs) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + x) : "memory");
+        } else {
+          dst[x] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+    }
+    // column scales (rinv, pen): padding columns get pen = -inf so they never win
+    for (int x = threadIdx.x; x < 2 * kScrChunk; x += blockDim.x) {
+      const int part = x / kScrChunk, col = x % kScrChunk;
+      const int64_t j = j0 + col;
+      sf[(buf * 2 + part) * kScrChunk + col] =
+          j < tc ? __ldg((part ? pen : rinv) + hk * tc + j) : (part ? -INFINITY : 0.0f);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  Best2 bs[kScrMT][2];
+#pragma unroll
+  for (int mt = 0; mt < kScrMT; ++mt) bs[mt][0] = bs[mt][1] = Best2{-INFINITY, -INFINITY, 0};
+  auto take = [&](int mt, int hr, float v, int j) {
+    if (!kListed) {
+      best2_push(bs[mt][hr], v, j);
+    } else if (v >= thr[mt][hr]) {
+      const int64_t r = r0 + mt * 16 + g + 8 * hr;
+      if (r < nrows) {
+        const int slot = atomicAdd(&L.cand_n[list_base + r], 1);
+        if (slot < kScrCand) L.cand[(list_base + r) * kScrCand + slot] = j;
+      }
+    }
+  };
+  load_chunk(0, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nchunks) {
+      load_chunk(c + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t* bh = reinterpret_cast<const uint32_t*>(sb + (buf * 2 + 0) * kChunkElems);
+    const uint32_t* bl = reinterpret_cast<const uint32_t*>(sb + (buf * 2 + 1) * kChunkElems);
+    const float* sri = sf + (buf * 2 + 0) * kScrChunk;
+    const float* spe = sf + (buf * 2 + 1) * kScrChunk;
+    const int j0 = c * kScrChunk;
+#pragma unroll 2
+    for (int nt = 0; nt < kScrChunk / 8; ++nt) {
+      float acc[kScrMT][4];
+#pragma unroll
+      for (int mt = 0; mt < kScrMT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.0f;
+      const int rowb = (nt * 8 + g) * (kScrPad / 2);  // 32-bit words
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t h0 = bh[rowb + ks * 8 + t4], h1 = bh[rowb + ks * 8 + 4 + t4];
+        const uint32_t l0 = bl[rowb + ks * 8 + t4], l1 = bl[rowb + ks * 8 + 4 + t4];
+#pragma unroll
+        for (int mt = 0; mt < kScrMT; ++mt) {
+          mma_bf16_16816(acc[mt], af[mt][ks], h0, h1);
+          mma_bf16_16816(acc[mt], af[mt][ks], l0, l1);
+        }
+      }
+      const int col = nt * 8 + 2 * t4;
+      const float2 ri = *reinterpret_cast<const float2*>(sri + col);
+      const float2 pe = *reinterpret_cast<const float2*>(spe + col);
+#pragma unroll
+      for (int mt = 0; mt < kScrMT; ++mt) {
+        take(mt, 0, fmaf(acc[mt][0], ri.x, pe.x), j0 + col);
+        take(mt, 0, fmaf(acc[mt][1], ri.y, pe.y), j0 + col + 1);
+        take(mt, 1, fmaf(acc[mt][2], ri.x, pe.x), j0 + col);
+        take(mt, 1, fmaf(acc[mt][3], ri.y, pe.y), j0 + col + 1);
+      }
+    }
+    __syncthreads();
+  }
+  if (kListed) return;
+  // the quad's lanes hold disjoint centroid columns of the same rows
+#pragma unroll
+  for (int mt = 0; mt < kScrMT; ++mt)
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr)
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        Best2 x{__shfl_xor_sync(0xffffffffu, bs[mt][hr].m, o), __shfl_xor_sync(0xffffffffu, bs[mt][hr].s2, o),
+                __shfl_xor_sync(0xffffffffu, bs[mt][hr].j, o)};
+        bs[mt][hr] = best2_merge(bs[mt][hr], x);
+      }
+  if (t4 < 2) {
+#pragma unroll
+    for (int mt = 0; mt < kScrMT; ++mt) {
+      const Best2 b = t4 ? bs[mt][1] : bs[mt][0];
+      const int64_t r = r0 + mt * 16 + g + 8 * t4;
+      if (r >= n) continue;
+      const int64_t gi = (int64_t)blockIdx.y * n + r;
+      const float qv = qn[gi];
+      // scaled scores are cos * |q|; the screen decides only with a clear 2 delta margin
+      const float dq = kScrDelta * qv;
+      if (!(qv > 0.0f)) {
+        groups[gi] = (uint32_t)tc;  // no positive-norm match (permutation.hpp:246-258)
+      } else if (b.m > -INFINITY && b.s2 < b.m - 2.0f * dq && b.m > -qv + dq) {
+        groups[gi] = (uint32_t)b.j;
+      } else {
+        const int slot = atomicAdd(&L.count[hk], 1);
+        L.rows[list_base + slot] = (int32_t)gi;
+        L.best[list_base + slot] = b.m;
+      }
+    }
+  }
+}
+
+// stage 3: exact cosines (permutation.hpp:244-258) of each listed row's
+// candidates, one warp per row (lane = candidate); a row with more candidates
+// than kept (or none: the best was -inf) scans every centroid, lanes taking
+// j = lane, lane + 32, ... in increasing order.  Argmax with the first index on
+// ties, over sims > -1 only.
+__global__ void __launch_bounds__(256) query_group_exact_kernel(
+    const __nv_bfloat16* __restrict__ q, const float* __restrict__ cent, const float* __restrict__ qn,
+    const float* __restrict__ cn, int k_group, int64_t n, int64_t tc, ScreenLists L, uint32_t* __restrict__ groups) {
+  const int hk = blockIdx.y;
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t list_base = (int64_t)hk * k_group * n;
+  const int64_t rows = L.count[hk];
+  for (int64_t w = (int64_t)blockIdx.x * 8 + wl; w < rows; w += (int64_t)gridDim.x * 8) {
+    const int64_t gi = L.rows[list_base + w];
+    const int nc = L.cand_n[list_base + w];
+    const __nv_bfloat16* qi = q + gi * 128;
+    const float qv = qn[gi];
+    float best = -1.0f;
+    int bj = -1;
+    auto consider = [&](int64_t j) {
+      const float cv = cn[hk * tc + j];
+      float sim = -1.0f;
+      if (qv > 0.0f && cv > 0.0f) {
+        const float* cj = cent + ((int64_t)hk * tc + j) * 128;
+        float dot = 0.0f;
+        for (int c = 0; c < 128; ++c) dot = __fadd_rn(dot, __fmul_rn(__bfloat162float(qi[c]), __ldg(cj + c)));
+        sim = __fdiv_rn(dot, __fmul_rn(qv, cv));
+      }
+      if (sim > best || (sim == best && bj >= 0 && (int)j < bj && sim > -1.0f)) {
+        best = sim;
+        bj = (int)j;
+      }
+    };
+    if (nc >= 1 && nc <= kScrCand) {
+      if (lane < nc) consider(L.cand[(list_base + w) * kScrCand + lane]);
+    } else {
+      for (int64_t j = lane; j < tc; j += 32) consider(j);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (oj >= 0 && (bj < 0 || ob > best || (ob == best && oj < bj))) {
+        best = ob;
+        bj = oj;
+      }
+    }
+    if (lane == 0) groups[gi] = bj < 0 ? (uint32_t)tc : (uint32_t)bj;
+  }
+}
+
 inline int grid_for(int64_t total, int threads) {
   const int64_t b = (total + threads - 1) / threads;
   return (int)min64(b, 148 * 32);
@@ -648,7 +947,10 @@ int launch_segmented_sort(const void* keys, int key_kind, int heads, int64_t n, 
 
 size_t query_perm_workspace_bytes(int hq, int64_t n, int d, int64_t block) {
   const int64_t tc = ceil_div(n, block);
-  return (size_t)hq * tc * d * 4 + (size_t)hq * tc * 4 + (size_t)hq * n * 4 + (size_t)hq * n * 8 + 1024;
+  // centroids, their norms, |q|, the per-query best keys (exact path) or the
+  // fallback list (screen path), then the screen's split centroids and scales
+  return (size_t)hq * tc * d * 4 + (size_t)hq * tc * 4 + (size_t)hq * n * 4 + (size_t)hq * n * 8 +
+         (size_t)hq * n * 4 * (kScrCand + 2) + (size_t)hq * tc * (kScrPad * 4 + 8) + 4096;
 }
 
 int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_heads, int64_t n, int d,
@@ -665,7 +967,6 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
   p += (size_t)hq * n * 4;
   p = reinterpret_cast<char*>(((uintptr_t)p + 15) & ~(uintptr_t)15);
   unsigned long long* best = reinterpret_cast<unsigned long long*>(p);
-  PBS_CUDA_CHECK(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * hq * n, st));
   const size_t csmem = sizeof(float) * d;
   if (dtype == PBS_DTYPE_BF16) {
     centroid_kernel<__nv_bfloat16><<<dim3((unsigned)tc, (unsigned)k_heads), 128, csmem, st>>>(
@@ -674,6 +975,63 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
     qnorm_kernel<__nv_bfloat16><<<(unsigned)ceil_div((int64_t)hq * n, 128), 128, 0, st>>>(
         static_cast<const __nv_bfloat16*>(q), (int64_t)hq * n, d, qn);
     PBS_LAUNCH_CHECK("qnorm_kernel");
+    if (d == 128 && (uintptr_t)q % 16 == 0 && !getenv("PBS_QGROUP_EXACT")) {
+      // screen on the tensor cores, exact re-check of the undecided rows' candidates
+      const int kg = hq / k_heads;
+      char* p2 = reinterpret_cast<char*>(best);  // the exact path's per-row keys are not used here
+      ScreenLists SL;
+      SL.count = reinterpret_cast<int32_t*>(p2);
+      p2 += 1024;
+      SL.rows = reinterpret_cast<int32_t*>(p2);
+      p2 += (size_t)hq * n * 4;
+      SL.best = reinterpret_cast<float*>(p2);
+      p2 += (size_t)hq * n * 4;
+      SL.cand_n = reinterpret_cast<int32_t*>(p2);
+      p2 += (size_t)hq * n * 4;
+      SL.cand = reinterpret_cast<int32_t*>(p2);
+      p2 += (size_t)hq * n * 4 * kScrCand;
+      p2 = reinterpret_cast<char*>(((uintptr_t)p2 + 255) & ~(uintptr_t)255);
+      __nv_bfloat16* chi = reinterpret_cast<__nv_bfloat16*>(p2);
+      __nv_bfloat16* clo = chi + (size_t)k_heads * tc * kScrPad;
+      float* rinv = reinterpret_cast<float*>(clo + (size_t)k_heads * tc * kScrPad);
+      float* pen = rinv + (size_t)k_heads * tc;
+      PBS_CUDA_CHECK(cudaMemsetAsync(SL.count, 0, sizeof(int32_t) * k_heads, st));
+      PBS_CUDA_CHECK(cudaMemsetAsync(SL.cand_n, 0, sizeof(int32_t) * hq * n, st));
+      centroid_split_kernel<<<(unsigned)(k_heads * tc), 128, 0, st>>>(cent, cn, (int64_t)k_heads * tc, chi, clo,
+                                                                       rinv, pen);
+      PBS_LAUNCH_CHECK("centroid_split_kernel");
+      const size_t smem = (size_t)2 * 2 * kScrChunk * kScrPad * 2 + (size_t)2 * 2 * kScrChunk * 4;
+      static DeviceOnce scr_once;
+      if (int rc = once_per_device(scr_once, [smem] {
+            PBS_CUDA_CHECK(cudaFuncSetAttribute(query_group_screen_kernel<false>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PBS_CUDA_CHECK(cudaFuncSetAttribute(query_group_screen_kernel<true>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            return (int)PBS_OK;
+          }))
+        return rc;
+      const auto* qb = static_cast<const __nv_bfloat16*>(q);
+      query_group_screen_kernel<false><<<dim3((unsigned)ceil_div(n, kScrRows), (unsigned)hq), 256, smem, st>>>(
+          qb, chi, clo, rinv, pen, qn, kg, n, tc, groups, SL);
+      PBS_LAUNCH_CHECK("query_group_screen_kernel");
+      // the listed rows (at most every row of a KV group; CTAs past a head's count exit at once)
+      query_group_screen_kernel<true><<<dim3((unsigned)ceil_div((int64_t)kg * n, kScrRows), (unsigned)k_heads), 256,
+                                        smem, st>>>(qb, chi, clo, rinv, pen, qn, kg, n, tc, groups, SL);
+      PBS_LAUNCH_CHECK("query_group_screen_kernel");
+      query_group_exact_kernel<<<dim3((unsigned)num_sms() * 4, (unsigned)k_heads), 256, 0, st>>>(qb, cent, qn, cn, kg,
+                                                                                             n, tc, SL, groups);
+      PBS_LAUNCH_CHECK("query_group_exact_kernel");
+      if (getenv("PBS_QGROUP_STATS")) {  // debug: rows the screen left to the exact re-check
+        std::vector<int32_t> c(k_heads);
+        cudaMemcpyAsync(c.data(), SL.count, 4 * k_heads, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        long long tot = 0;
+        for (int x : c) tot += x;
+        fprintf(stderr, "query groups: %lld of %lld rows re-checked exactly\n", tot, (long long)hq * n);
+      }
+      return PBS_OK;
+    }
+    PBS_CUDA_CHECK(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * hq * n, st));
     const dim3 g3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq);
     if (d % 16 == 0)
       query_group_kernel<__nv_bfloat16, true><<<g3, xgemm::kThreads, 0, st>>>(
@@ -688,6 +1046,7 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
     qnorm_kernel<float><<<(unsigned)ceil_div((int64_t)hq * n, 128), 128, 0, st>>>(
         static_cast<const float*>(q), (int64_t)hq * n, d, qn);
     PBS_LAUNCH_CHECK("qnorm_kernel");
+    PBS_CUDA_CHECK(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * hq * n, st));
     const dim3 g3((unsigned)ceil_div(n, kTile), (unsigned)ceil_div(tc, kTile), (unsigned)hq);
     if (d % 16 == 0)
       query_group_kernel<float, true><<<g3, xgemm::kThreads, 0, st>>>(static_cast<const float*>(q), cent, qn, cn,

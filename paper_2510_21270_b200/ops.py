@@ -134,8 +134,10 @@ def build_query_permutation(q, k, block_size, segment_size, with_inverse=True):
     _check_dev(q, k)
     shape = make_shape(q, k)
     hq, n, d = q.shape
-    tc = -(-n // block_size)
-    need = hq * n * 4 + hq * tc * d * 4 + hq * tc * 4 + hq * n * 4 + hq * n * 8 + 8192
+    need = lib().pbs_query_permutation_workspace_size(C.byref(shape), block_size)
+    if need == 0:
+        check(lib().pbs_build_query_permutation(None, None, 0, C.byref(shape), block_size, segment_size,
+                                                None, None, None, 0, _stream()))
     ws = workspace(need, q.device)
     perm = torch.empty(hq, n, dtype=torch.int32, device=q.device)
     inv = torch.empty_like(perm) if with_inverse else None

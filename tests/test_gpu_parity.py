@@ -189,6 +189,37 @@ def test_unpermute_inverts_the_gather(ops, d, dtype):
         np.testing.assert_array_equal(got[hh], want)
 
 
+@pytest.mark.parametrize("hq,hkv,n,b,kind", [(4, 2, 16384, 128, "vertical_lines"), (2, 1, 4096, 64, "gaussian"),
+                                               (2, 2, 3000, 128, "adversarial")])
+def test_query_permutation_screen_matches_exact(ops, oracle, monkeypatch, hq, hkv, n, b, kind):
+    """build_query_permutation (permutation.hpp:206-275), bf16 d = 128: the
+    tensor-core cosine screen + exact re-check equals the all-exact SIMT path and
+    (sampled heads) the C restatement, including exact ties (duplicated key
+    blocks -> identical centroids: smallest index), a zero-norm centroid, zero
+    and anti-aligned queries."""
+    rng = np.random.default_rng(21)
+    d, seg = 128, 2 * b
+    tq, tk, tv, q, k, v = bf16_inputs(rng, hq, hkv, n, d, kind="gaussian" if kind == "adversarial" else kind)
+    if kind == "adversarial":
+        k[:, 3 * b:4 * b] = k[:, 0:b]          # identical centroids 0 and 3
+        k[:, 5 * b:6 * b] = k[:, 0:b]          # and 5
+        k[:, 7 * b:8 * b] = 0.0                # zero-norm centroid
+        cen = k[0, 0:b].mean(axis=0)
+        q[:, 10:20] = cen * 4                   # exactly aligned with the tied centroids
+        q[:, 20:30] = 0.0                       # zero-norm queries
+        q[:, 30:40] = -cen                      # anti-aligned
+        tq = torch.from_numpy(q).to(torch.bfloat16).cuda()
+        tk = torch.from_numpy(k).to(torch.bfloat16).cuda()
+        q, k = tq.float().cpu().numpy(), tk.float().cpu().numpy()
+    perm_s, inv_s = ops.build_query_permutation(tq, tk, b, seg)
+    monkeypatch.setenv("PBS_QGROUP_EXACT", "1")
+    perm_e, inv_e = ops.build_query_permutation(tq, tk, b, seg)
+    assert torch.equal(perm_s, perm_e) and torch.equal(inv_s, inv_e)
+    for h in (0, hq - 1):
+        want = oracle.build_query_permutation(q[h], k[kv_of(h, hq, hkv)], b, seg)
+        np.testing.assert_array_equal(perm_s[h].cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("t,s_blocks,tau", [(256, 2, 0.9), (1024, 2, 0.9), (2048, 4, 0.75), (300, 1, 0.5)])
 def test_select_exact_sum_path_edge_rows(ops, oracle, t, s_blocks, tau):
     """block_selection.hpp:171-206 on constructed rows: the order-free exact
