@@ -454,7 +454,11 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_warp_kernel(
       all = true;
     } else {
       uint32_t lo = 0u, hi = 0x7f800001u;  // crit(lo) holds, crit(hi) fails (no finite v >= +inf bits + 1)
-      while (hi - lo > 1u) {
+      // tau mode: any theta with crit(theta) is a valid candidate bound; stopping
+      // once theta is known to the exponent and 4 mantissa bits (C at most ~6%
+      // wider than the minimal set) leaves the exact prefix to the bisection over C
+      const uint32_t stop = (k_top > 0) ? 1u : (1u << 19);
+      while (hi - lo > stop) {
         const uint32_t mid = lo + (hi - lo) / 2u;
         if (crit(mid)) lo = mid;
         else hi = mid;
