@@ -85,7 +85,14 @@ static_assert((168 - kRegsControl) * 128 >= (kRegsSoftmax - 168) * kSoftmaxThrea
 #define PBS_POLY_PER16 0
 #endif
 constexpr int kPolyPer16 = PBS_POLY_PER16;
-constexpr int kItemRing = 4;
+#ifndef PBS_ITEM_RING
+#define PBS_ITEM_RING 1
+#endif
+// items claimed ahead of the consumers: a deep ring let the first CTAs to reach
+// a head's heavy items each hoard several of them (CTA end times spread over
+// 1.4 ms of a 5 ms 4-head launch with 4 slots, 0.6 ms with 2, 0.17 ms with 1;
+// e2e at C3 50.1 / 49.1 / 48.1 ms)
+constexpr int kItemRing = PBS_ITEM_RING;
 constexpr int kItemConsumers = 3 + kSoftmaxThreads / 32;  // warps 0, 1, 2 and the softmax warps
 constexpr int kPanelBytes = kBM * 128;            // 128 rows x 64 bf16 (SW128 panel)
 constexpr int kTileBytes = 2 * kPanelBytes;       // 128 x 128 bf16 = 32 KB
@@ -652,6 +659,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar->tmem_base;
+#ifdef PBS_ATTN_EVENTS
+  if (threadIdx.x == 0 && a.trace) {  // per-CTA start time (global ns)
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.trace[32 + 2048 * 8 + 512 + blockIdx.x] = gt;
+  }
+#endif
 
   if (warp < 4) {
    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
@@ -1006,6 +1020,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+#ifdef PBS_ATTN_EVENTS
+  if (threadIdx.x == 0 && a.trace) {  // per-CTA end time (global ns) for the launch's tail
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.trace[32 + 2048 * 8 + blockIdx.x] = gt;
+  }
+#endif
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -1287,7 +1308,7 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   if (const char* e = getenv("PBS_ATTN_GRID")) grid = (int)min64(grid, atoi(e) > 0 ? atoi(e) : grid);  // debug
   // debug (-DPBS_ATTN_SPANS builds): per-phase cycle sums of every CTA, dumped to $PBS_ATTN_TRACE
   const char* trace_path = getenv("PBS_ATTN_TRACE");
-  constexpr int kSpanWords = 32 + 2048 * 8;
+  constexpr int kSpanWords = 32 + 2048 * 8 + 1024;
   if (trace_path) {
     PBS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), kSpanWords * 8, st));
     PBS_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, kSpanWords * 8, st));
