@@ -130,7 +130,12 @@ void run(int warps) {
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
-int main() {
+int main(int argc, char**) {
+  if (argc > 1) {  // N sweep: does a narrow MMA cost proportionally less?
+    run<0, 256, 0, true>(1); run<0, 128, 0, true>(1); run<0, 64, 0, true>(1); run<0, 32, 0, true>(1); run<0, 16, 0, true>(1);
+    run<1, 64, 0, true>(1); run<1, 32, 0, true>(1);
+    return 0;
+  }
   run<0, 128, 0>(1); run<1, 128, 0>(1); run<2, 128, 0>(1); run<2, 128, 0, false, 2>(1);
   run<1, 128, 0, false, 3>(1); run<1, 128, 0, false, 4>(1); run<1, 128, 0, false, 5>(1);
   run<0, 128, 0, true>(1); run<0, 256, 0, true>(1);
