@@ -72,7 +72,7 @@ constexpr int kGroups = 2;                   // softmax warpgroups = query tiles
 constexpr int kCols = kBN;                   // key columns per softmax thread
 constexpr int kSoftmaxThreads = 128 * kGroups;
 constexpr int kThreads = 128 + kSoftmaxThreads;
-constexpr int kRegsControl = 72;                  // setmaxnreg: producers / MMA issuer / scheduler
+constexpr int kRegsControl = 88;                  // setmaxnreg: producers / MMA issuer / scheduler
 constexpr int kRegsSoftmax = 208;                 //             softmax warpgroups
 static_assert((168 - kRegsControl) * 128 >= (kRegsSoftmax - 168) * kSoftmaxThreads, "register file split");
 // keys of every 16 whose exp2 runs on the FMA pipe (polynomial) instead of the
