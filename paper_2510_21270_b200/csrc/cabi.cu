@@ -644,6 +644,7 @@ struct Arena {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   cudaEvent_t ev_rep[2] = {nullptr, nullptr};
   cudaEvent_t ev_comp[2] = {nullptr, nullptr};  // per slot: the group's compute is done (its inputs are free)
+  cudaEvent_t ev_q0a = nullptr;  // group 0's V and the first half of its Q are on the device
   std::vector<cudaEvent_t> ev_k;  // per KV head: its keys are on the device (estimate-first path)
   // per slot: stage timers and pinned copies of the report counters, so a
   // group's report is built while the next group computes
@@ -701,6 +702,7 @@ int arena_streams(Arena& A) {
     PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_comp[i], cudaEventDisableTiming));
     A.timer[i] = new Timer(true, A.st[1]);
   }
+  PBS_CUDA_CHECK(cudaEventCreateWithFlags(&A.ev_q0a, cudaEventDisableTiming));
   return PBS_OK;
 }
 }  // namespace
@@ -861,17 +863,21 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
   auto rep_hs = [&](int i) {
     return reinterpret_cast<int32_t*>(A.pinned + i * rep_bytes + al((size_t)g * t * 4) + al((size_t)g * t * 8));
   };
-  // Work chunks: one per KV group, except that the LAST group (key_permute, pi
-  // precomputed) runs in two head halves, so the output of the first goes back
-  // to the host while the second computes and the drain after the last kernel
-  // is half a group (single-head slices cost more in per-launch tails than
-  // they save in drain: measured 1.85 ms per 1-head slice vs 1.26 per head).
+  // Work chunks: one per KV group, except that the FIRST and the LAST group
+  // (key_permute, pi precomputed) run in two head halves: the first half of
+  // group 0 starts once its V and half of its Q are in (the fill before the
+  // first kernel is half a group's queries), and the output of the last group's
+  // first half goes back to the host while the second computes (the drain after
+  // the last kernel is half a group).  Single-head slices cost more in
+  // per-launch tails than they save: measured 1.85 ms per 1-head slice vs 1.26
+  // per head.
   struct Chunk {
     int64_t c, a, b;  // KV group c, its query heads [a, b) (local to the group)
   };
   std::vector<Chunk> chunks;
+  const bool split0 = est_first && g >= 2;
   for (int64_t c = 0; c < hkv; ++c) {
-    const int64_t parts = (est_first && c == hkv - 1) ? std::min<int64_t>(g, 2) : 1;
+    const int64_t parts = (est_first && (c == hkv - 1 || c == 0)) ? std::min<int64_t>(g, 2) : 1;
     for (int64_t j = 0; j < parts; ++j) chunks.push_back(Chunk{c, j * g / parts, (j + 1) * g / parts});
   }
   // fold the report of chunk kk (its counters were fetched on s_run) into the total
@@ -910,6 +916,16 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
     // s_run by ev_out below), so the inputs of the next group stream in while
     // the previous output is still being copied out
     if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_in, A.ev_comp[c % nslots], 0));
+    if (c == 0 && split0) {  // V, then Q in the two head halves of the first chunks
+      const size_t qh = (size_t)(g / 2) * n * d * es;
+      PBS_CUDA_CHECK(cudaMemcpyAsync(S.v, hv_, kvb, cudaMemcpyHostToDevice, s_in));
+      PBS_CUDA_CHECK(cudaMemcpyAsync(S.q, hq_, qh, cudaMemcpyHostToDevice, s_in));
+      PBS_CUDA_CHECK(cudaEventRecord(A.ev_q0a, s_in));
+      PBS_CUDA_CHECK(cudaMemcpyAsync(S.q + qh, hq_ + qh, qb - qh, cudaMemcpyHostToDevice, s_in));
+      PBS_CUDA_CHECK(cudaEventRecord(A.ev_in[0], s_in));
+      tr.mark("in: Q,V of group 0 landed", s_in);
+      return PBS_OK;
+    }
     PBS_CUDA_CHECK(cudaMemcpyAsync(S.q, hq_ + (size_t)c * qb, qb, cudaMemcpyHostToDevice, s_in));
     if (!est_first) PBS_CUDA_CHECK(cudaMemcpyAsync(S.k, hk_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
     PBS_CUDA_CHECK(cudaMemcpyAsync(S.v, hv_ + (size_t)c * kvb, kvb, cudaMemcpyHostToDevice, s_in));
@@ -949,9 +965,10 @@ int pbs_attention_host(const void* q, const void* k, const void* v, const pbs_sh
         if (int rc = copy_in(c + 1)) return rc;
       if (est_first && c == 1)
         if (int rc = estimate_groups(1, hkv)) return rc;
-      PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_in[i], 0));
       if (c >= nslots) PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, A.ev_out[i], 0));  // S.out copied out
     }
+    // the chunk's inputs: all of the group's, or for group 0's first half its V and half of its Q
+    PBS_CUDA_CHECK(cudaStreamWaitEvent(s_run, (c == 0 && split0 && ch.a == 0) ? A.ev_q0a : A.ev_in[i], 0));
     pbs_shape cs2 = cs;
     cs2.num_q_heads = (int32_t)(ch.b - ch.a);
     const size_t qoff = (size_t)ch.a * n * d * es, poff = (size_t)ch.a * n, moff = (size_t)ch.a * t * t;

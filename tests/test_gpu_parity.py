@@ -775,3 +775,33 @@ def test_two_processes_one_gpu_gather(ops, tmp_path):
     path = str(tmp_path / "ok.pt")
     mp.spawn(_two_process_worker, args=(2, port, path), nprocs=2, join=True)
     assert torch.load(path)["ok"]
+
+
+# ---------------------------------------------------------------------------
+def test_c1_config_end_to_end_matches_reference(ops, ref):
+    """BASELINE configs[0] (C1): one head, N = 4096, d = 128, B = 64, S = 256,
+    tau = 0.9, key_permute, fp32, inputs from the reference's own generator
+    (pbs::generate_head, vertical lines, seed 1, 16 lines of strength 150;
+    workload.hpp:145-198), run by the unmodified reference pbs_attention
+    (pipeline.hpp:107-193) and by both device entries (inputs resident, and the
+    host-buffer call).  pi / sigma / mask / counts bit-exact, output within the
+    f32 bar (scripts/c1_bench.py times the same case)."""
+    from oracle import make_config as ref_config
+    from oracle.gen_golden import generate_head
+
+    n, d, b, s, tau = 4096, 128, 64, 256, 0.9
+    q, k, v, _ = generate_head(ref, "vertical_lines", n, d, 1, b, s, line_count=16, line_strength=150.0,
+                               dtype=np.float32)
+    rr = ref.pbs_attention(q, k, v, ref_config(block_size=b, segment_size=s, tau=tau, strategy="key_permute"))
+    cfg = ops.make_config(block_size=b, segment_size=s, tau=tau, strategy="key_permute")
+    tq, tk, tv = (torch.from_numpy(x[None].copy()) for x in (q, k, v))
+    dev = ops.pbs_attention(tq.cuda(), tk.cuda(), tv.cuda(), cfg)
+    host = ops.pbs_attention_host(tq, tk, tv, cfg, return_perms=True)
+    for res in (dev, host):
+        np.testing.assert_array_equal(res.pi.cpu().numpy()[0], rr.pi)
+        np.testing.assert_array_equal(res.sigma.cpu().numpy()[0], rr.sigma)
+        np.testing.assert_array_equal(res.mask.cpu().numpy()[0], rr.mask)
+        assert_f32(np.abs(res.output.cpu().numpy()[0] - rr.output))
+        for key in ("selected_blocks", "total_admissible_blocks"):
+            assert res.report[key] == rr.report[key]
+        assert res.report["block_density"] == rr.report["block_density"]
