@@ -323,6 +323,35 @@ PBS_API int pbs_tensor_load(const char* path, void* dst, int32_t dst_dtype, void
 PBS_API int pbs_tensor_save(const char* path, const void* src, int32_t src_dtype, int64_t heads, int64_t rows,
                             int64_t cols, int32_t file_dtype, int32_t as_stack, void* stream);
 
+/* ---- synthetic workloads (workload.hpp, rng.hpp) -------------------------- */
+/* WorkloadSpec (workload.hpp:21-38) for run manifests that name a `workload`
+ * (manifest.hpp:26-39) instead of input files. */
+enum pbs_workload_kind {
+  PBS_WORKLOAD_GAUSSIAN = 0,
+  PBS_WORKLOAD_VERTICAL_LINES = 1,
+  PBS_WORKLOAD_BLOCK_DIAG = 2,
+  PBS_WORKLOAD_MIXED = 3
+};
+enum pbs_line_scatter { PBS_SCATTER_CLUSTERED = 0, PBS_SCATTER_SCATTERED = 1 };
+enum pbs_host_dtype { PBS_HOST_F32 = 0, PBS_HOST_F64 = 1 };
+typedef struct pbs_workload_spec {
+  int32_t kind;         /* pbs_workload_kind (default gaussian) */
+  int32_t scatter;      /* pbs_line_scatter (default scattered) */
+  int64_t n, d, heads;  /* defaults 1024, 64, 1 */
+  uint64_t seed;        /* default 0 */
+  int64_t line_count;   /* default 8 */
+  double line_strength; /* default 150 */
+} pbs_workload_spec;
+/* generate_head (workload.hpp:145-198) on the HOST: head `head` of the
+ * workload into row-major [n, d] host buffers q, k, v of host_dtype (the
+ * manifest's precision), bit-identical to the reference generator; the planted
+ * line positions go to `planted` (capacity line_count, may be NULL) and their
+ * number to *planted_count.  Validation and error texts of
+ * WorkloadSpec::validate. */
+PBS_API int pbs_generate_workload_head(const pbs_workload_spec* spec, int64_t head, int64_t block_size,
+                                       int64_t segment_size, int32_t host_dtype, void* q, void* k, void* v,
+                                       int64_t* planted, int64_t* planted_count);
+
 /* ---- device memory (for FFI callers without the CUDA runtime) ------------ */
 #define PBS_COPY_H2D 0
 #define PBS_COPY_D2H 1

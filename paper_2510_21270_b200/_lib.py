@@ -26,7 +26,7 @@ STRATEGIES = {"none": 0, "key_permute": 1, "query_permute": 2, "both": 3}
 
 # every symbol include/pbs_cabi.h declares
 EXPORTS = [
-    "pbs_last_error", "pbs_version", "pbs_kernel_launches", "pbs_workspace_size", "pbs_estimate_key_importance",
+    "pbs_last_error", "pbs_generate_workload_head", "pbs_version", "pbs_kernel_launches", "pbs_workspace_size", "pbs_estimate_key_importance",
     "pbs_build_key_permutation", "pbs_build_query_permutation", "pbs_query_permutation_workspace_size", "pbs_apply_rows", "pbs_unpermute",
     "pbs_meanpool_block_scores", "pbs_select_blocks", "pbs_select_blocks_top_k", "pbs_block_sparse_attention_fwd",
     "pbs_dense_causal_attention_fwd", "pbs_check_status", "pbs_attention", "pbs_attention_host",
@@ -84,6 +84,22 @@ class TensorInfo(C.Structure):
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class WorkloadSpec(C.Structure):
+    """pbs_workload_spec == WorkloadSpec (workload.hpp:21-38), the reference's defaults."""
+
+    _fields_ = [("kind", C.c_int32), ("scatter", C.c_int32), ("n", C.c_int64), ("d", C.c_int64),
+                ("heads", C.c_int64), ("seed", C.c_uint64), ("line_count", C.c_int64), ("line_strength", C.c_double)]
+
+    def __init__(self, **kw):
+        super().__init__(kind=0, scatter=1, n=1024, d=64, heads=1, seed=0, line_count=8, line_strength=150.0)
+        for key, value in kw.items():
+            setattr(self, key, value)
+
+
+WORKLOAD_KINDS = {"gaussian": 0, "vertical_lines": 1, "block_diag": 2, "mixed": 3}
+LINE_SCATTER = {"clustered": 0, "scattered": 1}
 
 
 class PbsError(RuntimeError):
@@ -153,6 +169,7 @@ _SIGS = {
     "pbs_tensor_load": (C.c_int, [C.c_char_p, VP, I32, VP]),
     "pbs_tensor_save": (C.c_int, [C.c_char_p, VP, I32, I64, I64, I64, I32, I32, VP]),
     "pbs_debug_expf": (C.c_int, [VP, VP, I64, VP]),
+    "pbs_generate_workload_head": (C.c_int, [C.POINTER(WorkloadSpec), I64, I64, I64, I32, VP, VP, VP, VP, VP]),
     "pbs_malloc": (C.c_int, [SZ, C.POINTER(VP)]),
     "pbs_free": (C.c_int, [VP]),
     "pbs_memcpy": (C.c_int, [VP, VP, SZ, I32, VP]),

@@ -21,8 +21,13 @@ is refused with E_CONFIG unless the caller opts into a lower device precision
 (`--device-precision f32|bf16`, or run_manifest(device_precision=...)); the
 output file keeps the manifest's dtype.  Other differences, by design: there is
 no N^2 limit on the coverage (pbs_main.cpp:202-207 refuses N^2 > 2^26 on the
-CPU); `workload` manifests (the reference's synthetic generator) are refused --
-generate the tensors with the reference and pass them as `inputs`.
+CPU).
+
+`workload` manifests (manifest.hpp:26-39) are generated on the host by the
+library's restatement of the reference generator (pbs_generate_workload_head,
+workload.hpp:145-198, bit-identical tensors in the manifest's precision), then
+uploaded and run like `inputs`; `--seed` overrides the workload seed as the
+CLI does (pbs_main.cpp:56).
 """
 from __future__ import annotations
 
@@ -66,9 +71,10 @@ class RunManifest:
     """RunManifest (manifest.hpp:28-39), `inputs` form; pipeline defaults of
     PipelineConfig (pipeline.hpp:30-37) and ForcedPolicy (block_selection.hpp:163-166)."""
 
-    q: str
-    k: str
-    v: str
+    q: str = ""
+    k: str = ""
+    v: str = ""
+    workload: dict | None = None  # WorkloadSpec fields (workload_from_json), or None for `inputs`
     block_size: int = 128
     segment_size: int = 256
     tau: float = 0.9
@@ -87,6 +93,36 @@ class RunManifest:
                                forced_diagonal_band=self.force_diagonal_band, scale=self.scale)
 
 
+_WORKLOAD_DEFAULTS = {"kind": "gaussian", "n": 1024, "d": 64, "heads": 1, "seed": 0, "line_count": 8,
+                      "line_strength": 150.0, "scatter": "scattered"}
+
+
+def workload_from_json(j: dict) -> dict:
+    """workload_from_json (manifest.hpp:76-93) + WorkloadSpec::validate
+    (workload.hpp:30-37), the reference's defaults and error texts."""
+    if not isinstance(j, dict):
+        raise _config_error('bad value for "workload"')
+    _expect_keys(j, tuple(_WORKLOAD_DEFAULTS), "workload")
+    w = dict(_WORKLOAD_DEFAULTS)
+    for key in ("kind", "scatter"):
+        w[key] = _read(j, key, str, w[key])
+    for key in ("n", "d", "heads", "seed", "line_count"):
+        w[key] = _read(j, key, int, w[key])
+    w["line_strength"] = _read(j, "line_strength", float, w["line_strength"])
+    if w["kind"] not in _lib.WORKLOAD_KINDS:
+        raise _config_error(f"unknown workload kind '{w['kind']}'")
+    if w["scatter"] not in _lib.LINE_SCATTER:
+        raise _config_error(f"unknown scatter mode '{w['scatter']}'")
+    if w["n"] == 0 or w["d"] == 0 or w["heads"] == 0:
+        raise _config_error("workload dims must be >= 1")
+    if w["kind"] in ("vertical_lines", "mixed"):
+        if w["line_count"] > w["n"]:
+            raise _config_error("line count exceeds sequence length")
+        if w["line_strength"] <= 0:
+            raise _config_error("line strength must be > 0")
+    return w
+
+
 def manifest_from_json(j: dict) -> RunManifest:
     """manifest_from_json (manifest.hpp:143-166)."""
     if not isinstance(j, dict):
@@ -95,14 +131,14 @@ def manifest_from_json(j: dict) -> RunManifest:
     if ("workload" in j) == ("inputs" in j):
         raise _config_error('manifest needs exactly one of "workload" or "inputs"')
     if "workload" in j:
-        raise _config_error('"workload" manifests are not run on the device path: generate the tensors with the '
-                            'reference (pbs gen) and pass them as "inputs"')
-    inp = j["inputs"]
-    _expect_keys(inp, ("q", "k", "v"), "inputs")
-    q, k, v = (_read(inp, x, str, "") for x in ("q", "k", "v"))
-    if not q or not k or not v:
-        raise _config_error("inputs need all of q, k, v paths")
-    m = RunManifest(q, k, v)
+        m = RunManifest(workload=workload_from_json(j["workload"]))
+    else:
+        inp = j["inputs"]
+        _expect_keys(inp, ("q", "k", "v"), "inputs")
+        q, k, v = (_read(inp, x, str, "") for x in ("q", "k", "v"))
+        if not q or not k or not v:
+            raise _config_error("inputs need all of q, k, v paths")
+        m = RunManifest(q, k, v)
     p = j.get("pipeline", {})
     _expect_keys(p, ("block_size", "segment_size", "tau", "strategy", "precision", "force_first_block",
                      "force_diagonal_band", "scale"), "pipeline")
@@ -177,14 +213,25 @@ def device_dtype(m: RunManifest, device_precision=None):
                         "bf16 to run an f64 manifest at lower precision)")
 
 
-def run_manifest(m: RunManifest, base_dir=".", device_precision=None) -> dict:
-    """The CLI's `run` (pbs_main.cpp:197-232) on the GPU; returns the report document."""
+def workload_tensors(m: RunManifest, dtype):
+    """generate_workload (workload.hpp:200-213) in the manifest's precision on
+    the host, every head, then to the device as [heads, n, d] of `dtype`."""
+    import numpy as np
     import torch
 
     from . import ops
 
-    def resolve(p):
-        return p if os.path.isabs(p) else os.path.join(base_dir, p)
+    w = m.workload
+    spec = ops.workload_spec(**w)
+    host_prec = "f32" if m.precision == "f32" else "f64"
+    heads = [ops.generate_workload_head(spec, h, m.block_size, m.segment_size, host_prec) for h in range(w["heads"])]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return tuple(torch.from_numpy(np.stack([hd[i] for hd in heads])).to(dev).to(dtype) for i in range(3))
+
+
+def _load_inputs(m: RunManifest, resolve, dt):
+    """load_inputs' `inputs` branch (pbs_main.cpp:83-97) straight to the device."""
+    from . import ops
 
     infos = [ops.tensor_info(resolve(x)) for x in (m.q, m.k, m.v)]
     hc = [i["heads"] for i in infos]
@@ -198,10 +245,27 @@ def run_manifest(m: RunManifest, base_dir=".", device_precision=None) -> dict:
         raise _config_error(f"pipeline expects self-attention: N == M, got {qr} vs {kr}")
     if qc != kc or kr != vr or vc != kc:
         raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, "E_SHAPE: pipeline inputs have inconsistent shapes")
-    dt = device_dtype(m, device_precision)
     q, k, v = (ops.load_tensor(resolve(x), dtype=dt) for x in (m.q, m.k, m.v))
     from_stack = any(i["ndim"] == 3 for i in infos)
     q, k, v = (x if x.dim() == 3 else x.unsqueeze(0) for x in (q, k, v))
+    return q, k, v, from_stack
+
+
+def run_manifest(m: RunManifest, base_dir=".", device_precision=None) -> dict:
+    """The CLI's `run` (pbs_main.cpp:197-232) on the GPU; returns the report document."""
+    import torch
+
+    from . import ops
+
+    def resolve(p):
+        return p if os.path.isabs(p) else os.path.join(base_dir, p)
+
+    dt = device_dtype(m, device_precision)
+    if m.workload is not None:
+        q, k, v = workload_tensors(m, dt)
+        from_stack = q.shape[0] > 1  # generate_workload's heads (pbs_main.cpp:74-80)
+    else:
+        q, k, v, from_stack = _load_inputs(m, resolve, dt)
     cfg = m.config()
     outs, reports = [], []
     for h in range(q.shape[0]):
@@ -246,7 +310,10 @@ def sweep_manifest(m: RunManifest, base_dir=".", taus=(), segments=(), strategie
         return p if os.path.isabs(p) else os.path.join(base_dir, p)
 
     dt = device_dtype(m, device_precision)
-    q, k, v = (ops.load_tensor(resolve(x), dtype=dt) for x in (m.q, m.k, m.v))
+    if m.workload is not None:
+        q, k, v = workload_tensors(m, dt)
+    else:
+        q, k, v = (ops.load_tensor(resolve(x), dtype=dt) for x in (m.q, m.k, m.v))
     q, k, v = (x[:1] if x.dim() == 3 else x.unsqueeze(0) for x in (q, k, v))
     taus = list(taus) or [m.tau]
     segments = list(segments) or [m.segment_size]
@@ -273,6 +340,7 @@ def main(argv=None) -> int:
     r.add_argument("--manifest", required=True)
     r.add_argument("--device-precision", choices=["f32", "bf16"], default=None,
                    help="device element type (default: the manifest's precision; f64 needs this)")
+    r.add_argument("--seed", type=int, default=None, help="Workload seed override")
     sw = sub.add_parser("sweep", help="Density/coverage/error sweep as CSV")
     sw.add_argument("--manifest", required=True)
     sw.add_argument("--tau-list", default="")
@@ -280,9 +348,12 @@ def main(argv=None) -> int:
     sw.add_argument("--strategies", default="")
     sw.add_argument("--out", default="")
     sw.add_argument("--device-precision", choices=["f32", "bf16"], default=None)
+    sw.add_argument("--seed", type=int, default=None, help="Workload seed override")
     args = ap.parse_args(argv)
     try:
         m = load_manifest(args.manifest)
+        if args.seed is not None and m.workload is not None:  # apply_overrides (pbs_main.cpp:56)
+            m.workload["seed"] = args.seed
         base = os.path.dirname(os.path.abspath(args.manifest))
         if args.cmd == "run":
             run_manifest(m, base, args.device_precision)

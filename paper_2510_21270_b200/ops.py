@@ -391,6 +391,34 @@ def save_tensor(path, t: torch.Tensor, file_dtype="f32", as_stack=None):
                                 _stream()))
 
 
+def workload_spec(kind="gaussian", n=1024, d=64, heads=1, seed=0, line_count=8, line_strength=150.0,
+                  scatter="scattered") -> "_lib.WorkloadSpec":
+    """WorkloadSpec (workload.hpp:21-38) with the reference's defaults; kind and
+    scatter by their manifest names (workload_kind_from_name, scatter_from_name)."""
+    if kind not in _lib.WORKLOAD_KINDS:
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, f"E_CONFIG: unknown workload kind '{kind}'")
+    if scatter not in _lib.LINE_SCATTER:
+        raise _lib.ConfigError(_lib.PBS_ERR_CONFIG, f"E_CONFIG: unknown scatter mode '{scatter}'")
+    return _lib.WorkloadSpec(kind=_lib.WORKLOAD_KINDS[kind], scatter=_lib.LINE_SCATTER[scatter], n=n, d=d,
+                             heads=heads, seed=seed, line_count=line_count, line_strength=line_strength)
+
+
+def generate_workload_head(spec, head, block_size, segment_size, precision="f32"):
+    """generate_head (workload.hpp:145-198) on the host, bit-identical to the
+    reference: numpy q, k, v [n, d] in the manifest precision (f32 / f64) and
+    the planted line positions."""
+    import numpy as np
+
+    dt = {"f32": np.float32, "f64": np.float64}[precision]
+    q, k, v = (np.empty((spec.n, spec.d), dtype=dt) for _ in range(3))
+    planted = np.zeros(max(int(spec.line_count), 1), dtype=np.int64)
+    cnt = C.c_int64(0)
+    check(lib().pbs_generate_workload_head(C.byref(spec), head, block_size, segment_size,
+                                           0 if precision == "f32" else 1, q.ctypes.data, k.ctypes.data,
+                                           v.ctypes.data, planted.ctypes.data, C.byref(cnt)))
+    return q, k, v, planted[:cnt.value]
+
+
 def debug_expf(x: torch.Tensor) -> torch.Tensor:
     _check_dev(x)
     y = torch.empty_like(x)
