@@ -71,10 +71,13 @@ def parse():
                     help="permutation strategy (the paper's operating point is key_permute)")
     ap.add_argument("--top-k", type=int, default=0,
                     help="select the top-k blocks per row instead of the tau threshold (extension)")
+    ap.add_argument("--block", type=int, choices=[64, 128], default=128,
+                    help="block size B (128: the paper's configs; 64: the variant, 2 x 2 blocks per tensor-core tile)")
     args = ap.parse_args()
-    global HQ, HKV, N, PREFIX, STRATEGY
+    global HQ, HKV, N, PREFIX, STRATEGY, BLOCK
     HQ, HKV, N, PREFIX = MODELS[args.model]
     STRATEGY = args.strategy
+    BLOCK = args.block
     if args.seq is None:
         args.seq = N
     return args
@@ -474,7 +477,7 @@ def main():
     # DRAM bytes per attention launch from an ncu capture of THIS workload (profiles/attn_traffic.json,
     # keyed by config.workload; null when no capture of this config exists)
     workload = f"{PREFIX}_{n // 1024}k_pbs" + (f"_{STRATEGY}" if STRATEGY != "key_permute" else "") + \
-        (f"_top{args.top_k}" if args.top_k else "")
+        (f"_top{args.top_k}" if args.top_k else "") + (f"_b{BLOCK}" if BLOCK != 128 else "")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tpath) and world == 1:

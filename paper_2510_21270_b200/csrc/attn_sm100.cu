@@ -358,8 +358,11 @@ __host__ __device__ constexpr uint32_t make_idesc(uint32_t a_mn_major, uint32_t 
 
 struct KernelArgs {
   int hq, kv_heads, group;
-  int64_t n, t;
-  int64_t npairs;  // ceil(t / 2): items are (head, pair of query blocks 2p, 2p + 1)
+  int64_t n, t;    // t = ceil(n / block): query / key blocks of the selection
+  int64_t block;   // B: 128, or 64 (sub-blocked tiles, below)
+  int sub;         // B = 64: a 128 x 128 tile holds 2 x 2 selection blocks with their own classes
+  int64_t t128;    // ceil(n / 128): tiles per head
+  int64_t npairs;  // ceil(t128 / 2): items are (head, pair of query tiles 2p, 2p + 1)
   int64_t p_lo, p_hi;  // pairs [p_lo, p_hi) of every head (a shard's query-block range)
   float scale_log2;
   const int32_t* kv_idx;
@@ -429,20 +432,20 @@ __device__ __forceinline__ Item item_of(const KernelArgs& a, int64_t idx) {
 
 __device__ __forceinline__ int2 q_range(const KernelArgs& a, int h, int64_t qb) {
   if (a.q_mm) return a.q_mm[(int64_t)h * a.t + qb];
-  const int64_t lo = qb * kBM;
-  return make_int2((int)lo, (int)(min64(a.n, lo + kBM) - 1));
+  const int64_t lo = qb * a.block;
+  return make_int2((int)lo, (int)(min64(a.n, lo + a.block) - 1));
 }
 __device__ __forceinline__ int2 k_range(const KernelArgs& a, int h, int64_t kb) {
   if (a.k_mm) return a.k_mm[(int64_t)h * a.t + kb];
-  const int64_t lo = kb * kBN;
-  return make_int2((int)lo, (int)(min64(a.n, lo + kBN) - 1));
+  const int64_t lo = kb * a.block;
+  return make_int2((int)lo, (int)(min64(a.n, lo + a.block) - 1));
 }
 
 // 0 none, 1 partial, 2 full (AdmissibilityIndex::classify); a ragged key block is
 // treated as partial so that keys past N are masked.
 __device__ __forceinline__ int block_class(const KernelArgs& a, int h, int64_t qb, int64_t kb) {
   const bool masked = a.causal || a.q_orig || a.k_orig;
-  const bool ragged = (kb + 1) * kBN > a.n;
+  const bool ragged = (kb + 1) * a.block > a.n;
   if (!masked) return ragged ? 1 : 2;
   const int2 qr = q_range(a, h, qb), kr = k_range(a, h, kb);
   if (kr.y <= qr.x) return ragged ? 1 : 2;
@@ -467,16 +470,31 @@ __device__ __forceinline__ Visit visit_begin(const KernelArgs& a, const Item& it
     v.list = nullptr;
     v.len = (int)(min64(2 * it.p + 1, a.t - 1) + 1);  // 0 .. last query block of the pair
   } else {
-    v.list = a.vis + ((int64_t)it.h * a.npairs + it.p) * a.t;
+    v.list = a.vis + ((int64_t)it.h * a.npairs + it.p) * a.t128;
     v.len = a.nvis[(int64_t)it.h * a.npairs + it.p];
   }
   return v;
 }
 
+// Sub-blocked entries (B = 64): kt | sc << 16, sc = 2-bit classes of the 8
+// selection blocks of the entry, bit 2 * (4 w + 2 a + b) for tile w, query half
+// a (rows 64a..) and key half b (keys 64b..)
+constexpr int kSubShift = 16;
+__device__ __forceinline__ int sub_class(uint32_t sc, int w, int a_half, int b_half) {
+  return (int)((sc >> (2 * (4 * w + 2 * a_half + b_half))) & 3u);
+}
+// tile w's class from its four blocks: 0 none visited, 2 all four full, else 1
+__device__ __forceinline__ int tile_class(uint32_t sc, int w) {
+  const uint32_t q = (sc >> (8 * w)) & 0xffu;
+  return q == 0 ? 0 : (q == 0xaau ? 2 : 1);
+}
+
 // all 32 lanes of the warp must call this with the same e (e non-decreasing);
-// c0 / c1: the block's class for tile 0 / tile 1 (0 = not visited by that tile)
+// c0 / c1: the block's class for tile 0 / tile 1 (0 = not visited by that tile);
+// sc: the sub-blocked classes (B = 64), else 0
 __device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, Visit& v, int e, int lane,
-                                          int64_t& kb, int& c0, int& c1) {
+                                          int64_t& kb, int& c0, int& c1, uint32_t& sc) {
+  sc = 0;
   if (a.dense) {
     kb = e;
     const bool ragged = (kb + 1) * kBN > a.n;
@@ -490,9 +508,23 @@ __device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, V
     v.cache = (v.base + lane < v.len) ? (uint32_t)__ldg(v.list + v.base + lane) : 0u;
   }
   const uint32_t x = __shfl_sync(0xffffffffu, v.cache, e - v.base);
+  if (a.sub) {
+    kb = x & ((1u << kSubShift) - 1u);
+    sc = x >> kSubShift;
+    c0 = tile_class(sc, 0);
+    c1 = tile_class(sc, 1);
+    return;
+  }
   kb = x & kKbMask;
   c0 = (int)((x >> kKbBits) & 3u);
   c1 = (int)((x >> (kKbBits + 2)) & 3u);
+}
+
+// overload for the roles that only need the tiles' classes
+__device__ __forceinline__ void visit_get(const KernelArgs& a, const Item& it, Visit& v, int e, int lane,
+                                          int64_t& kb, int& c0, int& c1) {
+  uint32_t sc;
+  visit_get(a, it, v, e, lane, kb, c0, c1, sc);
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
@@ -682,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (kp && lane == 0) {
         for (int w = 0; w < kGroups; ++w) {
           int64_t qb = 2 * it.p + w;
-          if (qb >= a.t) qb = 2 * it.p;  // a lone last tile: tile 1's buffer gets tile 0's rows (never read)
+          if (qb >= a.t128) qb = 2 * it.p;  // a lone last tile: tile 1's buffer gets tile 0's rows (never read)
           mbar_wait_backoff(&bar->q_empty[w], (q_it & 1) ^ 1);
           mbar_expect_tx(&bar->q_full[w], kTileBytes);
           for (int p = 0; p < 2; ++p)
@@ -869,9 +901,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t idx; (idx = items.next(bar, lane)) >= 0;) {
       const Item it = item_of(a, idx);
       Visit vis = visit_begin(a, it);
-      const int64_t qb = 2 * it.p + w;
+      const int64_t qb = 2 * it.p + w;  // query tile (128 rows)
       const int64_t i = qb * kBM + row;
-      const bool valid = qb < a.t && i < a.n;
+      const bool valid = qb < a.t128 && i < a.n;
+      // the selection block of this thread's row (degenerate-row reports)
+      const int64_t qsel = a.sub ? 2 * qb + (row >> 6) : qb;
       const int qo = valid ? (a.q_orig ? a.q_orig[(int64_t)it.h * a.n + i] : (int)i) : -1;
       float m = -INFINITY;  // running max (log2 domain)
       float l = 0.0f;       // running sum
@@ -879,8 +913,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = 0; e < vis.len; ++e) {
         int64_t kb;
         int c0, c1;
+        uint32_t scl;
         EVT(row == 0 && w == 0 && s_cnt < 1024, 1024 + s_cnt, 0);
-        visit_get(a, it, vis, e, lane, kb, c0, c1);
+        visit_get(a, it, vis, e, lane, kb, c0, c1, scl);
         const int cls = w ? c1 : c0;
         if (cls == 0) continue;  // warp-uniform: a block's class is the tile's
         any = true;
@@ -921,12 +956,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           // time, so the 128 scores below are loaded already masked
 #pragma unroll 1
           for (int c = 0; c < kCols / 32; ++c) {
+            // B = 64: this warp's query half against key half c / 2 -- a block
+            // not selected for it is masked whole, a full one not at all
+            const int bc = a.sub ? sub_class(scl, w, quad >> 1, c >> 1) : 1;
+            if (bc == 2) continue;
             uint32_t t32[32];
             TMEM_LD32(tS + c * 32, t32);
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (ko[c * 32 + j] > qo) t32[j] = 0xff800000u;  // -inf: inadmissible (attention.hpp:298-300)
+              if (bc == 0 || ko[c * 32 + j] > qo) t32[j] = 0xff800000u;  // -inf: inadmissible (attention.hpp:298-300)
             TMEM_ST32(tS + c * 32, t32);
           }
           tmem_wait_st();
@@ -976,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!any) {  // the tile visits no block: no PV ran, O_w is not ours to read
         if (valid && a.status) {
           a.status[0] = 1;
-          atomicMin(&a.status[1], (int)(it.h * a.t + qb));
+          atomicMin(&a.status[1], (int)(it.h * a.t + qsel));
         }
         continue;
       }
@@ -985,7 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (valid && !(l > 0.0f) && a.status) {
         a.status[0] = 1;
-        atomicMin(&a.status[1], (int)(it.h * a.t + qb));
+        atomicMin(&a.status[1], (int)(it.h * a.t + qsel));
       }
       const int64_t orow = valid ? (a.out_rows ? (int64_t)a.out_rows[(int64_t)it.h * a.n + i] : i) : 0;
       if (a.lse && valid)  // natural-log LSE: l = sum 2^(s c - m), c = scale log2(e)
@@ -1062,7 +1101,7 @@ __global__ void visit_pair_kernel(KernelArgs a, int words, int32_t* __restrict__
     }
   }
   __syncwarp();
-  int32_t* out = vis + g * a.t;
+  int32_t* out = vis + g * a.t128;
   int total = 0;
   for (int w0 = 0; w0 < words; w0 += 32) {
     const int wi = w0 + lane;
@@ -1095,14 +1134,80 @@ __global__ void visit_pair_kernel(KernelArgs a, int words, int32_t* __restrict__
   if (lane == 0) nvis[g] = total;
 }
 
+// B = 64 (sub-blocked tiles): per item (head, pair of query tiles = query
+// blocks 4p .. 4p + 3) the ascending union of the 128-key tiles that hold any
+// selected block of the four query blocks, each with the eight blocks' classes
+// (kt | sc << 16, sub_class layout).  One warp per item, one bitmap per
+// (tile, query half, key half) in shared memory.
+__global__ void visit_quad_kernel(KernelArgs a, int words, int32_t* __restrict__ vis, int32_t* __restrict__ nvis) {
+  extern __shared__ uint32_t bm_smem[];
+  const int wip = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kVisitWarps + wip;
+  if (g >= (int64_t)a.hq * a.npairs) return;
+  uint32_t* bm = bm_smem + (size_t)wip * 8 * words;
+  for (int x = lane; x < 8 * words; x += 32) bm[x] = 0u;
+  __syncwarp();
+  const int h = (int)(g / a.npairs);
+  const int64_t p = g % a.npairs;
+  for (int q = 0; q < 4; ++q) {
+    const int64_t qb = 4 * p + q;
+    if (qb >= a.t) break;
+    const int cnt = a.kv_cnt[(int64_t)h * a.t + qb];
+    const int32_t* list = a.kv_idx + ((int64_t)h * a.t + qb) * a.t;
+    for (int e = lane; e < cnt; e += 32) {
+      const int kb = list[e], kt = kb >> 1, s = 2 * q + (kb & 1);  // s = 4 w + 2 a + b
+      atomicOr(&bm[s * words + (kt >> 5)], 1u << (kt & 31));
+    }
+  }
+  __syncwarp();
+  auto classes = [&](const uint32_t (&m)[8], int bit, int64_t kt) {
+    uint32_t sc = 0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if ((m[s] >> bit) & 1u) sc |= (uint32_t)block_class(a, h, 4 * p + (s >> 1), 2 * kt + (s & 1)) << (2 * s);
+    return sc;
+  };
+  int32_t* out = vis + g * a.t128;
+  int total = 0;
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int wi = w0 + lane;
+    uint32_t m[8], any = 0u;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      m[s] = wi < words ? bm[s * words + wi] : 0u;
+      any |= m[s];
+    }
+    uint32_t keep = 0u;
+    for (uint32_t u = any; u; u &= u - 1) {
+      const int bit = __ffs(u) - 1;
+      if (classes(m, bit, (int64_t)wi * 32 + bit)) keep |= 1u << bit;
+    }
+    const int cnt = __popc(keep);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = total + incl - cnt;
+    for (uint32_t u = keep; u; u &= u - 1) {
+      const int bit = __ffs(u) - 1;
+      const int64_t kt = (int64_t)wi * 32 + bit;
+      out[pos++] = (int32_t)((uint32_t)kt | (classes(m, bit, kt) << kSubShift));
+    }
+    total += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) nvis[g] = total;
+}
+
 // per-block [min, max] of an original-position map (AdmissibilityIndex::build)
 __global__ void block_minmax_kernel(const int32_t* __restrict__ orig, int heads, int64_t n, int64_t t,
-                                    int2* __restrict__ mm) {
+                                    int64_t block, int2* __restrict__ mm) {
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (g >= (int64_t)heads * t) return;
   const int64_t h = g / t, b = g % t;
-  const int64_t lo = b * kBM, hi = min64(n, lo + kBM);
+  const int64_t lo = b * block, hi = min64(n, lo + block);
   int mn = 0x7fffffff, mx = -1;
   for (int64_t p = lo + lane; p < hi; p += 32) {
     const int v = orig[h * n + p];
@@ -1186,7 +1291,9 @@ void* stream_scratch(cudaStream_t st, size_t bytes) {
 }  // namespace
 
 bool attention_sm100_supported(const AttnParams& p) {
-  if (p.dtype != PBS_DTYPE_BF16 || p.d != kD || p.block != kBM) return false;
+  if (p.dtype != PBS_DTYPE_BF16 || p.d != kD) return false;
+  // B = 128 tiles; B = 64 block-sparse lists as 2 x 2 blocks per tile
+  if (p.block != kBM && !(p.block == 64 && p.kv_idx)) return false;
   if ((uintptr_t)p.q % 16 || (uintptr_t)p.k % 16 || (uintptr_t)p.v % 16 || (uintptr_t)p.out % 16) return false;
   int dev = 0, major = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
@@ -1231,6 +1338,9 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   a.group = p.hq / p.kv_heads;
   a.n = p.n;
   a.t = t;
+  a.block = p.block;
+  a.sub = p.block == 64 ? 1 : 0;
+  a.t128 = ceil_div(p.n, (int64_t)kBM);
   a.scale_log2 = p.scale * 1.4426950408889634f;
   a.kv_idx = p.kv_idx;
   a.kv_cnt = p.kv_cnt;
@@ -1243,15 +1353,17 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
   a.causal = p.causal;
   a.dense = p.kv_idx == nullptr;
   if (a.dense && !p.causal) return fail(PBS_ERR_CONFIG, "E_CONFIG", "attention without a block list must be causal");
-  a.npairs = ceil_div(t, 2);
+  a.npairs = ceil_div(a.t128, 2);
   {
+    // items are pairs of 128-row tiles: 2 query blocks at B = 128, 4 at B = 64
+    const int64_t per = a.sub ? 4 : 2;
     const int64_t qb_end = p.qb_end > 0 ? min64(p.qb_end, t) : t;
-    if (p.qb_begin < 0 || p.qb_begin >= qb_end || (p.qb_begin & 1))
-      return fail(PBS_ERR_CONFIG, "E_CONFIG", "query-block range must be non-empty and start on an even block");
-    a.p_lo = p.qb_begin / 2;
-    a.p_hi = ceil_div(qb_end, 2);
-    if (qb_end != t && (qb_end & 1))
-      return fail(PBS_ERR_CONFIG, "E_CONFIG", "query-block range must end on an even block or at the last one");
+    if (p.qb_begin < 0 || p.qb_begin >= qb_end || (p.qb_begin % per))
+      return fail(PBS_ERR_CONFIG, "E_CONFIG", "query-block range must be non-empty and start on a whole tile pair");
+    a.p_lo = p.qb_begin / per;
+    a.p_hi = ceil_div(qb_end, per);
+    if (qb_end != t && (qb_end % per))
+      return fail(PBS_ERR_CONFIG, "E_CONFIG", "query-block range must end on a whole tile pair or at the last block");
   }
   a.items = (int64_t)p.hq * (a.p_hi - a.p_lo);
   // scratch: block min/max of the original positions + visit lists
@@ -1266,34 +1378,42 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
     int2* mm = static_cast<int2*>(sched_ws);
     const int64_t rows = (int64_t)p.hq * t;
     if (p.q_orig) {
-      block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.q_orig, p.hq, p.n, t, mm);
+      block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.q_orig, p.hq, p.n, t, p.block, mm);
       PBS_LAUNCH_CHECK("block_minmax_kernel");
       a.q_mm = mm;
     }
     if (p.k_orig) {
-      block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.k_orig, p.hq, p.n, t, mm + rows);
+      block_minmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(p.k_orig, p.hq, p.n, t, p.block, mm + rows);
       PBS_LAUNCH_CHECK("block_minmax_kernel");
       a.k_mm = mm + rows;
     }
   }
   if (!a.dense) {
     int32_t* vis = static_cast<int32_t*>(sched_ws) + (2 * (size_t)p.hq * t * sizeof(int2)) / sizeof(int32_t);
-    int32_t* nvis = vis + (size_t)p.hq * a.npairs * t;
-    const int words = (int)ceil_div(t, 32);
-    const size_t smem = (size_t)kVisitWarps * 2 * words * sizeof(uint32_t);
+    int32_t* nvis = vis + (size_t)p.hq * a.npairs * a.t128;
+    const int words = (int)ceil_div(a.t128, 32);
+    const size_t smem = (size_t)kVisitWarps * (a.sub ? 8 : 2) * words * sizeof(uint32_t);
     if (smem > 48 * 1024) {
       static DeviceOnce vis_once;
       if (int rc = once_per_device(vis_once, [] {
             PBS_CUDA_CHECK(cudaFuncSetAttribute(visit_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                200 * 1024));
+            PBS_CUDA_CHECK(cudaFuncSetAttribute(visit_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 200 * 1024));
             return (int)PBS_OK;
           }))
         return rc;
     }
     // every pair of every head (the items may be a query-block range of them)
-    visit_pair_kernel<<<(unsigned)ceil_div((int64_t)p.hq * a.npairs, kVisitWarps), kVisitWarps * 32, smem, st>>>(
-        a, words, vis, nvis);
-    PBS_LAUNCH_CHECK("visit_pair_kernel");
+    if (a.sub) {
+      visit_quad_kernel<<<(unsigned)ceil_div((int64_t)p.hq * a.npairs, kVisitWarps), kVisitWarps * 32, smem, st>>>(
+          a, words, vis, nvis);
+      PBS_LAUNCH_CHECK("visit_quad_kernel");
+    } else {
+      visit_pair_kernel<<<(unsigned)ceil_div((int64_t)p.hq * a.npairs, kVisitWarps), kVisitWarps * 32, smem, st>>>(
+          a, words, vis, nvis);
+      PBS_LAUNCH_CHECK("visit_pair_kernel");
+    }
     a.vis = vis;
     a.nvis = nvis;
   }

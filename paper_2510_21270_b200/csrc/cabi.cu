@@ -132,6 +132,8 @@ Layout plan(const pbs_shape* s, const pbs_pipeline_config* c) {
 
 int run_attention(const AttnParams& p, void* sched, cudaStream_t st) {
   if (attention_sm100_supported(p)) return launch_attention_sm100(p, sched, st);
+  if (getenv("PBS_REQUIRE_TC"))  // tests: the shape must take the tensor-core kernel
+    return fail(PBS_ERR_CONFIG, "E_CONFIG", "PBS_REQUIRE_TC: this attention call would take the SIMT kernel");
   return launch_attention_simt(p, st);
 }
 

@@ -33,23 +33,23 @@ namespace pbs_b200 {
 namespace {
 
 // ---- work model and shard plan -------------------------------------------------
-// Unit = (head h, pair p): query blocks 2p and 2p + 1 (the attention kernel's
-// item).  Weight = the causal key blocks its tiles visit, (2p + 1) + (2p + 2),
-// or 2p + 1 for a lone last tile: the PBS selection keeps a similar fraction
-// of every row, so causal work is the balance proxy.
+// Unit = (head h, pair p): the query blocks of one pair of 128-row tiles (the
+// attention kernel's item): blocks 2p, 2p + 1 at B = 128, 4p .. 4p + 3 at
+// B = 64 (two blocks per tile), 2p, 2p + 1 for other block sizes.  Weight = the
+// causal key blocks its query blocks visit, qb + 1 each: the PBS selection
+// keeps a similar fraction of every row, so causal work is the balance proxy.
 struct Units {
-  int64_t t, pairs, head_w;
+  int64_t t, per, pairs, head_w;
   explicit Units(int64_t n, int64_t b) {
     t = ceil_div(n, b);
-    pairs = ceil_div(t, 2);
+    per = b == 64 ? 4 : 2;
+    pairs = ceil_div(t, per);
     head_w = before(pairs);
   }
-  // work of pairs [0, p) of one head
+  // work of pairs [0, p) of one head: sum over query blocks qb < per p of (qb + 1)
   int64_t before(int64_t p) const {
-    const int64_t full = std::min<int64_t>(p, t / 2);  // pairs with two tiles
-    int64_t w = 2 * full * full + full;                 // sum_{v < full} 4v + 3
-    if (p > full) w += t;                                // the lone last tile (t odd): qb = t - 1 visits t blocks
-    return w;
+    const int64_t m = std::min<int64_t>(per * p, t);
+    return m * (m + 1) / 2;
   }
   // first unit whose preceding work (global, head-major) is >= target
   void boundary(int64_t target, int64_t hq, int64_t& h, int64_t& p) const {
@@ -93,13 +93,13 @@ int shard_plan(const pbs_shape* g, int64_t block, int32_t world, int32_t rank, p
   // [h0:p0, h1:p1) in head-major unit order -> heads [head_begin, head_end),
   // the first from block qb_begin, the last up to block qb_end
   s->head_begin = (int32_t)h0;
-  s->qb_begin = 2 * p0;
+  s->qb_begin = u.per * p0;
   if (p1 == 0) {
     s->head_end = (int32_t)h1;
     s->qb_end = u.t;
   } else {
     s->head_end = (int32_t)(h1 + 1);
-    s->qb_end = 2 * p1;
+    s->qb_end = u.per * p1;
   }
   if (h0 >= hq || (h0 == h1 && p0 == p1)) {  // no work for this rank
     s->head_begin = s->head_end = (int32_t)std::min<int64_t>(h0, hq);

@@ -42,9 +42,14 @@ def _use_model(name):
     return bench
 
 
-def _pair_work(t):
-    """Causal key blocks visited per (head, pair): tiles 2p and 2p + 1."""
-    return [(2 * p + 1) + (2 * p + 2 if 2 * p + 1 < t else 0) for p in range((t + 1) // 2)]
+def _per(b):
+    """Query blocks per unit: a pair of 128-row tiles (4 blocks at B = 64), else 2."""
+    return 4 if b == 64 else 2
+
+
+def _pair_work(t, per=2):
+    """Causal key blocks visited per (head, unit): query blocks per*p .. per*p + per - 1."""
+    return [sum(qb + 1 for qb in range(per * p, min(per * p + per, t))) for p in range(-(-t // per))]
 
 
 @pytest.mark.parametrize("hq,hkv,n,b", [(32, 8, 131072, 128), (28, 4, 262144, 128), (32, 8, 32768, 128),
@@ -53,7 +58,8 @@ def _pair_work(t):
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
 def test_shard_plan_covers_balances_and_is_contiguous(hq, hkv, n, b, world):
     t = -(-n // b)
-    w = _pair_work(t)
+    per = _per(b)
+    w = _pair_work(t, per)
     owner = {}
     rows = []
     loads = []
@@ -63,8 +69,8 @@ def test_shard_plan_covers_balances_and_is_contiguous(hq, hkv, n, b, world):
         for h in range(s["head_begin"], s["head_end"]):
             lo = s["qb_begin"] if h == s["head_begin"] else 0
             hi = s["qb_end"] if h == s["head_end"] - 1 else t
-            assert lo % 2 == 0 and (hi % 2 == 0 or hi == t) and lo < hi
-            for p in range(lo // 2, -(-hi // 2)):
+            assert lo % per == 0 and (hi % per == 0 or hi == t) and lo < hi
+            for p in range(lo // per, -(-hi // per)):
                 assert (h, p) not in owner
                 owner[(h, p)] = r
                 load += w[p]

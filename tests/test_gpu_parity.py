@@ -122,10 +122,14 @@ def test_block_scores_and_selection_bitexact(ops, oracle, n, d, b, s, tau):
     (2, 1, 1024, 128, 128, 256, 0.9),
     (4, 2, 1536 + 64, 128, 128, 256, 0.8),  # ragged final block
     (1, 1, 512, 64, 32, 128, 0.7),
+    (2, 1, 1024, 128, 64, 256, 0.9),  # B = 64 on the tensor cores (2 x 2 blocks per tile)
+    (4, 2, 2048 + 64 + 17, 128, 64, 128, 0.85),  # B = 64, ragged, lone last block of a tile pair
 ])
-def test_pipeline_matches_oracle(ops, oracle, strategy, hq, hkv, n, d, b, s, tau):
+def test_pipeline_matches_oracle(ops, oracle, monkeypatch, strategy, hq, hkv, n, d, b, s, tau):
     from oracle import make_config as ocfg
 
+    if d == 128:  # bf16, d = 128, B = 64 / 128: must run the tcgen05 kernel
+        monkeypatch.setenv("PBS_REQUIRE_TC", "1")
     rng = np.random.default_rng(11)
     tq, tk, tv, q, k, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0, block=b)
     if strategy == "none":
@@ -466,14 +470,16 @@ def _torch_block_sparse_ref(q, k, v, b, kv_idx, kv_cnt, q_orig, k_orig, out_rows
     return out
 
 
-@pytest.mark.parametrize("n", [4096 + 50, 6144])
-def test_block_sparse_many_items_per_slot(ops, n):
+@pytest.mark.parametrize("n,b", [(4096 + 50, 128), (6144, 128), (4096 + 50, 64), (3000, 64)])
+def test_block_sparse_many_items_per_slot(ops, monkeypatch, n, b):
     """Several (head, query block) items per tensor-core slot (32 heads x 33-48
     blocks over 148 x 2 slots): Q reloads, O hand-over between items, K/V ring
     wrap-around, ragged final blocks, permuted original positions and the fused
-    un-permute, against a dense torch restatement."""
+    un-permute, against a dense torch restatement.  B = 64: every 128 x 128 tile
+    carries four blocks selected (and classed) independently."""
+    monkeypatch.setenv("PBS_REQUIRE_TC", "1")
     torch.manual_seed(0)
-    hq, hkv, d, b, seg = 32, 8, 128, 128, 256
+    hq, hkv, d, seg = 32, 8, 128, 256
     t = -(-n // b)
     q = torch.randn(hq, n, d, device="cuda").to(torch.bfloat16)
     k = torch.randn(hkv, n, d, device="cuda").to(torch.bfloat16)
