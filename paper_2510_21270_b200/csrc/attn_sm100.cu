@@ -641,7 +641,9 @@ struct ItemStream {
   __device__ __forceinline__ int64_t next(Barriers* bar, int lane) {
     const int slot = (int)(n % kItemRing);
     mbar_wait(&bar->item_full[slot], (n / kItemRing) & 1);
-    const int32_t idx = *reinterpret_cast<volatile int32_t*>(&bar->item_ring[slot]);
+    // atomic access: the slot hand-over is ordered by the mbarriers, which
+    // compute-sanitizer's racecheck does not model for plain shared accesses
+    const int32_t idx = atomicOr(&bar->item_ring[slot], 0);
     __syncwarp();
     if (lane == 0) mbar_arrive(&bar->item_empty[slot]);
     ++n;
@@ -873,7 +875,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar->item_empty[slot], ((n / kItemRing) & 1) ^ 1);
         int32_t idx = atomicAdd(a.item_counter, 1);
         if ((int64_t)idx >= a.items) idx = -1;
-        *reinterpret_cast<volatile int32_t*>(&bar->item_ring[slot]) = idx;
+        atomicExch(&bar->item_ring[slot], idx);
         mbar_arrive(&bar->item_full[slot]);  // release: the consumers' wait orders the read after the write
         if (idx < 0) break;
       }
