@@ -6,7 +6,8 @@ Configs (BASELINE.json configs[1..3]), inputs from
   * C2  Llama-3.1-8B shapes (32 q / 8 kv heads, d = 128) at N = 32768;
   * C3  the same at N = 131072 (the headline);
   * C4  Qwen2.5-7B shapes (28 q / 4 kv heads) at N = 262144.
-B = 128, S = 256, tau = 0.9, key_permute (PAPER:266).
+B = 128, S = 256, tau = 0.9, key_permute; C2 also at B = 64 (the
+block-size variant, two selection blocks per tensor-core tile side).
 
 For EVERY query head, on the bf16-upcast inputs (exact in f32):
   * importance scores (permutation.hpp:143-178) bit for bit;
@@ -35,10 +36,10 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-B, S, TAU = 128, 256, 0.9
+S, TAU = 256, 0.9
 
-CONFIGS = {"c2_llama_32k": ("llama", 32768), "c3_llama_128k": ("llama", 131072),
-           "c4_qwen_256k": ("qwen", 262144)}
+CONFIGS = {"c2_llama_32k": ("llama", 32768, 128), "c3_llama_128k": ("llama", 131072, 128),
+           "c4_qwen_256k": ("qwen", 262144, 128), "c2_llama_32k_b64": ("llama", 32768, 64)}
 
 
 def _audit(sorted_scores):
@@ -62,7 +63,7 @@ def fullsize(request):
     import bench
     from paper_2510_21270_b200 import ops
 
-    model, n = CONFIGS[request.param]
+    model, n, B = CONFIGS[request.param]
     hq, hkv, _, prefix = bench.MODELS[model]
     bench.HQ, bench.HKV, bench.PREFIX = hq, hkv, prefix
     q, k, v = bench.make_inputs(torch, n, 0, hq, list(range(hkv)), "cuda")
@@ -76,13 +77,13 @@ def fullsize(request):
     kh = k.float().cpu().numpy()
     del q, k, v, res, scores, bscores
     torch.cuda.empty_cache()
-    yield request.param, hq, hkv, n, qh, kh, dev
+    yield request.param, hq, hkv, n, B, qh, kh, dev
 
 
 def test_fullsize_pi_and_mask_equal_reference(fullsize):
     from oracle import Oracle
 
-    name, hq, hkv, n, q, k, dev = fullsize
+    name, hq, hkv, n, B, q, k, dev = fullsize
     ref = Oracle("ref")
     g = hq // hkv
     t = n // B
