@@ -1,3 +1,2 @@
 cd "${GRAFT_REPO_ROOT:-.}"
-export PBS_AUDIT_DIR=gpurun_out/audit
-timeout 900 python -m pytest tests/test_fullsize_parity.py -x -q -m gpu --timeout 600 -k "b64 or c2" -s 2>&1 | grep -E "^\{|passed|failed|Error" | head
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu --timeout 120 -k "shards_reassemble" 2>&1 | tail -3

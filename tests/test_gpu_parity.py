@@ -686,22 +686,24 @@ def test_host_entry_concurrent_callers(ops):
 
 
 # ---- head-parallel shards on the device -------------------
-@pytest.mark.parametrize("hq,hkv,n,world", [(8, 2, 2048, 2), (8, 2, 2048 + 64, 4), (14, 2, 4096, 4),
-                                            (7, 1, 2048, 2), (7, 1, 4096 + 128, 8), (3, 3, 640, 8)])
-def test_shards_reassemble_pbs_attention(ops, hq, hkv, n, world):
+@pytest.mark.parametrize("hq,hkv,n,world,b", [(8, 2, 2048, 2, 128), (8, 2, 2048 + 64, 4, 128),
+                                              (14, 2, 4096, 4, 128), (7, 1, 2048, 2, 128),
+                                              (7, 1, 4096 + 128, 8, 128), (3, 3, 640, 8, 128),
+                                              (7, 1, 4096 + 64 + 9, 4, 64), (8, 2, 3072, 8, 64)])
+def test_shards_reassemble_pbs_attention(ops, hq, hkv, n, world, b):
     """Every rank's pbs_attention_shard run one after another on this GPU into
     one buffer equals the single pbs_attention call bit for bit -- including
     ranks whose share cuts inside a head (Qwen-like groups of 7) and ranks
     that need only some KV heads; the reports sum to the single call's."""
     rng = np.random.default_rng(hq * n + world)
     tq, tk, tv, *_ = bf16_inputs(rng, hq, hkv, n, 128, kind="vertical_lines")
-    cfg = ops.make_config()
+    cfg = ops.make_config(block_size=b)
     want = ops.pbs_attention(tq, tk, tv, cfg)
     out = torch.zeros_like(tq)
     sel = 0
     cuts = 0
     for r in range(world):
-        s = ops.shard_plan(hq, hkv, n, 128, 128, world, r)
+        s = ops.shard_plan(hq, hkv, n, 128, b, world, r)
         if s["out_rows"] == 0:
             continue
         cuts += s["qb_begin"] != 0
