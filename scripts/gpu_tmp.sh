@@ -1,2 +1,3 @@
 cd "${GRAFT_REPO_ROOT:-.}"
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu --timeout 120 -k "shards_reassemble" 2>&1 | tail -3
+python scripts/pcie_probe.py 2>&1 | tail -2
+python scripts/e2e_trace.py 32768 2>&1 | tail -40
