@@ -1395,6 +1395,12 @@ int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st)
     int32_t* nvis = vis + (size_t)p.hq * a.npairs * a.t128;
     const int words = (int)ceil_div(a.t128, 32);
     const size_t smem = (size_t)kVisitWarps * (a.sub ? 8 : 2) * words * sizeof(uint32_t);
+    // the pre-pass keeps one bitmap row per key tile in shared memory, and a
+    // sub-blocked entry packs the tile index into 16 bits
+    if (smem > 200 * 1024 || (a.sub && a.t128 > 0xffff))
+      return fail(PBS_ERR_CONFIG, "E_CONFIG",
+                  "block-sparse attention on the tensor cores: sequence too long for the visit lists (N = " +
+                      std::to_string(p.n) + ", B = " + std::to_string(p.block) + ")");
     if (smem > 48 * 1024) {
       static DeviceOnce vis_once;
       if (int rc = once_per_device(vis_once, [] {
