@@ -1,3 +1,2 @@
 cd "${GRAFT_REPO_ROOT:-.}"
-python scripts/pcie_probe.py 2>&1 | tail -2
-python scripts/e2e_trace.py 32768 2>&1 | tail -40
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu --timeout 120 -k "tiny_and_ragged or selection_extremes" 2>&1 | tail -4

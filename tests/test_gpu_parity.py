@@ -152,15 +152,18 @@ def test_pipeline_matches_oracle(ops, oracle, monkeypatch, strategy, hq, hkv, n,
 
 
 @pytest.mark.parametrize("strategy", ["key_permute", "none", "query_permute", "both"])
-@pytest.mark.parametrize("n", [1, 100, 128, 129, 383])
-def test_pipeline_tiny_and_ragged_lengths(ops, oracle, strategy, n):
+@pytest.mark.parametrize("n,b", [(1, 128), (100, 128), (128, 128), (129, 128), (383, 128),
+                                 (1, 64), (63, 64), (65, 64), (129, 64), (300, 64)])
+def test_pipeline_tiny_and_ragged_lengths(ops, oracle, monkeypatch, strategy, n, b):
     """Sequence lengths at and around one block on the tcgen05 path (d = 128,
-    B = 128, bf16): a single key, a partial only block, exactly one block, one
-    key past it, a segment plus a ragged block."""
+    bf16, B = 128 and 64): a single key, a partial only block, exactly one
+    block, one key past it, a segment plus a ragged block; at B = 64 also a
+    lone query block in its tile pair."""
     from oracle import make_config as ocfg
 
+    monkeypatch.setenv("PBS_REQUIRE_TC", "1")
     rng = np.random.default_rng(n)
-    hq, hkv, d, b, s, tau = 2, 1, 128, 128, 256, 0.9
+    hq, hkv, d, s, tau = 2, 1, 128, 256, 0.9
     tq, tk, tv, q, k, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0)
     if strategy == "none":
         s = 0
@@ -305,13 +308,16 @@ def test_pipeline_top_k_matches_oracle(ops, oracle, k):
 
 
 @pytest.mark.parametrize("tau,top_k", [(0.0, 0), (0.9, 1000), (0.9, 1)])
-def test_selection_extremes_match_oracle(ops, oracle, tau, top_k):
+@pytest.mark.parametrize("b", [128, 64])
+def test_selection_extremes_match_oracle(ops, oracle, monkeypatch, tau, top_k, b):
     """tau = 0 (forced blocks only), top_k beyond every row's admissible count
-    (everything admissible) and top_k = 1, through the whole pipeline."""
+    (everything admissible) and top_k = 1, through the whole pipeline, on the
+    tensor-core path at B = 128 and B = 64."""
     from oracle import make_config as ocfg
 
+    monkeypatch.setenv("PBS_REQUIRE_TC", "1")
     rng = np.random.default_rng(13)
-    hq, hkv, n, d, b, s = 2, 1, 2048 + 77, 128, 128, 256
+    hq, hkv, n, d, s = 2, 1, 2048 + 77, 128, 256
     tq, tk, tv, q, kk, v = bf16_inputs(rng, hq, hkv, n, d, kind="vertical_lines", strength=20.0, block=b)
     res = ops.pbs_attention(tq, tk, tv, ops.make_config(block_size=b, segment_size=s, tau=tau, top_k=top_k))
     out, pi, mask = res.output.float().cpu().numpy(), res.pi.cpu().numpy(), res.mask.cpu().numpy()
