@@ -421,12 +421,15 @@ def test_degenerate_row_raises(ops):
 # hkv = 1: one group; key_permute with hkv > 1: the estimate of every head runs
 # up front (K streamed per KV head) and the groups take pi; query_permute with
 # hkv > 1: per-group pipelines on two slots
-@pytest.mark.parametrize("hq,hkv,n,strategy", [(2, 1, 1024, "key_permute"), (8, 4, 2048 + 128, "key_permute"),
-                                               (6, 3, 1024, "query_permute")])
-def test_host_entry_matches_device_entry(ops, hq, hkv, n, strategy):
+@pytest.mark.parametrize("hq,hkv,n,strategy,b", [(2, 1, 1024, "key_permute", 128),
+                                                 (8, 4, 2048 + 128, "key_permute", 128),
+                                                 (6, 3, 1024, "query_permute", 128),
+                                                 (8, 4, 2048 + 64 + 5, "key_permute", 64),
+                                                 (6, 2, 1536, "both", 64)])
+def test_host_entry_matches_device_entry(ops, hq, hkv, n, strategy, b):
     rng = np.random.default_rng(9)
     tq, tk, tv, *_ = bf16_inputs(rng, hq, hkv, n, 128, kind="vertical_lines")
-    cfg = ops.make_config(strategy=strategy)
+    cfg = ops.make_config(strategy=strategy, block_size=b)
     dev = ops.pbs_attention(tq, tk, tv, cfg)
     host = ops.pbs_attention_host(tq.cpu(), tk.cpu(), tv.cpu(), cfg, return_perms=True)
     assert torch.equal(host.output, dev.output.cpu())
