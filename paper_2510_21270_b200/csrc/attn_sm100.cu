@@ -1327,6 +1327,21 @@ int make_f32_map_3d(void* map, const float* base, int64_t d0, int64_t d1, int64_
   return PBS_OK;
 }
 
+int make_bf16_sw128_map_3d(void* map, const void* base, int64_t d0, int64_t d1, int64_t d2, int64_t row_elems,
+                           int box0, int box1) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(PBS_ERR_CUDA, "E_CUDA", "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  const cuuint64_t strides[2] = {(cuuint64_t)row_elems * 2, (cuuint64_t)d1 * row_elems * 2};
+  const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PBS_ERR_CUDA, "E_CUDA", "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return PBS_OK;
+}
+
 int launch_attention_sm100(const AttnParams& p, void* sched_ws, cudaStream_t st) {
   const int64_t t = ceil_div(p.n, p.block);
   if (t == 0) return PBS_OK;

@@ -30,6 +30,7 @@
 #include "expf_glibc.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
+#include "tc.cuh"
 
 namespace pbs_b200 {
 
@@ -511,9 +512,6 @@ __global__ void query_group_finalize_kernel(const unsigned long long* __restrict
 //     (sequential c, rounded products, IEEE division), argmax with the first
 //     index on ties; a row with more than kScrCand candidates scans every
 //     centroid exactly.
-constexpr int kScrMT = 2;                  // 16-row MMA tiles per warp (B fragments reused across them)
-constexpr int kScrRows = 8 * 16 * kScrMT;  // queries per CTA
-constexpr int kScrChunk = 64;              // centroids per shared-memory chunk
 constexpr int kScrPad = 136;               // bf16 per padded centroid row (272 B: conflict-free fragment loads)
 constexpr int kScrCand = 16;               // candidates kept per listed row
 constexpr float kScrDelta = 1e-4f;
@@ -534,14 +532,6 @@ __global__ void centroid_split_kernel(const float* __restrict__ cent, const floa
     rinv[r] = v > 0.0f ? 1.0f / v : 0.0f;
     pen[r] = v > 0.0f ? 0.0f : -INFINITY;
   }
-}
-
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-      "{%0, %1, %2, %3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 struct Best2 {
@@ -574,171 +564,261 @@ struct ScreenLists {
   int32_t* cand_n; // [k_heads][k_group * n]
 };
 
-// kListed = false: rows blockIdx.x * kScrRows.. of head blockIdx.y (decide or list);
-// kListed = true: the rows listed for KV head blockIdx.y (emit candidates).
+// K3 screen on the 5th-generation tensor cores.  Persistent CTAs (one per SM)
+// walk tiles of 128 query rows -- rows r0.. of one head (kListed = false:
+// decide or list), or 128 of the rows listed for one KV head (kListed = true:
+// emit candidates) -- and score each tile against every centroid of its KV
+// head in chunks of 128 (N):
+//   S = Q C_hi^T + Q C_lo^T  (16 tcgen05.mma, K = 128 + 128, f32 in TMEM; two
+//   accumulators, so a chunk's MMAs run while the epilogue reads the previous)
+// giving the scaled scores cos * |q| = S * rinv_j + pen_j.  Warp 0 loads (Q
+// tiles double-buffered: one TMA tile, or the listed rows gathered by cp.async
+// into the same SW128 layout; centroid chunks hi + lo by TMA, two stages),
+// warp 1 owns TMEM and issues the MMAs, warps 2-17 read the accumulator: four
+// warps per TMEM lane quadrant, each taking 32 of a chunk's 128 columns, with
+// four independent (best, second best) pairs per thread (first index on ties)
+// merged per row at the end of the tile, or the row's candidates.  Every output
+// element depends only on its own row and column, so both passes compute
+// bit-identical scores for a listed row.
+constexpr int kQsChunk = 128;  // centroids per chunk (MMA N)
+constexpr int kQsEpiWarps = 16;
+constexpr int kQsThreads = 64 + 32 * kQsEpiWarps;
+struct QsSmem {
+  static constexpr int q = 0;                          // [2][128 rows x 128 bf16] (two SW128 panels each)
+  static constexpr int c = 2 * 32768;                  // [stage 0..1][hi, lo] x 32 KB
+  static constexpr int ri = c + 2 * 2 * 32768;         // [2][128] f32: rinv, pen of the chunk in flight
+  static constexpr int xch = ri + 2 * 2 * kQsChunk * 4;  // [128 rows][4] Best2 partials
+  static constexpr int bars = xch + 128 * 4 * 12;
+  static constexpr int total = bars + 256 + 1024;      // + alignment slack
+};
+
+// tile index -> (KV head or head, first row); listed: tiles of each KV head's list in turn
 template <bool kListed>
-__global__ void __launch_bounds__(256) query_group_screen_kernel(
-    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ chi, const __nv_bfloat16* __restrict__ clo,
-    const float* __restrict__ rinv, const float* __restrict__ pen, const float* __restrict__ qn, int k_group,
-    int64_t n, int64_t tc, uint32_t* __restrict__ groups, ScreenLists L) {
-  extern __shared__ __align__(16) unsigned char scr_smem[];
-  // [2 bufs][2 (hi, lo)][kScrChunk][kScrPad] bf16, then [2 bufs][2 (rinv, pen)][kScrChunk] f32
-  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(scr_smem);
-  float* sf = reinterpret_cast<float*>(scr_smem + (size_t)2 * 2 * kScrChunk * kScrPad * 2);
+__device__ __forceinline__ bool qs_tile(int64_t t, int heads, int64_t n, const int32_t* count, int& h, int64_t& r0) {
+  if (!kListed) {
+    const int64_t per = (n + 127) / 128;
+    h = (int)(t / per);
+    r0 = (t % per) * 128;
+    return h < heads;
+  }
+  for (h = 0; h < heads; ++h) {
+    const int64_t per = ((int64_t)count[h] + 127) / 128;
+    if (t < per) {
+      r0 = t * 128;
+      return true;
+    }
+    t -= per;
+  }
+  return false;
+}
+
+template <bool kListed>
+__global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
+    const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_chi,
+    const __grid_constant__ CUtensorMap tm_clo, const __nv_bfloat16* __restrict__ q, const float* __restrict__ rinv,
+    const float* __restrict__ pen, const float* __restrict__ qn, int heads, int k_group, int64_t n, int64_t tc,
+    uint32_t* __restrict__ groups, ScreenLists L) {
+  extern __shared__ __align__(1024) unsigned char qs_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)qs_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + QsSmem::bars);
+  uint64_t* q_full = bar;        // [2]
+  uint64_t* q_empty = bar + 2;   // [2]
+  uint64_t* c_full = bar + 4;    // [2] centroid stage (and its rinv / pen) loaded
+  uint64_t* c_empty = bar + 6;   // [2] its MMAs complete (and its scales read)
+  uint64_t* s_full = bar + 8;    // [2] accumulator b holds a chunk's scores
+  uint64_t* s_free = bar + 10;   // [2] the epilogue read accumulator b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  float* sri = reinterpret_cast<float*>(sm + QsSmem::ri);
+  Best2* xch = reinterpret_cast<Best2*>(sm + QsSmem::xch);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int hk = kListed ? (int)blockIdx.y : (int)blockIdx.y / k_group;
-  const int64_t list_base = (int64_t)hk * k_group * n;
-  const int64_t nrows = kListed ? (int64_t)L.count[hk] : n;
-  if ((int64_t)blockIdx.x * kScrRows >= nrows) return;
-  const int64_t r0 = (int64_t)blockIdx.x * kScrRows + warp * 16 * kScrMT;
-  auto row_of = [&](int64_t r) -> int64_t {  // global row (h * n + i) of local row r; past the end: the last row
-    r = min64(r, nrows - 1);
-    return kListed ? (int64_t)L.rows[list_base + r] : (int64_t)blockIdx.y * n + r;
-  };
-  uint32_t af[kScrMT][8][4];
-#pragma unroll
-  for (int mt = 0; mt < kScrMT; ++mt) {
-    const uint32_t* qa = reinterpret_cast<const uint32_t*>(q + row_of(r0 + mt * 16 + g) * 128);
-    const uint32_t* qb = reinterpret_cast<const uint32_t*>(q + row_of(r0 + mt * 16 + g + 8) * 128);
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      af[mt][ks][0] = __ldg(qa + ks * 8 + t4);
-      af[mt][ks][1] = __ldg(qb + ks * 8 + t4);
-      af[mt][ks][2] = __ldg(qa + ks * 8 + 4 + t4);
-      af[mt][ks][3] = __ldg(qb + ks * 8 + 4 + t4);
+  const int nchunks = (int)((tc + kQsChunk - 1) / kQsChunk);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&q_full[b], 1);
+      ptx::mbar_init(&q_empty[b], 1);
+      ptx::mbar_init(&c_full[b], 2);  // the TMA (expect_tx) + the scales (lanes' writes, one arrival)
+      ptx::mbar_init(&c_empty[b], 1 + kQsEpiWarps);  // MMA commit + every epilogue warp past the scales
+      ptx::mbar_init(&s_full[b], 1);
+      ptx::mbar_init(&s_free[b], kQsEpiWarps);
     }
+    ptx::fence_mbar_init();
   }
-  // listed mode: the candidate threshold of each of this thread's rows
-  float thr[kScrMT][2];
-  if (kListed) {
-#pragma unroll
-    for (int mt = 0; mt < kScrMT; ++mt)
-#pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        const int64_t r = min64(r0 + mt * 16 + g + 8 * hr, nrows - 1);
-        thr[mt][hr] = L.best[list_base + r] - 2.0f * kScrDelta * qn[L.rows[list_base + r]];
-      }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(ptx::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  const __nv_bfloat16* ghi = chi + (int64_t)hk * tc * kScrPad;
-  const __nv_bfloat16* glo = clo + (int64_t)hk * tc * kScrPad;
-  const int nchunks = (int)((tc + kScrChunk - 1) / kScrChunk);
-  constexpr int kChunkElems = kScrChunk * kScrPad;  // per part
-  auto load_chunk = [&](int c, int buf) {
-    const int64_t j0 = (int64_t)c * kScrChunk;
-    const int rows = (int)min64(kScrChunk, tc - j0);
-    for (int part = 0; part < 2; ++part) {
-      const uint4* src = reinterpret_cast<const uint4*>((part ? glo : ghi) + j0 * kScrPad);
-      uint4* dst = reinterpret_cast<uint4*>(sb + (buf * 2 + part) * kChunkElems);
-      const int vecs = rows * kScrPad / 8;
-      for (int x = threadIdx.x; x < kChunkElems / 8; x += blockDim.x) {
-        const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(dst + x);
-        if (x < vecs) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + x) : "memory");
-        } else {
-          dst[x] = make_uint4(0u, 0u, 0u, 0u);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int k_heads = heads / (kListed ? 1 : k_group);
+  (void)k_heads;
+  if (warp == 0) {
+    // ---- loads: per tile Q, then the centroid chunks
+    uint32_t it = 0, cit = 0;
+    int h;
+    int64_t r0;
+    for (int64_t t = blockIdx.x; qs_tile<kListed>(t, heads, n, L.count, h, r0); t += gridDim.x, ++it) {
+      const int hk = kListed ? h : h / k_group;
+      const int qb = it & 1;
+      ptx::mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
+      unsigned char* qd = sm + QsSmem::q + qb * 32768;
+      if (!kListed) {
+        if (lane == 0) {
+          ptx::mbar_expect_tx(&q_full[qb], 32768);
+          for (int p = 0; p < 2; ++p) tc::tma_load_3d(qd + p * 16384, &tm_q, &q_full[qb], p * 64, (int)r0, h);
         }
-      }
-    }
-    // column scales (rinv, pen): padding columns get pen = -inf so they never win
-    for (int x = threadIdx.x; x < 2 * kScrChunk; x += blockDim.x) {
-      const int part = x / kScrChunk, col = x % kScrChunk;
-      const int64_t j = j0 + col;
-      sf[(buf * 2 + part) * kScrChunk + col] =
-          j < tc ? __ldg((part ? pen : rinv) + hk * tc + j) : (part ? -INFINITY : 0.0f);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  Best2 bs[kScrMT][2];
-#pragma unroll
-  for (int mt = 0; mt < kScrMT; ++mt) bs[mt][0] = bs[mt][1] = Best2{-INFINITY, -INFINITY, 0};
-  auto take = [&](int mt, int hr, float v, int j) {
-    if (!kListed) {
-      best2_push(bs[mt][hr], v, j);
-    } else if (v >= thr[mt][hr]) {
-      const int64_t r = r0 + mt * 16 + g + 8 * hr;
-      if (r < nrows) {
-        const int slot = atomicAdd(&L.cand_n[list_base + r], 1);
-        if (slot < kScrCand) L.cand[(list_base + r) * kScrCand + slot] = j;
-      }
-    }
-  };
-  load_chunk(0, 0);
-  for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nchunks) {
-      load_chunk(c + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t* bh = reinterpret_cast<const uint32_t*>(sb + (buf * 2 + 0) * kChunkElems);
-    const uint32_t* bl = reinterpret_cast<const uint32_t*>(sb + (buf * 2 + 1) * kChunkElems);
-    const float* sri = sf + (buf * 2 + 0) * kScrChunk;
-    const float* spe = sf + (buf * 2 + 1) * kScrChunk;
-    const int j0 = c * kScrChunk;
-#pragma unroll 2
-    for (int nt = 0; nt < kScrChunk / 8; ++nt) {
-      float acc[kScrMT][4];
-#pragma unroll
-      for (int mt = 0; mt < kScrMT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.0f;
-      const int rowb = (nt * 8 + g) * (kScrPad / 2);  // 32-bit words
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const uint32_t h0 = bh[rowb + ks * 8 + t4], h1 = bh[rowb + ks * 8 + 4 + t4];
-        const uint32_t l0 = bl[rowb + ks * 8 + t4], l1 = bl[rowb + ks * 8 + 4 + t4];
-#pragma unroll
-        for (int mt = 0; mt < kScrMT; ++mt) {
-          mma_bf16_16816(acc[mt], af[mt][ks], h0, h1);
-          mma_bf16_16816(acc[mt], af[mt][ks], l0, l1);
-        }
-      }
-      const int col = nt * 8 + 2 * t4;
-      const float2 ri = *reinterpret_cast<const float2*>(sri + col);
-      const float2 pe = *reinterpret_cast<const float2*>(spe + col);
-#pragma unroll
-      for (int mt = 0; mt < kScrMT; ++mt) {
-        take(mt, 0, fmaf(acc[mt][0], ri.x, pe.x), j0 + col);
-        take(mt, 0, fmaf(acc[mt][1], ri.y, pe.y), j0 + col + 1);
-        take(mt, 1, fmaf(acc[mt][2], ri.x, pe.x), j0 + col);
-        take(mt, 1, fmaf(acc[mt][3], ri.y, pe.y), j0 + col + 1);
-      }
-    }
-    __syncthreads();
-  }
-  if (kListed) return;
-  // the quad's lanes hold disjoint centroid columns of the same rows
-#pragma unroll
-  for (int mt = 0; mt < kScrMT; ++mt)
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr)
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        Best2 x{__shfl_xor_sync(0xffffffffu, bs[mt][hr].m, o), __shfl_xor_sync(0xffffffffu, bs[mt][hr].s2, o),
-                __shfl_xor_sync(0xffffffffu, bs[mt][hr].j, o)};
-        bs[mt][hr] = best2_merge(bs[mt][hr], x);
-      }
-  if (t4 < 2) {
-#pragma unroll
-    for (int mt = 0; mt < kScrMT; ++mt) {
-      const Best2 b = t4 ? bs[mt][1] : bs[mt][0];
-      const int64_t r = r0 + mt * 16 + g + 8 * t4;
-      if (r >= n) continue;
-      const int64_t gi = (int64_t)blockIdx.y * n + r;
-      const float qv = qn[gi];
-      // scaled scores are cos * |q|; the screen decides only with a clear 2 delta margin
-      const float dq = kScrDelta * qv;
-      if (!(qv > 0.0f)) {
-        groups[gi] = (uint32_t)tc;  // no positive-norm match (permutation.hpp:246-258)
-      } else if (b.m > -INFINITY && b.s2 < b.m - 2.0f * dq && b.m > -qv + dq) {
-        groups[gi] = (uint32_t)b.j;
       } else {
-        const int slot = atomicAdd(&L.count[hk], 1);
-        L.rows[list_base + slot] = (int32_t)gi;
-        L.best[list_base + slot] = b.m;
+        // the listed rows (global row h * n + i) gathered into the SW128 K-major
+        // layout the TMA would write: 16-byte chunk cc of row rr at panel cc / 8,
+        // rr * 128 + ((cc % 8) ^ (rr % 8)) * 16; half a warp per 256-byte row
+        const int64_t nrows = L.count[h];
+        const int64_t lb = (int64_t)h * k_group * n;
+        int src[4];
+#pragma unroll
+        for (int jr = 0; jr < 4; ++jr) src[jr] = L.rows[lb + min64(r0 + 32 * jr + lane, nrows - 1)];
+        const int hb = lane >> 4, cc = lane & 15, c8 = cc & 7;
+        const uint32_t base = ptx::smem_u32(qd) + (uint32_t)(cc >> 3) * 16384u;
+#pragma unroll
+        for (int jr = 0; jr < 4; ++jr)
+#pragma unroll 4
+          for (int i = 0; i < 16; ++i) {
+            const int rr = 32 * jr + 2 * i + hb;
+            const int gi = __shfl_sync(0xffffffffu, src[jr], (2 * i + hb) & 31);
+            const uint32_t dst = base + (uint32_t)rr * 128u + ((uint32_t)(c8 ^ (rr & 7)) << 4);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(q + (int64_t)gi * 128 + cc * 8)
+                         : "memory");
+          }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the MMA's operand reads
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&q_full[qb]);
+      }
+      for (int c = 0; c < nchunks; ++c, ++cit) {
+        const int st = cit & 1;
+        ptx::mbar_wait(&c_empty[st], ((cit >> 1) & 1) ^ 1);
+        if (lane == 0) {
+          ptx::mbar_expect_tx(&c_full[st], 65536);  // centroids past tc zero-filled
+          unsigned char* dst = sm + QsSmem::c + st * 65536;
+          for (int p = 0; p < 2; ++p) {
+            tc::tma_load_3d(dst + p * 16384, &tm_chi, &c_full[st], p * 64, c * kQsChunk, hk);
+            tc::tma_load_3d(dst + 32768 + p * 16384, &tm_clo, &c_full[st], p * 64, c * kQsChunk, hk);
+          }
+        }
+        // the chunk's column scales (padding columns: pen -inf, never a winner)
+        for (int x = lane; x < kQsChunk; x += 32) {
+          const int64_t j = (int64_t)c * kQsChunk + x;
+          sri[st * 2 * kQsChunk + x] = j < tc ? __ldg(rinv + (int64_t)hk * tc + j) : 0.0f;
+          sri[st * 2 * kQsChunk + kQsChunk + x] = j < tc ? __ldg(pen + (int64_t)hk * tc + j) : -INFINITY;
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&c_full[st]);
       }
     }
+  } else if (warp == 1) {
+    // ---- MMA issuer
+    const uint32_t idesc = tc::idesc_bf16(kQsChunk);
+    uint32_t it = 0, cit = 0;
+    int h;
+    int64_t r0;
+    for (int64_t t = blockIdx.x; qs_tile<kListed>(t, heads, n, L.count, h, r0); t += gridDim.x, ++it) {
+      const int qb = it & 1;
+      ptx::mbar_wait(&q_full[qb], (it >> 1) & 1);
+      const uint64_t qdesc = tc::sdesc_sw128(ptx::smem_u32(sm + QsSmem::q + qb * 32768));
+      for (int c = 0; c < nchunks; ++c, ++cit) {
+        const int st = cit & 1, b = cit & 1;
+        ptx::mbar_wait(&c_full[st], (cit >> 1) & 1);
+        ptx::mbar_wait(&s_free[b], ((cit >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t cb = ptx::smem_u32(sm + QsSmem::c + st * 65536);
+        tc::mma_k128(tmem + b * kQsChunk, qdesc, tc::sdesc_sw128(cb), idesc, false);        // Q C_hi^T
+        tc::mma_k128(tmem + b * kQsChunk, qdesc, tc::sdesc_sw128(cb + 32768), idesc, true);  // + Q C_lo^T
+        tc::commit(&c_empty[st]);
+        tc::commit(&s_full[b]);
+      }
+      tc::commit(&q_empty[qb]);  // every MMA reading this Q tile issued
+    }
+  } else {
+    // ---- epilogue: warp e reads TMEM lane quadrant e % 4 (rows 32 (e % 4)..)
+    // and columns 32 (e / 4).. of each chunk
+    const int e = warp - 2, quad = warp & 3, cq = e >> 2;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    uint32_t cit = 0;
+    int h;
+    int64_t r0;
+    for (int64_t t = blockIdx.x; qs_tile<kListed>(t, heads, n, L.count, h, r0); t += gridDim.x) {
+      const int hk = kListed ? h : h / k_group;
+      const int64_t lb = (int64_t)hk * k_group * n;
+      const int64_t nrows = kListed ? (int64_t)L.count[h] : n;
+      const int64_t r = r0 + row;
+      const bool valid = r < nrows;
+      const int64_t rc = min64(r, nrows - 1);
+      const int64_t gi = kListed ? (int64_t)L.rows[lb + rc] : (int64_t)h * n + rc;
+      float thr = 0.0f;
+      if (kListed) thr = L.best[lb + rc] - 2.0f * kScrDelta * qn[gi];
+      // four independent running (best, second) pairs over j % 4 (a dependent
+      // compare chain per element would serialise the epilogue), merged with the
+      // first index on ties -- the same pair a j-ascending scan produces
+      Best2 bp[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bp[u] = Best2{-INFINITY, -INFINITY, 0};
+      for (int c = 0; c < nchunks; ++c, ++cit) {
+        const int st = cit & 1, b = cit & 1;
+        ptx::mbar_wait(&s_full[b], (cit >> 1) & 1);
+        ptx::mbar_wait(&c_full[st], (cit >> 1) & 1);  // the scales (already complete: the MMAs waited on it)
+        tc::fence_after();
+        uint32_t v[32];
+        PBS_TC_LD32(tmem + lane_off + (uint32_t)(b * kQsChunk + cq * 32), v);
+        tc::wait_ld();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_free[b]);
+        const float* scl = sri + st * 2 * kQsChunk + cq * 32;
+        const int j0 = c * kQsChunk + cq * 32;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const float x = fmaf(__uint_as_float(v[jj]), scl[jj], scl[kQsChunk + jj]);  // padding: pen -inf
+          if (!kListed) {
+            best2_push(bp[jj & 3], x, j0 + jj);
+          } else if (x >= thr && j0 + jj < tc) {
+            const int slot = atomicAdd(&L.cand_n[lb + rc], valid ? 1 : 0);
+            if (valid && slot < kScrCand) L.cand[(lb + rc) * kScrCand + slot] = j0 + jj;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&c_empty[st]);  // the scales of this stage read
+      }
+      if (kListed) continue;
+      // the row's four column groups (warps e % 4 == quad) merged in shared memory
+      xch[row * 4 + cq] = best2_merge(best2_merge(bp[0], bp[1]), best2_merge(bp[2], bp[3]));
+      ptx::named_bar_sync(1, 32 * kQsEpiWarps);
+      if (cq == 0 && valid) {
+        Best2 best = xch[row * 4];
+#pragma unroll
+        for (int u = 1; u < 4; ++u) best = best2_merge(best, xch[row * 4 + u]);
+        const float qv = qn[gi];
+        // scaled scores are cos * |q|; the screen decides only with a clear 2 delta margin
+        const float dq = kScrDelta * qv;
+        if (!(qv > 0.0f)) {
+          groups[gi] = (uint32_t)tc;  // no positive-norm match (permutation.hpp:246-258)
+        } else if (best.m > -INFINITY && best.s2 < best.m - 2.0f * dq && best.m > -qv + dq) {
+          groups[gi] = (uint32_t)best.j;
+        } else {
+          const int slot = atomicAdd(&L.count[hk], 1);
+          L.rows[lb + slot] = (int32_t)gi;
+          L.best[lb + slot] = best.m;
+        }
+      }
+      ptx::named_bar_sync(1, 32 * kQsEpiWarps);  // xch may be rewritten after this
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
   }
 }
 
@@ -1000,23 +1080,27 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
       centroid_split_kernel<<<(unsigned)(k_heads * tc), 128, 0, st>>>(cent, cn, (int64_t)k_heads * tc, chi, clo,
                                                                        rinv, pen);
       PBS_LAUNCH_CHECK("centroid_split_kernel");
-      const size_t smem = (size_t)2 * 2 * kScrChunk * kScrPad * 2 + (size_t)2 * 2 * kScrChunk * 4;
       static DeviceOnce scr_once;
-      if (int rc = once_per_device(scr_once, [smem] {
+      if (int rc = once_per_device(scr_once, [] {
             PBS_CUDA_CHECK(cudaFuncSetAttribute(query_group_screen_kernel<false>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, QsSmem::total));
             PBS_CUDA_CHECK(cudaFuncSetAttribute(query_group_screen_kernel<true>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, QsSmem::total));
             return (int)PBS_OK;
           }))
         return rc;
       const auto* qb = static_cast<const __nv_bfloat16*>(q);
-      query_group_screen_kernel<false><<<dim3((unsigned)ceil_div(n, kScrRows), (unsigned)hq), 256, smem, st>>>(
-          qb, chi, clo, rinv, pen, qn, kg, n, tc, groups, SL);
+      alignas(64) CUtensorMap tm_q, tm_chi, tm_clo;
+      if (int rc = make_bf16_sw128_map_3d(&tm_q, qb, 128, n, hq, 128, 64, 128)) return rc;
+      if (int rc = make_bf16_sw128_map_3d(&tm_chi, chi, 128, tc, k_heads, kScrPad, 64, 128)) return rc;
+      if (int rc = make_bf16_sw128_map_3d(&tm_clo, clo, 128, tc, k_heads, kScrPad, 64, 128)) return rc;
+      const int grid = num_sms();
+      query_group_screen_kernel<false><<<grid, kQsThreads, QsSmem::total, st>>>(tm_q, tm_chi, tm_clo, qb, rinv, pen,
+                                                                              qn, hq, kg, n, tc, groups, SL);
       PBS_LAUNCH_CHECK("query_group_screen_kernel");
-      // the listed rows (at most every row of a KV group; CTAs past a head's count exit at once)
-      query_group_screen_kernel<true><<<dim3((unsigned)ceil_div((int64_t)kg * n, kScrRows), (unsigned)k_heads), 256,
-                                        smem, st>>>(qb, chi, clo, rinv, pen, qn, kg, n, tc, groups, SL);
+      // the listed rows of every KV head (tile counts read on the device)
+      query_group_screen_kernel<true><<<grid, kQsThreads, QsSmem::total, st>>>(tm_q, tm_chi, tm_clo, qb, rinv, pen,
+                                                                             qn, k_heads, kg, n, tc, groups, SL);
       PBS_LAUNCH_CHECK("query_group_screen_kernel");
       query_group_exact_kernel<<<dim3((unsigned)num_sms() * 4, (unsigned)k_heads), 256, 0, st>>>(qb, cent, qn, cn, kg,
                                                                                              n, tc, SL, groups);

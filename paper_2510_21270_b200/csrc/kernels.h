@@ -34,6 +34,10 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
 int launch_identity(int32_t* perm, int heads, int64_t n, cudaStream_t st);
 // TMA map (a CUtensorMap, 64 bytes) over fp32 [d2][d1][d0] with a [1][box1][box0] box (attn_sm100.cu)
 int make_f32_map_3d(void* map, const float* base, int64_t d0, int64_t d1, int64_t d2, int box0, int box1);
+// bf16 [d2][d1][d0] with rows of `row_elems` (>= d0, 16-byte multiple) and a
+// [1, box1, box0] SW128 box: the tcgen05 K-major operand tiles
+int make_bf16_sw128_map_3d(void* map, const void* base, int64_t d0, int64_t d1, int64_t d2, int64_t row_elems,
+                           int box0, int box1);
 
 // ---- stage 2 (gather.cu) ------------------------------------------------------
 // the un-permute: dst[h][perm[h][i]] = src[h][i] (pipeline.hpp:178-180)
