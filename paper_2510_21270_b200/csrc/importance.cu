@@ -565,46 +565,50 @@ struct ScreenLists {
 };
 
 // K3 screen on the 5th-generation tensor cores.  Persistent CTAs (one per SM)
-// walk tiles of 128 query rows -- rows r0.. of one head (kListed = false:
-// decide or list), or 128 of the rows listed for one KV head (kListed = true:
-// emit candidates) -- and score each tile against every centroid of its KV
-// head in chunks of 128 (N):
-//   S = Q C_hi^T + Q C_lo^T  (16 tcgen05.mma, K = 128 + 128, f32 in TMEM; two
-//   accumulators, so a chunk's MMAs run while the epilogue reads the previous)
-// giving the scaled scores cos * |q| = S * rinv_j + pen_j.  Warp 0 loads (Q
-// tiles double-buffered: one TMA tile, or the listed rows gathered by cp.async
-// into the same SW128 layout; centroid chunks hi + lo by TMA, two stages),
-// warp 1 owns TMEM and issues the MMAs, warps 2-17 read the accumulator: four
-// warps per TMEM lane quadrant, each taking 32 of a chunk's 128 columns, with
-// four independent (best, second best) pairs per thread (first index on ties)
-// merged per row at the end of the tile, or the row's candidates.  Every output
-// element depends only on its own row and column, so both passes compute
-// bit-identical scores for a listed row.
+// walk tiles of 256 query rows (two 128-row sub-tiles) -- rows r0.. of one
+// head (kListed = false: decide or list), or 256 of the rows listed for one KV
+// head (kListed = true: emit candidates) -- and score each against every
+// centroid of its KV head in chunks of 128 (N):
+//   S_u = Q_u C_hi^T + Q_u C_lo^T  (per sub-tile u: 16 tcgen05.mma, K = 128 +
+//   128, f32 in TMEM; two accumulator sets, so a chunk's MMAs run while the
+//   epilogue reads the previous one)
+// giving the scaled scores cos * |q| = S * rinv_j + pen_j.  Both sub-tiles
+// share each centroid chunk: the chunks are the kernel's L2 traffic (a 128-row
+// tile re-reads 512 KB of centroids), which bounded the 128-row version.
+// Warp 0 loads (the Q tile by TMA, or the listed rows gathered by cp.async
+// into the same SW128 layout; centroid chunks hi + lo by TMA, two stages, with
+// their column scales), warp 1 owns TMEM and issues the MMAs, warps 2-17 read
+// the accumulators: four warps per TMEM lane quadrant, each taking 32 of a
+// chunk's 128 columns of both sub-tiles, with four independent (best, second
+// best) pairs per row (first index on ties) merged per row at the end of the
+// tile, or the rows' candidates.  Every output element depends only on its own
+// row and column, so both passes compute bit-identical scores for a listed row.
 constexpr int kQsChunk = 128;  // centroids per chunk (MMA N)
+constexpr int kQsRows = 256;   // query rows per tile (two MMA M = 128 sub-tiles)
 constexpr int kQsEpiWarps = 16;
 constexpr int kQsThreads = 64 + 32 * kQsEpiWarps;
 struct QsSmem {
-  static constexpr int q = 0;                          // [2][128 rows x 128 bf16] (two SW128 panels each)
-  static constexpr int c = 2 * 32768;                  // [stage 0..1][hi, lo] x 32 KB
-  static constexpr int ri = c + 2 * 2 * 32768;         // [2][128] f32: rinv, pen of the chunk in flight
-  static constexpr int xch = ri + 2 * 2 * kQsChunk * 4;  // [128 rows][4] Best2 partials
-  static constexpr int bars = xch + 128 * 4 * 12;
-  static constexpr int total = bars + 256 + 1024;      // + alignment slack
+  static constexpr int q = 0;                             // [sub-tile 0..1][128 rows x 128 bf16] (two SW128 panels each)
+  static constexpr int c = 2 * 32768;                     // [stage 0..1][hi, lo] x 32 KB
+  static constexpr int ri = c + 2 * 2 * 32768;            // [stage][rinv, pen][128] f32
+  static constexpr int xch = ri + 2 * 2 * kQsChunk * 4;   // [256 rows][4] Best2 partials
+  static constexpr int bars = xch + kQsRows * 4 * 12;
+  static constexpr int total = bars + 256 + 1024;         // + alignment slack
 };
 
-// tile index -> (KV head or head, first row); listed: tiles of each KV head's list in turn
+// tile index -> (head, or KV head when listed; first row); listed: each KV head's list in turn
 template <bool kListed>
 __device__ __forceinline__ bool qs_tile(int64_t t, int heads, int64_t n, const int32_t* count, int& h, int64_t& r0) {
   if (!kListed) {
-    const int64_t per = (n + 127) / 128;
+    const int64_t per = (n + kQsRows - 1) / kQsRows;
     h = (int)(t / per);
-    r0 = (t % per) * 128;
+    r0 = (t % per) * kQsRows;
     return h < heads;
   }
   for (h = 0; h < heads; ++h) {
-    const int64_t per = ((int64_t)count[h] + 127) / 128;
+    const int64_t per = ((int64_t)count[h] + kQsRows - 1) / kQsRows;
     if (t < per) {
-      r0 = t * 128;
+      r0 = t * kQsRows;
       return true;
     }
     t -= per;
@@ -619,24 +623,26 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
     const float* __restrict__ pen, const float* __restrict__ qn, int heads, int k_group, int64_t n, int64_t tc,
     uint32_t* __restrict__ groups, ScreenLists L) {
   extern __shared__ __align__(1024) unsigned char qs_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)qs_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned by pointer arithmetic on the shared array (a round trip
+  // through an integer would turn the scale reads below into generic loads)
+  unsigned char* sm = qs_raw + ((1024u - (ptx::smem_u32(qs_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + QsSmem::bars);
-  uint64_t* q_full = bar;        // [2]
-  uint64_t* q_empty = bar + 2;   // [2]
-  uint64_t* c_full = bar + 4;    // [2] centroid stage (and its rinv / pen) loaded
-  uint64_t* c_empty = bar + 6;   // [2] its MMAs complete (and its scales read)
-  uint64_t* s_full = bar + 8;    // [2] accumulator b holds a chunk's scores
-  uint64_t* s_free = bar + 10;   // [2] the epilogue read accumulator b
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* q_full = bar;        // the tile's Q rows loaded
+  uint64_t* q_empty = bar + 1;   // every MMA reading them complete
+  uint64_t* c_full = bar + 2;    // [2] centroid stage (and its scales) loaded
+  uint64_t* c_empty = bar + 4;   // [2] its MMAs complete and its scales read
+  uint64_t* s_full = bar + 6;    // [2] accumulator set b holds a chunk's scores
+  uint64_t* s_free = bar + 8;    // [2] the epilogue read accumulator set b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
   float* sri = reinterpret_cast<float*>(sm + QsSmem::ri);
   Best2* xch = reinterpret_cast<Best2*>(sm + QsSmem::xch);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nchunks = (int)((tc + kQsChunk - 1) / kQsChunk);
   if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
     for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&q_full[b], 1);
-      ptx::mbar_init(&q_empty[b], 1);
-      ptx::mbar_init(&c_full[b], 2);  // the TMA (expect_tx) + the scales (lanes' writes, one arrival)
+      ptx::mbar_init(&c_full[b], 2);                 // the TMA (expect_tx) + the scales
       ptx::mbar_init(&c_empty[b], 1 + kQsEpiWarps);  // MMA commit + every epilogue warp past the scales
       ptx::mbar_init(&s_full[b], 1);
       ptx::mbar_init(&s_free[b], kQsEpiWarps);
@@ -644,29 +650,28 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
     ptx::fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(ptx::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(ptx::smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int k_heads = heads / (kListed ? 1 : k_group);
-  (void)k_heads;
   if (warp == 0) {
-    // ---- loads: per tile Q, then the centroid chunks
+    // ---- loads: per tile Q, then the centroid chunks (the chunk stages run ahead of Q)
     uint32_t it = 0, cit = 0;
     int h;
     int64_t r0;
     for (int64_t t = blockIdx.x; qs_tile<kListed>(t, heads, n, L.count, h, r0); t += gridDim.x, ++it) {
       const int hk = kListed ? h : h / k_group;
-      const int qb = it & 1;
-      ptx::mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
-      unsigned char* qd = sm + QsSmem::q + qb * 32768;
+      ptx::mbar_wait(q_empty, (it & 1) ^ 1);
       if (!kListed) {
         if (lane == 0) {
-          ptx::mbar_expect_tx(&q_full[qb], 32768);
-          for (int p = 0; p < 2; ++p) tc::tma_load_3d(qd + p * 16384, &tm_q, &q_full[qb], p * 64, (int)r0, h);
+          ptx::mbar_expect_tx(q_full, 65536);  // rows past n zero-filled
+          for (int u = 0; u < 2; ++u)
+            for (int p = 0; p < 2; ++p)
+              tc::tma_load_3d(sm + QsSmem::q + u * 32768 + p * 16384, &tm_q, q_full, p * 64,
+                              (int)(r0 + u * 128), h);
         }
       } else {
         // the listed rows (global row h * n + i) gathered into the SW128 K-major
@@ -674,26 +679,29 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
         // rr * 128 + ((cc % 8) ^ (rr % 8)) * 16; half a warp per 256-byte row
         const int64_t nrows = L.count[h];
         const int64_t lb = (int64_t)h * k_group * n;
-        int src[4];
-#pragma unroll
-        for (int jr = 0; jr < 4; ++jr) src[jr] = L.rows[lb + min64(r0 + 32 * jr + lane, nrows - 1)];
         const int hb = lane >> 4, cc = lane & 15, c8 = cc & 7;
-        const uint32_t base = ptx::smem_u32(qd) + (uint32_t)(cc >> 3) * 16384u;
+        for (int u = 0; u < 2; ++u) {
+          int src[4];
 #pragma unroll
-        for (int jr = 0; jr < 4; ++jr)
+          for (int jr = 0; jr < 4; ++jr) src[jr] = L.rows[lb + min64(r0 + u * 128 + 32 * jr + lane, nrows - 1)];
+          const uint32_t base = ptx::smem_u32(sm + QsSmem::q + u * 32768) + (uint32_t)(cc >> 3) * 16384u;
+#pragma unroll
+          for (int jr = 0; jr < 4; ++jr)
 #pragma unroll 4
-          for (int i = 0; i < 16; ++i) {
-            const int rr = 32 * jr + 2 * i + hb;
-            const int gi = __shfl_sync(0xffffffffu, src[jr], (2 * i + hb) & 31);
-            const uint32_t dst = base + (uint32_t)rr * 128u + ((uint32_t)(c8 ^ (rr & 7)) << 4);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(q + (int64_t)gi * 128 + cc * 8)
-                         : "memory");
-          }
+            for (int i = 0; i < 16; ++i) {
+              const int rr = 32 * jr + 2 * i + hb;
+              const int gi = __shfl_sync(0xffffffffu, src[jr], (2 * i + hb) & 31);
+              const uint32_t dst = base + (uint32_t)rr * 128u + ((uint32_t)(c8 ^ (rr & 7)) << 4);
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                           "l"(q + (int64_t)gi * 128 + cc * 8)
+                           : "memory");
+            }
+        }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the MMA's operand reads
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&q_full[qb]);
+        if (lane == 0) ptx::mbar_arrive(q_full);
       }
       for (int c = 0; c < nchunks; ++c, ++cit) {
         const int st = cit & 1;
@@ -719,29 +727,32 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
   } else if (warp == 1) {
     // ---- MMA issuer
     const uint32_t idesc = tc::idesc_bf16(kQsChunk);
+    const uint64_t qdesc0 = tc::sdesc_sw128(ptx::smem_u32(sm + QsSmem::q));
+    const uint64_t qdesc1 = tc::sdesc_sw128(ptx::smem_u32(sm + QsSmem::q + 32768));
     uint32_t it = 0, cit = 0;
     int h;
     int64_t r0;
     for (int64_t t = blockIdx.x; qs_tile<kListed>(t, heads, n, L.count, h, r0); t += gridDim.x, ++it) {
-      const int qb = it & 1;
-      ptx::mbar_wait(&q_full[qb], (it >> 1) & 1);
-      const uint64_t qdesc = tc::sdesc_sw128(ptx::smem_u32(sm + QsSmem::q + qb * 32768));
+      ptx::mbar_wait(q_full, it & 1);
       for (int c = 0; c < nchunks; ++c, ++cit) {
         const int st = cit & 1, b = cit & 1;
         ptx::mbar_wait(&c_full[st], (cit >> 1) & 1);
         ptx::mbar_wait(&s_free[b], ((cit >> 1) & 1) ^ 1);
         tc::fence_after();
         const uint32_t cb = ptx::smem_u32(sm + QsSmem::c + st * 65536);
-        tc::mma_k128(tmem + b * kQsChunk, qdesc, tc::sdesc_sw128(cb), idesc, false);        // Q C_hi^T
-        tc::mma_k128(tmem + b * kQsChunk, qdesc, tc::sdesc_sw128(cb + 32768), idesc, true);  // + Q C_lo^T
+        const uint32_t acc = tmem + b * 2 * kQsChunk;
+        tc::mma_k128(acc, qdesc0, tc::sdesc_sw128(cb), idesc, false);                      // Q_0 C_hi^T
+        tc::mma_k128(acc, qdesc0, tc::sdesc_sw128(cb + 32768), idesc, true);               // + Q_0 C_lo^T
+        tc::mma_k128(acc + kQsChunk, qdesc1, tc::sdesc_sw128(cb), idesc, false);           // Q_1 C_hi^T
+        tc::mma_k128(acc + kQsChunk, qdesc1, tc::sdesc_sw128(cb + 32768), idesc, true);    // + Q_1 C_lo^T
         tc::commit(&c_empty[st]);
         tc::commit(&s_full[b]);
       }
-      tc::commit(&q_empty[qb]);  // every MMA reading this Q tile issued
+      tc::commit(q_empty);  // every MMA reading this Q tile issued
     }
   } else {
-    // ---- epilogue: warp e reads TMEM lane quadrant e % 4 (rows 32 (e % 4)..)
-    // and columns 32 (e / 4).. of each chunk
+    // ---- epilogue: warp e reads TMEM lane quadrant e % 4 (rows 32 (e % 4).. of
+    // both sub-tiles) and columns 32 (e / 4).. of each chunk
     const int e = warp - 2, quad = warp & 3, cq = e >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
@@ -752,62 +763,77 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
       const int hk = kListed ? h : h / k_group;
       const int64_t lb = (int64_t)hk * k_group * n;
       const int64_t nrows = kListed ? (int64_t)L.count[h] : n;
-      const int64_t r = r0 + row;
-      const bool valid = r < nrows;
-      const int64_t rc = min64(r, nrows - 1);
-      const int64_t gi = kListed ? (int64_t)L.rows[lb + rc] : (int64_t)h * n + rc;
-      float thr = 0.0f;
-      if (kListed) thr = L.best[lb + rc] - 2.0f * kScrDelta * qn[gi];
-      // four independent running (best, second) pairs over j % 4 (a dependent
-      // compare chain per element would serialise the epilogue), merged with the
-      // first index on ties -- the same pair a j-ascending scan produces
-      Best2 bp[4];
+      bool valid[2];
+      int64_t rc[2], gi[2];
+      float thr[2] = {0.0f, 0.0f};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) bp[u] = Best2{-INFINITY, -INFINITY, 0};
+      for (int u = 0; u < 2; ++u) {
+        const int64_t r = r0 + u * 128 + row;
+        valid[u] = r < nrows;
+        rc[u] = min64(r, nrows - 1);
+        gi[u] = kListed ? (int64_t)L.rows[lb + rc[u]] : (int64_t)h * n + rc[u];
+        if (kListed) thr[u] = L.best[lb + rc[u]] - 2.0f * kScrDelta * qn[gi[u]];
+      }
+      // four independent running (best, second) pairs per row over j % 4 (a
+      // dependent compare chain per element would serialise the epilogue),
+      // merged with the first index on ties -- the pair a j-ascending scan gives
+      Best2 bp[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) bp[u][x] = Best2{-INFINITY, -INFINITY, 0};
       for (int c = 0; c < nchunks; ++c, ++cit) {
         const int st = cit & 1, b = cit & 1;
         ptx::mbar_wait(&s_full[b], (cit >> 1) & 1);
-        ptx::mbar_wait(&c_full[st], (cit >> 1) & 1);  // the scales (already complete: the MMAs waited on it)
+        ptx::mbar_wait(&c_full[st], (cit >> 1) & 1);  // the scales (complete: the MMAs waited on it)
         tc::fence_after();
-        uint32_t v[32];
-        PBS_TC_LD32(tmem + lane_off + (uint32_t)(b * kQsChunk + cq * 32), v);
-        tc::wait_ld();
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&s_free[b]);
         const float* scl = sri + st * 2 * kQsChunk + cq * 32;
         const int j0 = c * kQsChunk + cq * 32;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const float x = fmaf(__uint_as_float(v[jj]), scl[jj], scl[kQsChunk + jj]);  // padding: pen -inf
-          if (!kListed) {
-            best2_push(bp[jj & 3], x, j0 + jj);
-          } else if (x >= thr && j0 + jj < tc) {
-            const int slot = atomicAdd(&L.cand_n[lb + rc], valid ? 1 : 0);
-            if (valid && slot < kScrCand) L.cand[(lb + rc) * kScrCand + slot] = j0 + jj;
+        for (int u = 0; u < 2; ++u) {  // one sub-tile at a time: 32 scores live per thread
+          uint32_t v[32];
+          PBS_TC_LD32(tmem + lane_off + (uint32_t)(b * 2 * kQsChunk + u * kQsChunk + cq * 32), v);
+          tc::wait_ld();
+          if (u == 1) {  // both sub-tiles' scores are in registers: the accumulator set may be rewritten
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&s_free[b]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const float x = fmaf(__uint_as_float(v[jj]), scl[jj], scl[kQsChunk + jj]);  // padding: pen -inf
+            if (!kListed) {
+              best2_push(bp[u][jj & 3], x, j0 + jj);
+            } else if (x >= thr[u] && valid[u] && j0 + jj < tc) {
+              const int slot = atomicAdd(&L.cand_n[lb + rc[u]], 1);
+              if (slot < kScrCand) L.cand[(lb + rc[u]) * kScrCand + slot] = j0 + jj;
+            }
           }
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&c_empty[st]);  // the scales of this stage read
       }
       if (kListed) continue;
-      // the row's four column groups (warps e % 4 == quad) merged in shared memory
-      xch[row * 4 + cq] = best2_merge(best2_merge(bp[0], bp[1]), best2_merge(bp[2], bp[3]));
-      ptx::named_bar_sync(1, 32 * kQsEpiWarps);
-      if (cq == 0 && valid) {
-        Best2 best = xch[row * 4];
+      // each row's four column groups (the warps of its quadrant) merged in shared memory
 #pragma unroll
-        for (int u = 1; u < 4; ++u) best = best2_merge(best, xch[row * 4 + u]);
-        const float qv = qn[gi];
+      for (int u = 0; u < 2; ++u)
+        xch[(u * 128 + row) * 4 + cq] = best2_merge(best2_merge(bp[u][0], bp[u][1]), best2_merge(bp[u][2], bp[u][3]));
+      ptx::named_bar_sync(1, 32 * kQsEpiWarps);
+      if (cq < 2 && valid[cq]) {  // warps cq = 0 / 1 decide the rows of sub-tile 0 / 1
+        const int u = cq;
+        Best2 best = xch[(u * 128 + row) * 4];
+#pragma unroll
+        for (int x = 1; x < 4; ++x) best = best2_merge(best, xch[(u * 128 + row) * 4 + x]);
+        const float qv = qn[gi[u]];
         // scaled scores are cos * |q|; the screen decides only with a clear 2 delta margin
         const float dq = kScrDelta * qv;
         if (!(qv > 0.0f)) {
-          groups[gi] = (uint32_t)tc;  // no positive-norm match (permutation.hpp:246-258)
+          groups[gi[u]] = (uint32_t)tc;  // no positive-norm match (permutation.hpp:246-258)
         } else if (best.m > -INFINITY && best.s2 < best.m - 2.0f * dq && best.m > -qv + dq) {
-          groups[gi] = (uint32_t)best.j;
+          groups[gi[u]] = (uint32_t)best.j;
         } else {
           const int slot = atomicAdd(&L.count[hk], 1);
-          L.rows[lb + slot] = (int32_t)gi;
+          L.rows[lb + slot] = (int32_t)gi[u];
           L.best[lb + slot] = best.m;
         }
       }
@@ -818,7 +844,7 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
