@@ -499,8 +499,8 @@ __global__ void query_group_finalize_kernel(const unsigned long long* __restrict
 
 // ---- K3 screen (bf16, d = 128): tensor-core cosine screen + exact re-check ----
 // The assignment only needs each query's argmax.  The centroids (f32) are split
-// into bf16 hi + lo parts, so q . (c_hi + c_lo) on the tensor cores (mma.sync
-// m16n8k16, f32 accumulation) is within 4.3e-5 |q||c| of the reference's
+// into bf16 hi + lo parts, so q . (c_hi + c_lo) on the tensor cores (tcgen05,
+// f32 accumulation in TMEM) is within 4.3e-5 |q||c| of the reference's
 // sequential f32 dot (split residual 2^-18, accumulation 256 x 2^-23, the
 // reference's own rounding 128 x 2^-24).  With delta = 1e-4 (2.3x that bound):
 //  1. screen: a row whose best screened cosine beats every other centroid by
@@ -512,7 +512,7 @@ __global__ void query_group_finalize_kernel(const unsigned long long* __restrict
 //     (sequential c, rounded products, IEEE division), argmax with the first
 //     index on ties; a row with more than kScrCand candidates scans every
 //     centroid exactly.
-constexpr int kScrPad = 136;               // bf16 per padded centroid row (272 B: conflict-free fragment loads)
+constexpr int kScrPad = 136;               // bf16 per padded centroid row (272 B; the TMA box reads the first 128)
 constexpr int kScrCand = 16;               // candidates kept per listed row
 constexpr float kScrDelta = 1e-4f;
 
