@@ -516,11 +516,21 @@ constexpr int kScrPad = 136;               // bf16 per padded centroid row (272 
 constexpr int kScrCand = 16;               // candidates kept per listed row
 constexpr float kScrDelta = 1e-4f;
 
-__global__ void centroid_split_kernel(const float* __restrict__ cent, const float* __restrict__ cn, int64_t rows,
-                                      __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
+// grid (tcp, k_heads): centroid j of KV head blockIdx.y; the column scales are
+// padded to tcp (a multiple of the screen's 128-centroid chunk) with rinv 0 and
+// pen -inf, so every chunk's scales are one aligned 512-byte bulk copy
+__global__ void centroid_split_kernel(const float* __restrict__ cent, const float* __restrict__ cn, int64_t tc,
+                                      int64_t tcp, __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
                                       float* __restrict__ rinv, float* __restrict__ pen) {
-  const int64_t r = blockIdx.x;
-  if (r >= rows) return;
+  const int64_t j = blockIdx.x;
+  if (j >= tc) {
+    if (threadIdx.x == 0) {
+      rinv[blockIdx.y * tcp + j] = 0.0f;
+      pen[blockIdx.y * tcp + j] = -INFINITY;
+    }
+    return;
+  }
+  const int64_t r = blockIdx.y * tc + j;
   for (int c = threadIdx.x; c < kScrPad; c += blockDim.x) {
     const float x = c < 128 ? cent[r * 128 + c] : 0.0f;
     const __nv_bfloat16 h = __float2bfloat16_rn(x);
@@ -529,8 +539,8 @@ __global__ void centroid_split_kernel(const float* __restrict__ cent, const floa
   }
   if (threadIdx.x == 0) {
     const float v = cn[r];
-    rinv[r] = v > 0.0f ? 1.0f / v : 0.0f;
-    pen[r] = v > 0.0f ? 0.0f : -INFINITY;
+    rinv[blockIdx.y * tcp + j] = v > 0.0f ? 1.0f / v : 0.0f;
+    pen[blockIdx.y * tcp + j] = v > 0.0f ? 0.0f : -INFINITY;
   }
 }
 
@@ -621,7 +631,7 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_chi,
     const __grid_constant__ CUtensorMap tm_clo, const __nv_bfloat16* __restrict__ q, const float* __restrict__ rinv,
     const float* __restrict__ pen, const float* __restrict__ qn, int heads, int k_group, int64_t n, int64_t tc,
-    uint32_t* __restrict__ groups, ScreenLists L) {
+    int64_t tcp, uint32_t* __restrict__ groups, ScreenLists L) {
   extern __shared__ __align__(1024) unsigned char qs_raw[];
   // 1024-byte aligned by pointer arithmetic on the shared array (a round trip
   // through an integer would turn the scale reads below into generic loads)
@@ -642,7 +652,7 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
     for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&c_full[b], 2);                 // the TMA (expect_tx) + the scales
+      ptx::mbar_init(&c_full[b], 1);                 // TMA tiles + scales (expect_tx)
       ptx::mbar_init(&c_empty[b], 1 + kQsEpiWarps);  // MMA commit + every epilogue warp past the scales
       ptx::mbar_init(&s_full[b], 1);
       ptx::mbar_init(&s_free[b], kQsEpiWarps);
@@ -707,21 +717,18 @@ __global__ void __launch_bounds__(kQsThreads, 1) query_group_screen_kernel(
         const int st = cit & 1;
         ptx::mbar_wait(&c_empty[st], ((cit >> 1) & 1) ^ 1);
         if (lane == 0) {
-          ptx::mbar_expect_tx(&c_full[st], 65536);  // centroids past tc zero-filled
+          // centroids past tc zero-filled; the chunk's column scales (padded:
+          // rinv 0, pen -inf past tc, never a winner) by two bulk copies
+          ptx::mbar_expect_tx(&c_full[st], 65536 + 2 * kQsChunk * 4);
           unsigned char* dst = sm + QsSmem::c + st * 65536;
           for (int p = 0; p < 2; ++p) {
             tc::tma_load_3d(dst + p * 16384, &tm_chi, &c_full[st], p * 64, c * kQsChunk, hk);
             tc::tma_load_3d(dst + 32768 + p * 16384, &tm_clo, &c_full[st], p * 64, c * kQsChunk, hk);
           }
+          const int64_t j0 = (int64_t)hk * tcp + (int64_t)c * kQsChunk;
+          tc::bulk_load(sri + st * 2 * kQsChunk, rinv + j0, kQsChunk * 4, &c_full[st]);
+          tc::bulk_load(sri + st * 2 * kQsChunk + kQsChunk, pen + j0, kQsChunk * 4, &c_full[st]);
         }
-        // the chunk's column scales (padding columns: pen -inf, never a winner)
-        for (int x = lane; x < kQsChunk; x += 32) {
-          const int64_t j = (int64_t)c * kQsChunk + x;
-          sri[st * 2 * kQsChunk + x] = j < tc ? __ldg(rinv + (int64_t)hk * tc + j) : 0.0f;
-          sri[st * 2 * kQsChunk + kQsChunk + x] = j < tc ? __ldg(pen + (int64_t)hk * tc + j) : -INFINITY;
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&c_full[st]);
       }
     }
   } else if (warp == 1) {
@@ -1056,7 +1063,8 @@ size_t query_perm_workspace_bytes(int hq, int64_t n, int d, int64_t block) {
   // centroids, their norms, |q|, the per-query best keys (exact path) or the
   // fallback list (screen path), then the screen's split centroids and scales
   return (size_t)hq * tc * d * 4 + (size_t)hq * tc * 4 + (size_t)hq * n * 4 + (size_t)hq * n * 8 +
-         (size_t)hq * n * 4 * (kScrCand + 2) + (size_t)hq * tc * (kScrPad * 4 + 8) + 4096;
+         (size_t)hq * n * 4 * (kScrCand + 2) + (size_t)hq * tc * kScrPad * 4 +
+         (size_t)hq * (tc + 128) * 8 + 4096;
 }
 
 int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_heads, int64_t n, int d,
@@ -1099,12 +1107,14 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
       p2 = reinterpret_cast<char*>(((uintptr_t)p2 + 255) & ~(uintptr_t)255);
       __nv_bfloat16* chi = reinterpret_cast<__nv_bfloat16*>(p2);
       __nv_bfloat16* clo = chi + (size_t)k_heads * tc * kScrPad;
-      float* rinv = reinterpret_cast<float*>(clo + (size_t)k_heads * tc * kScrPad);
-      float* pen = rinv + (size_t)k_heads * tc;
+      const int64_t tcp = (tc + kQsChunk - 1) / kQsChunk * kQsChunk;
+      float* rinv = reinterpret_cast<float*>(
+          ((uintptr_t)(clo + (size_t)k_heads * tc * kScrPad) + 15) & ~(uintptr_t)15);
+      float* pen = rinv + (size_t)k_heads * tcp;
       PBS_CUDA_CHECK(cudaMemsetAsync(SL.count, 0, sizeof(int32_t) * k_heads, st));
       PBS_CUDA_CHECK(cudaMemsetAsync(SL.cand_n, 0, sizeof(int32_t) * hq * n, st));
-      centroid_split_kernel<<<(unsigned)(k_heads * tc), 128, 0, st>>>(cent, cn, (int64_t)k_heads * tc, chi, clo,
-                                                                       rinv, pen);
+      centroid_split_kernel<<<dim3((unsigned)tcp, (unsigned)k_heads), 128, 0, st>>>(cent, cn, tc, tcp, chi, clo,
+                                                                                   rinv, pen);
       PBS_LAUNCH_CHECK("centroid_split_kernel");
       static DeviceOnce scr_once;
       if (int rc = once_per_device(scr_once, [] {
@@ -1122,11 +1132,11 @@ int launch_query_groups(const void* q, const void* k, int dtype, int hq, int k_h
       if (int rc = make_bf16_sw128_map_3d(&tm_clo, clo, 128, tc, k_heads, kScrPad, 64, 128)) return rc;
       const int grid = num_sms();
       query_group_screen_kernel<false><<<grid, kQsThreads, QsSmem::total, st>>>(tm_q, tm_chi, tm_clo, qb, rinv, pen,
-                                                                              qn, hq, kg, n, tc, groups, SL);
+                                                                              qn, hq, kg, n, tc, tcp, groups, SL);
       PBS_LAUNCH_CHECK("query_group_screen_kernel");
       // the listed rows of every KV head (tile counts read on the device)
       query_group_screen_kernel<true><<<grid, kQsThreads, QsSmem::total, st>>>(tm_q, tm_chi, tm_clo, qb, rinv, pen,
-                                                                             qn, k_heads, kg, n, tc, groups, SL);
+                                                                             qn, k_heads, kg, n, tc, tcp, groups, SL);
       PBS_LAUNCH_CHECK("query_group_screen_kernel");
       query_group_exact_kernel<<<dim3((unsigned)num_sms() * 4, (unsigned)k_heads), 256, 0, st>>>(qb, cent, qn, cn, kg,
                                                                                              n, tc, SL, groups);
