@@ -11,8 +11,10 @@
 // (under B = 128, S = 256 the two blocks of one segment).  The CTA streams the
 // union of the two tiles' visited key blocks once through shared memory and
 // each K/V tile feeds both query tiles, so the K/V bytes moved per tensor-core
-// FLOP halve against one tile per item (the L2 -> SM traffic was the MMA
-// warp's main wait).  Persistent CTAs (one per SM) take items from a global
+// FLOP halve against one tile per item, and the two tiles' softmax phases
+// interleave on each SM sub-partition (one tile's exponentials run while the
+// other's scores load; DESIGN.md §4 has the chain this sets and the
+// alternatives measured).  Persistent CTAs (one per SM) take items from a global
 // counter (warp 3 publishes them through an mbarrier ring), ordered one KV
 // source at a time for L2 locality, heaviest pairs first.
 // Warp roles (384 threads; setmaxnreg gives the softmax 208 registers):
